@@ -1,0 +1,140 @@
+/*
+ * rdkv.h — C ABI of librdkv, the B200-native Shared RAG-DCache hot path.
+ *
+ * The reference (`ragdcache`, /root/reference/pkg/src/ragdcache) is a pure-Python
+ * package; its "FFI" for this path is the set of in-process Python calls listed
+ * beside each entry point below.  The Python package `paper_2504_11765_b200`
+ * binds these symbols with ctypes (GIL released during every call) and keeps the
+ * reference's Python interfaces on top; INTEGRATION.md shows the binding a
+ * maintainer would add to the reference itself.
+ *
+ * Conventions
+ *   - Every status-returning function returns int32: 0 = ok, < 0 = error whose
+ *     class maps 1:1 onto the reference exception hierarchy (see RDKV_ERR_*).
+ *     rdkv_last_error() returns a thread-local message for the last failure.
+ *   - No allocation on hot calls: device / pinned buffers are owned by the caller
+ *     (PyTorch) and passed as plain pointers; `stream` is a cudaStream_t.
+ *   - GPU calls are asynchronous on `stream` and reentrant per stream.
+ */
+#ifndef RDKV_H
+#define RDKV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RDKV_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define RDKV_API __attribute__((visibility("default")))
+#else
+#define RDKV_API
+#endif
+
+/* ----------------------------------------------------------------- status */
+#define RDKV_OK 0
+#define RDKV_ERR_BAD_MAGIC (-1)          /* codec.BadMagicError          codec.py:44  */
+#define RDKV_ERR_UNSUPPORTED_VERSION (-2) /* codec.UnsupportedVersionError codec.py:48 */
+#define RDKV_ERR_TRUNCATED (-3)          /* codec.TruncatedError         codec.py:52  */
+#define RDKV_ERR_CHECKSUM (-4)           /* codec.ChecksumMismatchError  codec.py:56  */
+#define RDKV_ERR_MALFORMED (-5)          /* codec.MalformedHeaderError   codec.py:60  */
+#define RDKV_ERR_IO (-6)                 /* OSError on the store path    store.py:219, 268 */
+#define RDKV_ERR_ARG (-7)                /* ValueError                                */
+#define RDKV_ERR_CUDA (-8)               /* device failure (no reference analogue)    */
+
+RDKV_API int rdkv_abi_version(void);
+RDKV_API const char* rdkv_last_error(void);
+
+/* ------------------------------------------------------- L0: blob codec (H1) */
+
+/* 64-bit FNV-1a over `len` bytes starting from `seed` (pass 0xCBF29CE484222325
+ * for the standard offset).  Replaces codec.fnv1a64 (codec.py:64-69). */
+RDKV_API uint64_t rdkv_fnv1a64(const void* data, size_t len, uint64_t seed);
+
+/* FNV-1a of n independent buffers on up to `threads` host threads (one serial
+ * chain per buffer — the checksum itself cannot be split).  Used to hash the
+ * k prefix blobs of one combination concurrently (prefetch.py:146-152). */
+RDKV_API void rdkv_fnv1a64_many(const void* const* bufs, const size_t* lens, size_t n, uint64_t* out,
+                       int threads);
+
+/* Fixed-width view of the .rdkv header (codec.py:8-13, 35-36, 110-137). */
+typedef struct rdkv_header {
+  uint64_t model_hash;
+  uint64_t payload_len;
+  uint64_t checksum;
+  uint32_t token_count;
+  uint16_t version;
+  uint16_t doc_count;
+  uint16_t layers;
+  uint16_t kv_heads;
+  uint16_t head_dim;
+  uint8_t elem_width;
+  uint8_t reserved_pad[3];
+} rdkv_header;
+
+/* Bytes of the encoded header for `doc_count` doc ids: 46 + 8*doc_count
+ * (codec.header_size, codec.py:159-160). */
+RDKV_API size_t rdkv_header_size(uint32_t doc_count);
+
+/* Serialise a header (magic/version are written by the library) followed by
+ * the doc ids into `out` (capacity `cap`).  codec.encode, header part
+ * (codec.py:227-239).  Returns the number of bytes written or < 0. */
+RDKV_API int64_t rdkv_header_encode(const rdkv_header* h, const uint64_t* doc_ids, void* out, size_t cap);
+
+/* Parse and validate a header from the front of `data`; the doc ids are copied
+ * into `doc_ids` (capacity `ids_cap`).  Same checks and error classes as
+ * codec.decode_header (codec.py:242-279). */
+RDKV_API int rdkv_header_decode(const void* data, size_t len, rdkv_header* h, uint64_t* doc_ids,
+                       size_t ids_cap, size_t* header_len);
+
+/* Full decode check of an encoded blob: header, truncation, trailing bytes and
+ * the payload FNV-1a (codec.decode, codec.py:282-295). */
+RDKV_API int rdkv_blob_check(const void* data, size_t len, rdkv_header* h, uint64_t* doc_ids,
+                    size_t ids_cap, size_t* payload_off);
+
+/* ------------------------------------------------ L1: blob file I/O (H2) */
+
+/* Durable write: header + payload to `tmp_path`, then rename onto `final_path`
+ * so readers never observe a partial blob (KvStore.put, store.py:215-223). */
+RDKV_API int rdkv_blob_write(const char* tmp_path, const char* final_path, const void* header,
+                    size_t header_len, const void* payload, size_t payload_len);
+
+/* Size of a file in bytes, or < 0 (RDKV_ERR_IO). */
+RDKV_API int64_t rdkv_file_size(const char* path);
+
+/* Read a whole blob file into `buf` (capacity `cap`, normally pinned host
+ * memory) placing the payload at an `align`-byte boundary (payload offset in
+ * the file is 46+8k, never aligned).  With verify != 0 it runs the same
+ * validation as rdkv_blob_check (KvStore.get disk path: store.py:266-267).
+ * On success *file_off is where the file's first byte landed in `buf` and
+ * *payload_off where the payload starts. */
+RDKV_API int rdkv_blob_read(const char* path, void* buf, size_t cap, size_t align, int verify,
+                   rdkv_header* h, uint64_t* doc_ids, size_t ids_cap, size_t* file_off,
+                   size_t* payload_off);
+
+/* Drop a file's pages from the OS page cache (cold-read benchmarking). */
+RDKV_API int rdkv_drop_page_cache(const char* path);
+
+/* ------------------------------------------------------- K1: tcgen05 GEMM */
+
+/* Epilogue selectors for rdkv_gemm_bf16. */
+#define RDKV_EPI_STORE 0     /* D = A.B^T (bf16)                         */
+#define RDKV_EPI_STORE_F32 1 /* D = A.B^T (fp32)                         */
+#define RDKV_EPI_RESID 2     /* D = R + A.B^T (bf16)                     */
+#define RDKV_EPI_SWIGLU 3    /* D = silu(gate) * up, [gate|up] blocks of 64 */
+
+/* D[M,N] = A[M,K] . B[N,K]^T on the tcgen05 tensor cores (bf16 in, fp32
+ * accumulate).  Building block of the document / query prefill; exposed for
+ * tests and for callers that bring their own layers.  No reference analogue:
+ * the reference models this work as prefill_work (costs.py:82-86). */
+RDKV_API int rdkv_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* D, int64_t ldd,
+                   const void* R, int64_t ldr, int M, int N, int K, int epilogue, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RDKV_H */

@@ -1,0 +1,332 @@
+// K1 implementation: see gemm_tc.cuh for the design summary.
+#include <cudaTypedefs.h>
+#include <cstdio>
+#include <mutex>
+#include "common.cuh"
+#include "gemm_tc.cuh"
+
+namespace rdkv {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr uint32_t A_BYTES = BM * BK * 2;
+  static constexpr uint32_t B_BYTES = BN * BK * 2;
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr uint32_t TMEM_COLS = 2 * BN;  // double-buffered accumulator
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
+};
+
+__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+
+// Store 32 consecutive bf16 values (packed in 16 words) with 16-byte stores.
+__device__ __forceinline__ void st_bf16x32(__nv_bfloat16* dst, const uint32_t (&w)[16]) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) d[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+}
+
+template <int BN, int EPI, int DH>
+__global__ void __launch_bounds__(256, 1)
+    gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        int M, int N, int K, GemmEpi ep) {
+  using C = GemmCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int m_tiles = (M + BM - 1) / BM;
+  const int n_tiles = (N + BN - 1) / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int kblocks = K / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      const uint64_t pol_act = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int mb = t % m_tiles, nb = t / m_tiles;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          tma_load_2d(&tmA, &full[stage], sA + stage * C::A_BYTES, kb * BK, mb * BM, pol_act);
+          tma_load_2d_nohint(&tmB, &full[stage], sB + stage * C::B_BYTES, kb * BK, nb * BN);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (single thread)
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ad = sdesc_k_sw128(smem_u32(sA + stage * C::A_BYTES));
+          const uint64_t bd = sdesc_k_sw128(smem_u32(sB + stage * C::B_BYTES));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+          umma_commit(&empty[stage]);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM -> registers -> fused op -> global
+    const int wq = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int mb = t % m_tiles, nb = t / m_tiles;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * BM + wq * 32 + lane;
+      const bool row_ok = row < M;
+      const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(wq * 32) << 16);
+
+      if constexpr (EPI == EPI_STORE || EPI == EPI_STORE_F32 || EPI == EPI_RESID) {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c * 32, r);
+          tmem_ld_wait();
+          const int col = nb * BN + c * 32;
+          if (row_ok && col < N) {
+            if constexpr (EPI == EPI_STORE_F32) {
+              float4* dst = reinterpret_cast<float4*>(static_cast<float*>(ep.out) + (long long)row * ep.ldo + col);
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                dst[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                                     __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+            } else {
+              uint32_t w[16];
+              if constexpr (EPI == EPI_RESID) {
+                const uint4* src = reinterpret_cast<const uint4*>(ep.resid + (long long)row * ep.ldr + col);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const uint4 u = src[i];
+                  const uint32_t uu[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) {
+                    const float2 f = unpack_bf16(uu[j]);
+                    const int e = 8 * i + 2 * j;
+                    w[4 * i + j] = pack_bf16(f.x + __uint_as_float(r[e]), f.y + __uint_as_float(r[e + 1]));
+                  }
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) w[i] = pack_bf16(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+              }
+              st_bf16x32(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + col, w);
+            }
+          }
+        }
+      } else if constexpr (EPI == EPI_SWIGLU) {
+        constexpr int HALF = BN / 2;
+#pragma unroll 1
+        for (int c = 0; c < HALF / 32; ++c) {
+          uint32_t g[32], u[32];
+          tmem_ld32(taddr + c * 32, g);
+          tmem_ld32(taddr + HALF + c * 32, u);
+          tmem_ld_wait();
+          const int col = nb * HALF + c * 32;  // output column
+          if (row_ok && col < N / 2) {
+            uint32_t w[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float a0 = silu(__uint_as_float(g[2 * i])) * __uint_as_float(u[2 * i]);
+              const float a1 = silu(__uint_as_float(g[2 * i + 1])) * __uint_as_float(u[2 * i + 1]);
+              w[i] = pack_bf16(a0, a1);
+            }
+            st_bf16x32(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + col, w);
+          }
+        }
+      } else if constexpr (EPI == EPI_QKV) {
+        static_assert(BN % DH == 0, "tile must hold whole heads");
+        const int p = row_ok ? ep.pos[row] : 0;
+        const int sl = row_ok ? ep.slot[row] : 0;
+#pragma unroll 1
+        for (int hh = 0; hh < BN / DH; ++hh) {
+          float v[DH];
+#pragma unroll
+          for (int c = 0; c < DH / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld32(taddr + hh * DH + c * 32, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[c * 32 + i] = __uint_as_float(r[i]);
+          }
+          const int g = (nb * BN + hh * DH) / DH;  // global head index in [q | k | v]
+          if (!row_ok || g >= ep.hq + 2 * ep.hkv) continue;
+          if (g < ep.hq + ep.hkv) {
+            // rotate-half RoPE: pairs (i, i + DH/2)
+            const float2* cs = reinterpret_cast<const float2*>(ep.rope) + (long long)p * (DH / 2);
+#pragma unroll
+            for (int i = 0; i < DH / 2; ++i) {
+              const float2 t = cs[i];
+              const float x1 = v[i], x2 = v[i + DH / 2];
+              v[i] = x1 * t.x - x2 * t.y;
+              v[i + DH / 2] = x2 * t.x + x1 * t.y;
+            }
+          }
+          __nv_bfloat16* dst;
+          if (g < ep.hq)
+            dst = ep.q + (long long)row * ep.ldq + (long long)g * DH;
+          else if (g < ep.hq + ep.hkv)
+            dst = ep.kplane + (long long)(g - ep.hq) * ep.head_stride + (long long)sl * DH;
+          else
+            dst = ep.vplane + (long long)(g - ep.hq - ep.hkv) * ep.head_stride + (long long)sl * DH;
+#pragma unroll
+          for (int c = 0; c < DH / 32; ++c) {
+            uint32_t w[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) w[i] = pack_bf16(v[c * 32 + 2 * i], v[c * 32 + 2 * i + 1]);
+            st_bf16x32(dst + c * 32, w);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 K-major operand map: dims {K, rows}, box {64, box_rows}, 128-B swizzle.
+int make_tmap(CUtensorMap* m, const void* base, long long rows, long long K, long long ld, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return set_error(RDKV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(RDKV_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return 0;
+}
+
+template <int BN, int EPI, int DH>
+int launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const GemmEpi& ep,
+                cudaStream_t stream) {
+  using C = GemmCfg<BN>;
+  auto kern = gemm_bf16_tc_kernel<BN, EPI, DH>;
+  static bool attr_set = false;  // per template instance
+  if (!attr_set) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    attr_set = true;
+  }
+  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  kern<<<grid, 256, C::SMEM, stream>>>(ta, tb, M, N, K, ep);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace
+
+int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long long ldb, int M, int N,
+                int K, int kind, int dh, const GemmEpi& ep, cudaStream_t stream) {
+  if (M <= 0 || N <= 0) return 0;
+  if (K <= 0 || K % BK != 0) return set_error(RDKV_ERR_ARG, "gemm: K=%d must be a positive multiple of 64", K);
+  if (N % 32 != 0) return set_error(RDKV_ERR_ARG, "gemm: N=%d must be a multiple of 32", N);
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15)
+    return set_error(RDKV_ERR_ARG, "gemm: operands must be 16-byte aligned");
+  if ((lda | ldb) & 7) return set_error(RDKV_ERR_ARG, "gemm: leading dims must be multiples of 8");
+  constexpr int BN = 128;
+  CUtensorMap ta, tb;
+  int rc = make_tmap(&ta, A, M, K, lda, BM);
+  if (rc) return rc;
+  rc = make_tmap(&tb, B, N, K, ldb, BN);
+  if (rc) return rc;
+  switch (kind) {
+    case EPI_STORE: return launch_impl<BN, EPI_STORE, 0>(ta, tb, M, N, K, ep, stream);
+    case EPI_STORE_F32: return launch_impl<BN, EPI_STORE_F32, 0>(ta, tb, M, N, K, ep, stream);
+    case EPI_RESID: return launch_impl<BN, EPI_RESID, 0>(ta, tb, M, N, K, ep, stream);
+    case EPI_SWIGLU:
+      if (N % BN != 0) return set_error(RDKV_ERR_ARG, "swiglu: N must be a multiple of %d", BN);
+      return launch_impl<BN, EPI_SWIGLU, 0>(ta, tb, M, N, K, ep, stream);
+    case EPI_QKV:
+      if (dh == 64) return launch_impl<BN, EPI_QKV, 64>(ta, tb, M, N, K, ep, stream);
+      if (dh == 128) return launch_impl<BN, EPI_QKV, 128>(ta, tb, M, N, K, ep, stream);
+      return set_error(RDKV_ERR_ARG, "qkv: head_dim %d unsupported (64 or 128)", dh);
+    default: return set_error(RDKV_ERR_ARG, "gemm: unknown epilogue %d", kind);
+  }
+}
+
+}  // namespace rdkv

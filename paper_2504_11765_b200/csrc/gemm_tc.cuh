@@ -1,0 +1,46 @@
+// K1: persistent, warp-specialised tcgen05 GEMM for sm_100a.
+//
+//   D[M, N] = A[M, K] . B[N, K]^T      A, B bf16 K-major, fp32 accumulate in TMEM
+//
+// Roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer (one thread),
+// warp 2 = TMEM allocator, warps 4..7 = epilogue (one TMEM lane = one output row
+// per thread).  Operand tiles are staged by TMA with 128-byte swizzle into a
+// STAGES-deep smem ring guarded by full/empty mbarriers; the fp32 accumulator
+// is double-buffered in TMEM so the epilogue of tile i overlaps the MMAs of
+// tile i+1.  Fused epilogues replace the separate elementwise passes of a
+// plain transformer layer:
+//   STORE      bf16 D
+//   STORE_F32  fp32 D (LM-head logits)
+//   RESID      D = R + A.B^T (residual add; R may alias D)
+//   SWIGLU     weights interleaved in BN/2 blocks [gate | up]; D = silu(g) * u
+//   QKV        RoPE on q/k heads, q -> token-major buffer, k/v -> head-major
+//              KV planes at per-row slots (document blob layout or paged pool)
+#pragma once
+#include <cuda_runtime.h>
+#include "ptx.cuh"
+
+namespace rdkv {
+
+enum EpiKind : int { EPI_STORE = 0, EPI_STORE_F32 = 1, EPI_RESID = 2, EPI_SWIGLU = 3, EPI_QKV = 4 };
+
+struct GemmEpi {
+  void* out;                 // bf16 (or fp32 for STORE_F32)
+  long long ldo;             // elements
+  const __nv_bfloat16* resid;
+  long long ldr;
+  // QKV
+  __nv_bfloat16* q;
+  long long ldq;
+  __nv_bfloat16* kplane;     // K plane of this layer: [Hkv][slots][dh]
+  __nv_bfloat16* vplane;     // V plane of this layer
+  long long head_stride;     // elements between consecutive kv heads in a plane
+  const int* slot;           // per row: slot index inside the head plane
+  const int* pos;            // per row: RoPE position
+  const float* rope;         // [max_pos][dh/2] x (cos, sin)
+  int hq, hkv;
+};
+
+int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long long ldb, int M,
+                int N, int K, int kind, int dh, const GemmEpi& ep, cudaStream_t stream);
+
+}  // namespace rdkv

@@ -1,0 +1,80 @@
+"""K1 tcgen05 GEMM parity against a plain PyTorch fp32 reference of the same op."""
+
+import pytest
+import torch
+
+from paper_2504_11765_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+
+def _ptr(t):
+    return t.data_ptr() if t is not None else None
+
+
+def _gemm(A, B, D, epi, R=None):
+    s = torch.cuda.current_stream().cuda_stream
+    M, K = A.shape
+    N = B.shape[0]
+    _lib.check(_lib.lib().rdkv_gemm_bf16(
+        _ptr(A), A.stride(0), _ptr(B), B.stride(0), _ptr(D), D.stride(0),
+        _ptr(R), R.stride(0) if R is not None else 0, M, N, K, epi, s))
+
+
+def _inputs(M, N, K, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    A = (torch.randn(M, K, device="cuda", generator=g) / K ** 0.25).to(torch.bfloat16)
+    B = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.25).to(torch.bfloat16)
+    return A, B
+
+
+SHAPES = [(128, 128, 64), (256, 384, 512), (200, 96, 128), (37, 4096, 2048), (2048, 2048, 2048),
+          (1000, 3072, 2048), (64, 2048, 8192)]
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+def test_store_bf16(M, N, K):
+    A, B = _inputs(M, N, K)
+    D = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+    _gemm(A, B, D, _lib.EPI_STORE)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().T
+    torch.testing.assert_close(D.float(), ref, atol=2e-2, rtol=1e-2)
+
+
+@pytest.mark.parametrize("M,N,K", [(33, 1024, 256), (128, 128256 // 4, 2048)])
+def test_store_f32(M, N, K):
+    A, B = _inputs(M, N, K, seed=1)
+    D = torch.full((M, N), float("nan"), device="cuda", dtype=torch.float32)
+    _gemm(A, B, D, _lib.EPI_STORE_F32)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().T
+    torch.testing.assert_close(D, ref, atol=1e-3, rtol=1e-3)
+
+
+@pytest.mark.parametrize("M,N,K", [(300, 512, 1024), (2048, 2048, 8192)])
+def test_residual_in_place(M, N, K):
+    A, B = _inputs(M, N, K, seed=2)
+    X = torch.randn(M, N, device="cuda").to(torch.bfloat16)
+    ref = X.float() + A.float() @ B.float().T
+    _gemm(A, B, X, _lib.EPI_RESID)
+    torch.cuda.synchronize()
+    torch.testing.assert_close(X.float(), ref, atol=3e-2, rtol=1e-2)
+
+
+@pytest.mark.parametrize("M,N,K", [(130, 256, 128), (640, 2 * 8192, 2048)])
+def test_swiglu(M, N, K):
+    A, B = _inputs(M, N, K, seed=3)
+    D = torch.full((M, N // 2), float("nan"), device="cuda", dtype=torch.bfloat16)
+    _gemm(A, B, D, _lib.EPI_SWIGLU)
+    torch.cuda.synchronize()
+    full = (A.float() @ B.float().T).view(M, N // 128, 2, 64)
+    ref = (torch.nn.functional.silu(full[:, :, 0]) * full[:, :, 1]).reshape(M, N // 2)
+    torch.testing.assert_close(D.float(), ref, atol=2e-2, rtol=1e-2)
+
+
+def test_bad_k_rejected():
+    A, B = _inputs(128, 128, 96)
+    D = torch.empty(128, 128, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(_lib.NativeError):
+        _gemm(A, B, D, _lib.EPI_STORE)
