@@ -133,6 +133,98 @@ RDKV_API int rdkv_drop_page_cache(const char* path);
 RDKV_API int rdkv_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* D, int64_t ldd,
                    const void* R, int64_t ldr, int M, int N, int K, int epilogue, void* stream);
 
+/* -------------------------------------- document KV layout -> HBM (K3) */
+
+/* One cached blob payload already resident in HBM (staged by an async H2D
+ * copy from the pinned host tier, or fetched from a peer GPU). */
+typedef struct rdkv_unpack_job {
+  const void* src;      /* device payload [L][2][Hkv][n_tokens][dh], elem_width bytes each */
+  int32_t n_tokens;     /* tokens of the blob (header token_count)                        */
+  int32_t first_block;  /* index into block_table of the blob's first KV block            */
+  int64_t reserved;
+} rdkv_unpack_job;
+
+/* Unpack n_jobs blob payloads into the paged KV pool
+ *   pool: [L][2][Hkv][pool_slots][dh] bf16, token t of job j at slot
+ *         block_table[first_block + t / block_size] * block_size + t % block_size.
+ * Converts fp32 payloads (elem_width 4) to bf16.  HBM-bound: 2 x payload bytes
+ * per call.  Replaces the payload materialisation of codec.decode
+ * (codec.py:292) and the modeled load_time (costs.py:102-108). */
+RDKV_API int rdkv_kv_unpack(const rdkv_unpack_job* jobs_dev, int n_jobs, int max_tokens,
+                            const int32_t* block_table_dev, int block_size, void* pool_base,
+                            int layers, int kv_heads, int head_dim, int64_t pool_slots,
+                            int elem_width, void* stream);
+
+/* ------------------------------------------ model: document / query prefill */
+
+/* Llama-shaped decoder (RMSNorm, RoPE rotate-half, GQA, SwiGLU). */
+typedef struct rdkv_model_desc {
+  int32_t layers;
+  int32_t hidden;
+  int32_t n_heads;
+  int32_t kv_heads;
+  int32_t head_dim;
+  int32_t ffn;
+  int32_t vocab;
+  int32_t max_pos;
+  float rope_theta;
+  float norm_eps;
+} rdkv_model_desc;
+
+/* Weight pointers (device, 16-B aligned), in this order:
+ *   [0]                 embedding       bf16 [vocab][hidden]
+ *   per layer l (base 1 + 6l):
+ *     +0 attn_norm      fp32 [hidden]
+ *     +1 wqkv           bf16 [(n_heads + 2 kv_heads) head_dim][hidden]   (q | k | v rows)
+ *     +2 wo             bf16 [hidden][n_heads head_dim]
+ *     +3 mlp_norm       fp32 [hidden]
+ *     +4 w_gate_up      bf16 [2 ffn][hidden], rows interleaved in blocks of 64: g0..63 u0..63 g64..
+ *     +5 w_down         bf16 [hidden][ffn]
+ *   [1 + 6L]            final_norm      fp32 [hidden]
+ *   [2 + 6L]            lm_head         bf16 [vocab][hidden] (may alias the embedding)  */
+#define RDKV_WEIGHTS_PER_LAYER 6
+
+typedef struct rdkv_model rdkv_model;
+
+RDKV_API int rdkv_model_create(const rdkv_model_desc* desc, const void* const* weights,
+                               size_t n_weights, rdkv_model** out);
+RDKV_API void rdkv_model_destroy(rdkv_model* model);
+
+/* A batch of sequences, each = a cached prefix already in the KV pool plus
+ * n_new new tokens (uncached documents then the query).  n_cached = 0 for
+ * every sequence is the full-prompt prefill; a single sequence whose KV pool
+ * is a blob payload (kv_slots = n, block_size = n, block_table = {0}) is
+ * document-KV generation, written straight in the .rdkv payload layout. */
+typedef struct rdkv_batch {
+  int32_t n_seqs;              /* S                                                  */
+  int32_t n_tokens;            /* T = sum of n_new                                   */
+  int32_t max_new;             /* max n_new over sequences                           */
+  int32_t block_size;          /* KV block size in tokens                            */
+  int32_t bt_stride;           /* block-table entries per sequence                   */
+  int32_t want_logits;         /* 1: last-row logits + argmax; 0: KV only            */
+  const int32_t* tokens;       /* dev [T] new token ids, sequences back to back      */
+  const int32_t* pos;          /* dev [T] position of each new token (n_cached + i)  */
+  const int32_t* slot;         /* dev [T] KV-plane slot receiving each token's K/V   */
+  const int32_t* seq_start;    /* dev [S] first row of each sequence in [0, T)       */
+  const int32_t* seq_new;      /* dev [S]                                            */
+  const int32_t* seq_cached;   /* dev [S] cached-prefix tokens                       */
+  const int32_t* block_table;  /* dev [S * bt_stride]                                */
+  const int32_t* last_row;     /* dev [S] row of each sequence's last token          */
+  void* kv_base;               /* dev KV pool [L][2][Hkv][kv_slots][dh] bf16         */
+  int64_t kv_slots;
+  float* logits;               /* dev [S][vocab] fp32                                */
+  int32_t* next_token;         /* dev [S] argmax (first token), may be NULL          */
+} rdkv_batch;
+
+/* Device workspace needed by rdkv_forward for n_tokens / n_seqs. */
+RDKV_API size_t rdkv_workspace_bytes(const rdkv_model* model, int n_tokens, int n_seqs);
+
+/* Prefill a batch (K1 GEMMs + K2/K4 attention + K5 LM head) on `stream`.
+ * Replaces synth_blob (codec.py:188-224) for document KV and ttft
+ * (costs.py:121-144) / cached_prefill_work (costs.py:89-99) for queries. */
+RDKV_API int rdkv_forward(rdkv_model* model, const rdkv_batch* batch, void* workspace,
+                          size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,220 @@
+// HBM-bound helper kernels of the hot path:
+//   K3  kv_unpack     blob payload [L][2][Hkv][n][dh] (bf16 or fp32) -> paged pool planes
+//       embed         token ids -> residual rows
+//       rmsnorm       row RMSNorm with fp32 gain (optionally gathering rows)
+//       argmax        first index of the row maximum (torch.argmax tie rule)
+#include <cuda_bf16.h>
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels_misc.cuh"
+
+namespace rdkv {
+namespace {
+
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// ---------------------------------------------------------------- K3 unpack
+// One warp moves one segment = (job, layer, k|v, head, block): a contiguous
+// run of up to block_size*dh elements in the blob and in the pool plane.
+// 16-byte loads, UNROLL of them in flight per lane.
+template <int SRC_W>
+__global__ void __launch_bounds__(256) kv_unpack_kernel(const UnpackJob* __restrict__ jobs, const int* __restrict__ bt,
+                                                        int block_size, __nv_bfloat16* __restrict__ pool, int layers,
+                                                        int hkv, int dh, long long slots) {
+  const UnpackJob jb = jobs[blockIdx.y];
+  const int nblk = (jb.n_tokens + block_size - 1) / block_size;
+  const long long nseg = (long long)layers * 2 * hkv * nblk;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int UNROLL = 4;
+  for (long long seg = (long long)blockIdx.x * 8 + warp; seg < nseg; seg += (long long)gridDim.x * 8) {
+    const int b = (int)(seg % nblk);
+    const long long plane = seg / nblk;  // (l*2 + kv)*hkv + h
+    const int t0 = b * block_size;
+    const int ntok = min(block_size, jb.n_tokens - t0);
+    const long long n_el = (long long)ntok * dh;
+    const long long src_off = plane * (long long)jb.n_tokens * dh + (long long)t0 * dh;
+    const long long dst_off = plane * slots * dh + (long long)bt[jb.first_block + b] * block_size * dh;
+    __nv_bfloat16* dst = pool + dst_off;
+    if constexpr (SRC_W == 2) {
+      const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(jb.src) + src_off;
+      const long long nvec = n_el / 8;  // 8 bf16 per 16 B
+      long long i = lane;
+      for (; i + 32 * (UNROLL - 1) < nvec; i += 32 * UNROLL) {
+        uint4 v[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) v[u] = ld_stream(src + (i + 32 * u) * 8);
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) *reinterpret_cast<uint4*>(dst + (i + 32 * u) * 8) = v[u];
+      }
+      for (; i < nvec; i += 32) *reinterpret_cast<uint4*>(dst + i * 8) = ld_stream(src + i * 8);
+    } else {
+      const float* src = static_cast<const float*>(jb.src) + src_off;
+      const long long nvec = n_el / 8;  // 8 fp32 (32 B) -> 8 bf16 (16 B)
+      for (long long i = lane; i < nvec; i += 32) {
+        const uint4 a = ld_stream(src + i * 8), c = ld_stream(src + i * 8 + 4);
+        uint4 o;
+        o.x = pack_bf16_f(__uint_as_float(a.x), __uint_as_float(a.y));
+        o.y = pack_bf16_f(__uint_as_float(a.z), __uint_as_float(a.w));
+        o.z = pack_bf16_f(__uint_as_float(c.x), __uint_as_float(c.y));
+        o.w = pack_bf16_f(__uint_as_float(c.z), __uint_as_float(c.w));
+        *reinterpret_cast<uint4*>(dst + i * 8) = o;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- embed
+__global__ void embed_kernel(const int* __restrict__ tok, const __nv_bfloat16* __restrict__ table,
+                             __nv_bfloat16* __restrict__ out, int d, int vocab) {
+  const int t = blockIdx.x;
+  int id = tok[t];
+  id = id < 0 ? 0 : (id >= vocab ? vocab - 1 : id);
+  const uint4* src = reinterpret_cast<const uint4*>(table + (long long)id * d);
+  uint4* dst = reinterpret_cast<uint4*>(out + (long long)t * d);
+  for (int i = threadIdx.x; i < d / 8; i += blockDim.x) dst[i] = src[i];
+}
+
+// ---------------------------------------------------------------- rmsnorm
+// out[r] = x[src_row(r)] * rsqrt(mean(x^2) + eps) * gain ; one CTA per row.
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, long long ldx,
+                                                      const int* __restrict__ rows, const float* __restrict__ gain,
+                                                      __nv_bfloat16* __restrict__ out, long long ldo, int d,
+                                                      float eps) {
+  const int r = blockIdx.x;
+  const int src_row = rows ? rows[r] : r;
+  const __nv_bfloat16* xr = x + (long long)src_row * ldx;
+  float ss = 0.f;
+  for (int i = threadIdx.x * 8; i < d; i += blockDim.x * 8) {
+    const uint4 u = *reinterpret_cast<const uint4*>(xr + i);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = unpack_bf16_f(w[j]);
+      ss += f.x * f.x + f.y * f.y;
+    }
+  }
+  __shared__ float red[32];
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(red[0] / (float)d + eps);
+  __nv_bfloat16* orow = out + (long long)r * ldo;
+  for (int i = threadIdx.x * 8; i < d; i += blockDim.x * 8) {
+    const uint4 u = *reinterpret_cast<const uint4*>(xr + i);
+    const float4 g0 = *reinterpret_cast<const float4*>(gain + i);
+    const float4 g1 = *reinterpret_cast<const float4*>(gain + i + 4);
+    const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = unpack_bf16_f(w[j]);
+      o[j] = pack_bf16_f(f.x * inv * gg[2 * j], f.y * inv * gg[2 * j + 1]);
+    }
+    *reinterpret_cast<uint4*>(orow + i) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// ---------------------------------------------------------------- argmax
+__global__ void __launch_bounds__(1024) argmax_kernel(const float* __restrict__ logits, long long ld, int n,
+                                                      int* __restrict__ out) {
+  const float* row = logits + (long long)blockIdx.x * ld;
+  float best = -INFINITY;
+  int idx = 0x7fffffff;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const float v = row[i];
+    if (v > best) {  // strided scan: first occurrence within this thread
+      best = v;
+      idx = i;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const float vb = __shfl_xor_sync(0xffffffff, best, o);
+    const int ib = __shfl_xor_sync(0xffffffff, idx, o);
+    if (vb > best || (vb == best && ib < idx)) {
+      best = vb;
+      idx = ib;
+    }
+  }
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  if ((threadIdx.x & 31) == 0) {
+    sv[threadIdx.x >> 5] = best;
+    si[threadIdx.x >> 5] = idx;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int nw = blockDim.x >> 5;
+    best = threadIdx.x < nw ? sv[threadIdx.x] : -INFINITY;
+    idx = threadIdx.x < nw ? si[threadIdx.x] : 0x7fffffff;
+    for (int o = 16; o; o >>= 1) {
+      const float vb = __shfl_xor_sync(0xffffffff, best, o);
+      const int ib = __shfl_xor_sync(0xffffffff, idx, o);
+      if (vb > best || (vb == best && ib < idx)) {
+        best = vb;
+        idx = ib;
+      }
+    }
+    if (threadIdx.x == 0) out[blockIdx.x] = idx;
+  }
+}
+
+}  // namespace
+
+int launch_kv_unpack(const UnpackJob* jobs_dev, int n_jobs, int max_tokens, const int* bt, int block_size,
+                     void* pool, int layers, int hkv, int dh, long long slots, int elem_width, cudaStream_t st) {
+  if (n_jobs <= 0 || max_tokens <= 0) return 0;
+  if (dh % 8 != 0) return set_error(RDKV_ERR_ARG, "unpack: head_dim must be a multiple of 8");
+  if (elem_width != 2 && elem_width != 4) return set_error(RDKV_ERR_ARG, "unpack: elem_width must be 2 or 4");
+  const long long segs = (long long)layers * 2 * hkv * ((max_tokens + block_size - 1) / block_size);
+  long long gx = (segs + 7) / 8;
+  const long long cap = 4LL * num_sms() * 4;  // ~4 CTAs/SM resident, a few waves
+  if (gx > cap) gx = cap;
+  dim3 grid((unsigned)gx, (unsigned)n_jobs);
+  auto* dst = static_cast<__nv_bfloat16*>(pool);
+  if (elem_width == 2)
+    kv_unpack_kernel<2><<<grid, 256, 0, st>>>(jobs_dev, bt, block_size, dst, layers, hkv, dh, slots);
+  else
+    kv_unpack_kernel<4><<<grid, 256, 0, st>>>(jobs_dev, bt, block_size, dst, layers, hkv, dh, slots);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int launch_embed(const int* tok, const __nv_bfloat16* table, __nv_bfloat16* out, int n, int d, int vocab,
+                 cudaStream_t st) {
+  if (n <= 0) return 0;
+  embed_kernel<<<n, 128, 0, st>>>(tok, table, out, d, vocab);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int launch_rmsnorm(const __nv_bfloat16* x, long long ldx, const int* rows, const float* gain, __nv_bfloat16* out,
+                   long long ldo, int n_rows, int d, float eps, cudaStream_t st) {
+  if (n_rows <= 0) return 0;
+  if (d % 8 != 0) return set_error(RDKV_ERR_ARG, "rmsnorm: d must be a multiple of 8");
+  rmsnorm_kernel<<<n_rows, 256, 0, st>>>(x, ldx, rows, gain, out, ldo, d, eps);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int launch_argmax(const float* logits, long long ld, int rows, int n, int* out, cudaStream_t st) {
+  if (rows <= 0) return 0;
+  argmax_kernel<<<rows, 1024, 0, st>>>(logits, ld, n, out);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace rdkv

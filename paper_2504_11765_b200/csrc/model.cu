@@ -1,0 +1,206 @@
+// Llama-shaped decoder forward over a batch of sequences with a (possibly
+// cached) KV prefix — the device half of document-KV generation (replaces
+// codec.synth_blob, codec.py:188-224) and of prefill-with-cached-prefix
+// (replaces costs.ttft, costs.py:121-144).
+//
+// Per layer: RMSNorm -> QKV GEMM (RoPE + KV write epilogue) -> attention ->
+// O GEMM (+residual) -> RMSNorm -> gate/up GEMM (SwiGLU epilogue) -> down GEMM
+// (+residual).  The last row of each sequence then goes through the final
+// RMSNorm, the LM head (fp32 logits) and argmax = the first token.
+#include <cmath>
+#include <cstdlib>
+#include <new>
+#include <vector>
+
+#include "attention.cuh"
+#include "common.cuh"
+#include "gemm_tc.cuh"
+#include "kernels_misc.cuh"
+
+struct rdkv_model {
+  rdkv_model_desc d;
+  std::vector<const void*> w;  // see rdkv.h for the order
+  float* rope = nullptr;        // [max_pos][dh/2] (cos, sin)
+  int device = 0;
+};
+
+namespace rdkv {
+namespace {
+
+constexpr size_t kAlign = 256;
+inline size_t up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct Ws {
+  __nv_bfloat16 *x, *h, *q, *o, *a, *hl;
+};
+
+size_t ws_layout(const rdkv_model_desc& d, int T, int S, Ws* ws, void* base) {
+  const size_t qd = (size_t)d.n_heads * d.head_dim;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += up(bytes);
+    return o;
+  };
+  const size_t ox = take((size_t)T * d.hidden * 2), oh = take((size_t)T * d.hidden * 2);
+  const size_t oq = take((size_t)T * qd * 2), oo = take((size_t)T * qd * 2);
+  const size_t oa = take((size_t)T * d.ffn * 2), ol = take((size_t)(S > 0 ? S : 1) * d.hidden * 2);
+  if (ws && base) {
+    auto* b = static_cast<uint8_t*>(base);
+    ws->x = reinterpret_cast<__nv_bfloat16*>(b + ox);
+    ws->h = reinterpret_cast<__nv_bfloat16*>(b + oh);
+    ws->q = reinterpret_cast<__nv_bfloat16*>(b + oq);
+    ws->o = reinterpret_cast<__nv_bfloat16*>(b + oo);
+    ws->a = reinterpret_cast<__nv_bfloat16*>(b + oa);
+    ws->hl = reinterpret_cast<__nv_bfloat16*>(b + ol);
+  }
+  return off;
+}
+
+inline const __nv_bfloat16* W(const rdkv_model* m, int i) { return static_cast<const __nv_bfloat16*>(m->w[i]); }
+inline const float* G(const rdkv_model* m, int i) { return static_cast<const float*>(m->w[i]); }
+
+}  // namespace
+}  // namespace rdkv
+
+using namespace rdkv;
+
+extern "C" {
+
+int rdkv_model_create(const rdkv_model_desc* desc, const void* const* weights, size_t n_weights, rdkv_model** out) {
+  if (!desc || !weights || !out) return set_error(RDKV_ERR_ARG, "model_create: null argument");
+  const rdkv_model_desc& d = *desc;
+  if (d.layers < 1 || d.hidden < 64 || d.n_heads < 1 || d.kv_heads < 1 || d.n_heads % d.kv_heads)
+    return set_error(RDKV_ERR_ARG, "model_create: bad dimensions");
+  if (d.head_dim != 64 && d.head_dim != 128) return set_error(RDKV_ERR_ARG, "model_create: head_dim must be 64/128");
+  if (d.hidden % 64 || d.ffn % 64 || (d.n_heads * d.head_dim) % 64 || d.vocab % 32)
+    return set_error(RDKV_ERR_ARG, "model_create: hidden/ffn/heads*dh must be multiples of 64, vocab of 32");
+  const size_t need = (size_t)RDKV_WEIGHTS_PER_LAYER * d.layers + 3;
+  if (n_weights != need) return set_error(RDKV_ERR_ARG, "model_create: expected %zu weights, got %zu", need, n_weights);
+  for (size_t i = 0; i < n_weights; ++i)
+    if (!weights[i] || (reinterpret_cast<uintptr_t>(weights[i]) & 15))
+      return set_error(RDKV_ERR_ARG, "model_create: weight %zu null or not 16-byte aligned", i);
+  auto* m = new (std::nothrow) rdkv_model;
+  if (!m) return set_error(RDKV_ERR_ARG, "model_create: out of host memory");
+  m->d = d;
+  m->w.assign(weights, weights + n_weights);
+  cudaGetDevice(&m->device);
+  // RoPE table in double precision, rounded once to fp32 (same as the oracle).
+  const int half = d.head_dim / 2;
+  std::vector<float> tab((size_t)d.max_pos * half * 2);
+  for (int p = 0; p < d.max_pos; ++p)
+    for (int i = 0; i < half; ++i) {
+      const double inv = std::pow((double)d.rope_theta, -2.0 * i / (double)d.head_dim);
+      const double a = (double)p * inv;
+      tab[((size_t)p * half + i) * 2] = (float)std::cos(a);
+      tab[((size_t)p * half + i) * 2 + 1] = (float)std::sin(a);
+    }
+  if (cudaMalloc(&m->rope, tab.size() * sizeof(float)) != cudaSuccess ||
+      cudaMemcpy(m->rope, tab.data(), tab.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(m->rope);
+    delete m;
+    return set_error(RDKV_ERR_CUDA, "model_create: rope table upload failed");
+  }
+  *out = m;
+  return 0;
+}
+
+void rdkv_model_destroy(rdkv_model* m) {
+  if (!m) return;
+  cudaFree(m->rope);
+  delete m;
+}
+
+size_t rdkv_workspace_bytes(const rdkv_model* m, int n_tokens, int n_seqs) {
+  if (!m) return 0;
+  return ws_layout(m->d, n_tokens, n_seqs, nullptr, nullptr);
+}
+
+int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_bytes, void* stream) {
+  if (!m || !b) return set_error(RDKV_ERR_ARG, "forward: null argument");
+  const rdkv_model_desc& d = m->d;
+  const int T = b->n_tokens, S = b->n_seqs;
+  if (T <= 0 || S <= 0) return set_error(RDKV_ERR_ARG, "forward: empty batch");
+  if (b->block_size <= 0 || b->kv_slots <= 0 || !b->kv_base) return set_error(RDKV_ERR_ARG, "forward: bad KV pool");
+  Ws ws;
+  if (ws_layout(d, T, S, &ws, ws_base) > ws_bytes) return set_error(RDKV_ERR_ARG, "forward: workspace too small");
+  auto st = static_cast<cudaStream_t>(stream);
+  const int dh = d.head_dim, hq = d.n_heads, hkv = d.kv_heads;
+  const long long qd = (long long)hq * dh;
+  const long long plane = (long long)hkv * b->kv_slots * dh;  // elements per (layer, k|v) plane
+  auto* kv = static_cast<__nv_bfloat16*>(b->kv_base);
+
+  RDKV_TRY(launch_embed(b->tokens, W(m, 0), ws.x, T, d.hidden, d.vocab, st));
+  for (int l = 0; l < d.layers; ++l) {
+    const int wb = 1 + RDKV_WEIGHTS_PER_LAYER * l;
+    __nv_bfloat16* kpl = kv + (2LL * l) * plane;
+    __nv_bfloat16* vpl = kv + (2LL * l + 1) * plane;
+    // attention block
+    RDKV_TRY(launch_rmsnorm(ws.x, d.hidden, nullptr, G(m, wb + 0), ws.h, d.hidden, T, d.hidden, d.norm_eps, st));
+    GemmEpi eq{};
+    eq.q = ws.q;
+    eq.ldq = qd;
+    eq.kplane = kpl;
+    eq.vplane = vpl;
+    eq.head_stride = b->kv_slots * dh;
+    eq.slot = b->slot;
+    eq.pos = b->pos;
+    eq.rope = m->rope;
+    eq.hq = hq;
+    eq.hkv = hkv;
+    RDKV_TRY(launch_gemm(ws.h, d.hidden, W(m, wb + 1), d.hidden, T, (int)((hq + 2 * hkv) * dh), d.hidden, EPI_QKV, dh,
+                         eq, st));
+    AttnParams ap{};
+    ap.q = ws.q;
+    ap.ldq = qd;
+    ap.o = ws.o;
+    ap.ldo = qd;
+    ap.kplane = kpl;
+    ap.vplane = vpl;
+    ap.head_stride = b->kv_slots * dh;
+    ap.seq_start = b->seq_start;
+    ap.seq_new = b->seq_new;
+    ap.seq_cached = b->seq_cached;
+    ap.block_table = b->block_table;
+    ap.bt_stride = b->bt_stride;
+    ap.block_size = b->block_size;
+    ap.hq = hq;
+    ap.hkv = hkv;
+    ap.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)dh));
+    RDKV_TRY(launch_attention(ap, dh, S, b->max_new, st));
+    GemmEpi er{};
+    er.out = ws.x;
+    er.ldo = d.hidden;
+    er.resid = ws.x;
+    er.ldr = d.hidden;
+    RDKV_TRY(launch_gemm(ws.o, qd, W(m, wb + 2), qd, T, d.hidden, (int)qd, EPI_RESID, 0, er, st));
+    // MLP block
+    RDKV_TRY(launch_rmsnorm(ws.x, d.hidden, nullptr, G(m, wb + 3), ws.h, d.hidden, T, d.hidden, d.norm_eps, st));
+    GemmEpi eg{};
+    eg.out = ws.a;
+    eg.ldo = d.ffn;
+    RDKV_TRY(launch_gemm(ws.h, d.hidden, W(m, wb + 4), d.hidden, T, 2 * d.ffn, d.hidden, EPI_SWIGLU, 0, eg, st));
+    RDKV_TRY(launch_gemm(ws.a, d.ffn, W(m, wb + 5), d.ffn, T, d.hidden, d.ffn, EPI_RESID, 0, er, st));
+  }
+  if (b->want_logits) {
+    if (!b->logits || !b->last_row) return set_error(RDKV_ERR_ARG, "forward: logits requested without buffers");
+    const int fn = 1 + RDKV_WEIGHTS_PER_LAYER * d.layers;
+    RDKV_TRY(launch_rmsnorm(ws.x, d.hidden, b->last_row, G(m, fn), ws.hl, d.hidden, S, d.hidden, d.norm_eps, st));
+    GemmEpi el{};
+    el.out = b->logits;
+    el.ldo = d.vocab;
+    RDKV_TRY(launch_gemm(ws.hl, d.hidden, W(m, fn + 1), d.hidden, S, d.vocab, d.hidden, EPI_STORE_F32, 0, el, st));
+    if (b->next_token) RDKV_TRY(launch_argmax(b->logits, d.vocab, S, d.vocab, b->next_token, st));
+  }
+  return 0;
+}
+
+int rdkv_kv_unpack(const rdkv_unpack_job* jobs_dev, int n_jobs, int max_tokens, const int32_t* block_table_dev,
+                   int block_size, void* pool_base, int layers, int kv_heads, int head_dim, int64_t pool_slots,
+                   int elem_width, void* stream) {
+  if (block_size <= 0 || !pool_base || !jobs_dev) return set_error(RDKV_ERR_ARG, "kv_unpack: bad arguments");
+  return launch_kv_unpack(jobs_dev, n_jobs, max_tokens, block_table_dev, block_size, pool_base, layers, kv_heads,
+                          head_dim, pool_slots, elem_width, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,322 @@
+"""One model instance on one B200: document-KV generation, KV load into a
+paged HBM pool, and batched query prefill over cached document prefixes.
+
+This is the device half of the reference path.  Each method names the
+reference function whose *semantics* it implements:
+
+* :meth:`Engine.generate_doc_kv` — the payload of ``synth_blob``
+  (codec.py:188-224): KV of an ordered document combination computed from
+  scratch over its concatenated tokens at positions 0..n-1 (prefetch.py:6-8),
+  written by the QKV-GEMM epilogue straight into the `.rdkv` payload layout.
+* :meth:`Engine.load_cached` — ``KvStore.get`` payload -> HBM
+  (store.py:250-280, ``load_time`` costs.py:102-108): async H2D of the pinned
+  payload on a side stream, then the K3 unpack kernel into pool blocks.
+* :meth:`Engine.prefill` — ``ttft`` / ``cached_prefill_work``
+  (costs.py:89-144): new tokens (uncached documents, then the query) attend
+  over the cached prefix plus themselves; the last row yields the first-token
+  logits and argmax.
+
+All GPU work goes through librdkv's C ABI; there is no PyTorch compute path.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from collections import deque
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .model import ModelSpec, ModelWeights, init_weights
+
+
+class RdkvModelDesc(C.Structure):
+    _fields_ = [("layers", C.c_int32), ("hidden", C.c_int32), ("n_heads", C.c_int32), ("kv_heads", C.c_int32),
+                ("head_dim", C.c_int32), ("ffn", C.c_int32), ("vocab", C.c_int32), ("max_pos", C.c_int32),
+                ("rope_theta", C.c_float), ("norm_eps", C.c_float)]
+
+
+class RdkvBatch(C.Structure):
+    _fields_ = [("n_seqs", C.c_int32), ("n_tokens", C.c_int32), ("max_new", C.c_int32), ("block_size", C.c_int32),
+                ("bt_stride", C.c_int32), ("want_logits", C.c_int32),
+                ("tokens", C.c_void_p), ("pos", C.c_void_p), ("slot", C.c_void_p), ("seq_start", C.c_void_p),
+                ("seq_new", C.c_void_p), ("seq_cached", C.c_void_p), ("block_table", C.c_void_p),
+                ("last_row", C.c_void_p), ("kv_base", C.c_void_p), ("kv_slots", C.c_int64),
+                ("logits", C.c_void_p), ("next_token", C.c_void_p)]
+
+
+class RdkvUnpackJob(C.Structure):
+    _fields_ = [("src", C.c_void_p), ("n_tokens", C.c_int32), ("first_block", C.c_int32), ("reserved", C.c_int64)]
+
+
+_UNPACK_DTYPE = np.dtype([("src", "<u8"), ("n_tokens", "<i4"), ("first_block", "<i4"), ("reserved", "<i8")])
+
+_N_SIG = {
+    "rdkv_model_create": (C.c_int, [C.POINTER(RdkvModelDesc), C.POINTER(C.c_void_p), C.c_size_t,
+                                    C.POINTER(C.c_void_p)]),
+    "rdkv_model_destroy": (None, [C.c_void_p]),
+    "rdkv_workspace_bytes": (C.c_size_t, [C.c_void_p, C.c_int, C.c_int]),
+    "rdkv_forward": (C.c_int, [C.c_void_p, C.POINTER(RdkvBatch), C.c_void_p, C.c_size_t, C.c_void_p]),
+    "rdkv_kv_unpack": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int,
+                                 C.c_int, C.c_int64, C.c_int, C.c_void_p]),
+}
+
+
+def _L():
+    lib = _lib.lib()
+    if not getattr(lib, "_engine_sigs", False):
+        for name, (res, args) in _N_SIG.items():
+            fn = getattr(lib, name)
+            fn.restype, fn.argtypes = res, args
+        lib._engine_sigs = True
+    return lib
+
+
+def _stream_ptr(stream: torch.cuda.Stream | None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+# ----------------------------------------------------------------- KV pool
+
+
+class KvPool:
+    """Paged KV pool in HBM: planes [L][2][Hkv][slots][dh] bf16, slots = n_blocks * block_size.
+
+    Head-major like the blob payload, so unpacking a blob block is one
+    contiguous run per (layer, K|V, head) and the attention kernel reads
+    [block_size][dh] runs."""
+
+    def __init__(self, spec: ModelSpec, n_blocks: int, block_size: int = 64, device="cuda") -> None:
+        if block_size % 8:
+            raise ValueError("block_size must be a multiple of 8")
+        self.spec, self.block_size, self.n_blocks = spec, block_size, n_blocks
+        self.slots = n_blocks * block_size
+        numel = spec.layers * 2 * spec.kv_heads * self.slots * spec.head_dim
+        self.data = torch.empty(numel, dtype=torch.bfloat16, device=device)
+        self._free: deque[int] = deque(range(n_blocks))
+
+    def blocks_for(self, n_tokens: int) -> int:
+        return (n_tokens + self.block_size - 1) // self.block_size
+
+    def alloc(self, n_tokens: int) -> list[int]:
+        n = self.blocks_for(n_tokens)
+        if n > len(self._free):
+            raise MemoryError(f"KV pool exhausted: need {n} blocks, {len(self._free)} free")
+        return [self._free.popleft() for _ in range(n)]
+
+    def release(self, blocks: Sequence[int]) -> None:
+        self._free.extend(blocks)
+
+    @property
+    def free_blocks(self) -> int:
+        return len(self._free)
+
+    def gather(self, blocks: Sequence[int], n_tokens: int) -> torch.Tensor:
+        """[L][2][Hkv][n_tokens][dh] copy of a sequence's KV (tests/debug)."""
+        s = self.spec
+        v = self.data.view(s.layers, 2, s.kv_heads, self.slots, s.head_dim)
+        idx = torch.tensor([b * self.block_size + i for b in blocks for i in range(self.block_size)][:n_tokens],
+                           device=self.data.device)
+        return v.index_select(3, idx)
+
+
+# ----------------------------------------------------------------- batch plans
+
+
+@dataclass
+class SeqPlan:
+    tokens: np.ndarray          # new tokens (int32)
+    n_cached: int               # cached-prefix tokens already in the pool
+    blocks: Sequence[int]       # pool blocks covering positions [0, n_cached + len(tokens))
+
+
+class BatchPlan:
+    """Device metadata for rdkv_forward, packed into one int32 buffer (one H2D)."""
+
+    def __init__(self, seqs: Sequence[SeqPlan], block_size: int, device) -> None:
+        S = len(seqs)
+        n_new = np.array([len(s.tokens) for s in seqs], dtype=np.int32)
+        T = int(n_new.sum())
+        if S == 0 or T == 0:
+            raise ValueError("empty batch")
+        bt_stride = max(len(s.blocks) for s in seqs)
+        starts = np.zeros(S, np.int32)
+        starts[1:] = np.cumsum(n_new)[:-1]
+        cached = np.array([s.n_cached for s in seqs], dtype=np.int32)
+        bt = np.zeros((S, bt_stride), np.int32)
+        pos = np.empty(T, np.int32)
+        slot = np.empty(T, np.int32)
+        for i, s in enumerate(seqs):
+            blk = np.asarray(s.blocks, dtype=np.int64)
+            need = (s.n_cached + len(s.tokens) + block_size - 1) // block_size
+            if len(blk) < need:
+                raise ValueError(f"sequence {i}: {len(blk)} blocks cannot hold {s.n_cached + len(s.tokens)} tokens")
+            bt[i, : len(blk)] = blk
+            p = np.arange(s.n_cached, s.n_cached + len(s.tokens), dtype=np.int64)
+            a, b = starts[i], starts[i] + len(s.tokens)
+            pos[a:b] = p
+            slot[a:b] = blk[p // block_size] * block_size + p % block_size
+        last = starts + n_new - 1
+        toks = np.concatenate([np.asarray(s.tokens, dtype=np.int32) for s in seqs])
+        parts = [toks, pos, slot, starts, n_new, cached, bt.ravel(), last]
+        offs = np.cumsum([0] + [len(p) for p in parts])
+        host = torch.from_numpy(np.concatenate(parts).astype(np.int32))
+        if torch.cuda.is_available():
+            host = host.pin_memory()
+        self.meta = host.to(device, non_blocking=True)
+        base = self.meta.data_ptr()
+        self.ptr = {k: base + 4 * int(o) for k, o in zip(
+            ["tokens", "pos", "slot", "seq_start", "seq_new", "seq_cached", "block_table", "last_row"], offs[:-1])}
+        self.n_seqs, self.n_tokens, self.max_new = S, T, int(n_new.max())
+        self.bt_stride, self.block_size = bt_stride, block_size
+        self.n_new, self.n_cached = n_new, cached
+
+    def struct(self, kv_base: int, kv_slots: int, logits=None, next_token=None) -> RdkvBatch:
+        p = self.ptr
+        return RdkvBatch(
+            n_seqs=self.n_seqs, n_tokens=self.n_tokens, max_new=self.max_new, block_size=self.block_size,
+            bt_stride=self.bt_stride, want_logits=1 if logits is not None else 0,
+            tokens=p["tokens"], pos=p["pos"], slot=p["slot"], seq_start=p["seq_start"], seq_new=p["seq_new"],
+            seq_cached=p["seq_cached"], block_table=p["block_table"], last_row=p["last_row"],
+            kv_base=kv_base, kv_slots=kv_slots,
+            logits=logits.data_ptr() if logits is not None else None,
+            next_token=next_token.data_ptr() if next_token is not None else None)
+
+
+# ----------------------------------------------------------------- the model handle
+
+
+class DeviceModel:
+    """Owns an rdkv_model handle over device-resident weights."""
+
+    def __init__(self, weights: ModelWeights) -> None:
+        s = weights.spec
+        self.spec, self.weights = s, weights
+        self.device = weights.embed.device
+        desc = RdkvModelDesc(layers=s.layers, hidden=s.hidden, n_heads=s.n_heads, kv_heads=s.kv_heads,
+                             head_dim=s.head_dim, ffn=s.ffn, vocab=s.vocab, max_pos=s.max_pos,
+                             rope_theta=s.rope_theta, norm_eps=s.norm_eps)
+        ptrs = weights.pointer_list()
+        arr = (C.c_void_p * len(ptrs))(*ptrs)
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(_L().rdkv_model_create(C.byref(desc), arr, len(ptrs), C.byref(h)))
+        self._h = h
+        self._ws: torch.Tensor | None = None
+
+    def close(self) -> None:
+        if self._h:
+            _L().rdkv_model_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def workspace(self, n_tokens: int, n_seqs: int) -> torch.Tensor:
+        need = int(_L().rdkv_workspace_bytes(self._h, n_tokens, n_seqs))
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def forward(self, plan: BatchPlan, kv_base: int, kv_slots: int, logits=None, next_token=None,
+                stream: torch.cuda.Stream | None = None) -> None:
+        ws = self.workspace(plan.n_tokens, plan.n_seqs)
+        b = plan.struct(kv_base, kv_slots, logits, next_token)
+        _lib.check(_L().rdkv_forward(self._h, C.byref(b), ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
+
+
+def kv_unpack(pool: KvPool, jobs: Sequence[tuple[torch.Tensor, int, int]], block_table: torch.Tensor,
+              elem_width: int = 2, stream: torch.cuda.Stream | None = None) -> None:
+    """K3: unpack device-resident blob payloads into the pool.
+
+    ``jobs`` = (payload device tensor, n_tokens, first_block index into the flat
+    ``block_table`` int32 device tensor)."""
+    if not jobs:
+        return
+    arr = np.zeros(len(jobs), dtype=_UNPACK_DTYPE)
+    for i, (src, n, fb) in enumerate(jobs):
+        arr[i] = (src.data_ptr(), n, fb, 0)
+    host = torch.from_numpy(arr.view(np.uint8).copy())
+    if torch.cuda.is_available():
+        host = host.pin_memory()
+    dev = host.to(pool.data.device, non_blocking=True)
+    s = pool.spec
+    _lib.check(_L().rdkv_kv_unpack(dev.data_ptr(), len(jobs), max(n for _, n, _ in jobs), block_table.data_ptr(),
+                                   pool.block_size, pool.data.data_ptr(), s.layers, s.kv_heads, s.head_dim,
+                                   pool.slots, elem_width, _stream_ptr(stream)))
+    pool._last_jobs = dev  # keep alive until the stream consumes it
+
+
+# ----------------------------------------------------------------- the instance
+
+
+@dataclass
+class QueryRequest:
+    """One query: a cached prefix (device payload, or None) plus new tokens."""
+
+    new_tokens: np.ndarray
+    cached_payload: torch.Tensor | None = None   # device bf16 payload [L][2][Hkv][n_cached][dh]
+    n_cached: int = 0
+
+
+class Engine:
+    """Model instance bound to one GPU."""
+
+    def __init__(self, spec: ModelSpec, weights: ModelWeights | None = None, seed: int = 0, device="cuda",
+                 pool_tokens: int = 1 << 16, block_size: int = 64) -> None:
+        self.device = torch.device(device)
+        self.spec = spec
+        self.weights = weights if weights is not None else init_weights(spec, seed, self.device)
+        self.model = DeviceModel(self.weights)
+        self.pool = KvPool(spec, (pool_tokens + block_size - 1) // block_size, block_size, self.device)
+        self.copy_stream = torch.cuda.Stream(device=self.device)
+
+    # -------------------------------------------------------------- generation
+    def generate_doc_kv(self, tokens: np.ndarray, out: torch.Tensor | None = None,
+                        stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """Document KV of ``tokens`` (positions 0..n-1) in the blob payload layout
+        [L][2][Hkv][n][dh] bf16, as a flat device tensor."""
+        s, n = self.spec, len(tokens)
+        numel = s.layers * 2 * s.kv_heads * n * s.head_dim
+        if out is None:
+            out = torch.empty(numel, dtype=torch.bfloat16, device=self.device)
+        plan = BatchPlan([SeqPlan(np.asarray(tokens, np.int32), 0, [0])], block_size=n, device=self.device)
+        self.model.forward(plan, out.data_ptr(), n, stream=stream)
+        out._plan = plan  # metadata lifetime follows the output
+        return out
+
+    # -------------------------------------------------------------- query prefill
+    def prefill(self, requests: Sequence[QueryRequest], stream: torch.cuda.Stream | None = None):
+        """Batched prefill over cached prefixes -> (logits [S,V] fp32, next_token [S] int32)."""
+        pool = self.pool
+        seqs, owned = [], []
+        try:
+            for r in requests:
+                blocks = pool.alloc(r.n_cached + len(r.new_tokens))
+                owned.append(blocks)
+                seqs.append(SeqPlan(np.asarray(r.new_tokens, np.int32), r.n_cached, blocks))
+            plan = BatchPlan(seqs, pool.block_size, self.device)
+            jobs = [(r.cached_payload, r.n_cached, i * plan.bt_stride)
+                    for i, r in enumerate(requests) if r.n_cached > 0]
+            if jobs:
+                kv_unpack(pool, jobs, _bt_view(plan), stream=stream)
+            S = len(requests)
+            logits = torch.empty(S, self.spec.vocab, dtype=torch.float32, device=self.device)
+            nxt = torch.empty(S, dtype=torch.int32, device=self.device)
+            self.model.forward(plan, pool.data.data_ptr(), pool.slots, logits, nxt, stream=stream)
+            return logits, nxt
+        finally:
+            for b in owned:
+                pool.release(b)
+
+
+def _bt_view(plan: BatchPlan) -> torch.Tensor:
+    off = (plan.ptr["block_table"] - plan.meta.data_ptr()) // 4
+    return plan.meta[off: off + plan.n_seqs * plan.bt_stride]
