@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""Benchmark of the Shared RAG-DCache hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "C2"): Llama-3.2-1B-shaped random-init
+model, queries of 5 retrieved documents x 512 tokens + a 64-token query, doc
+ids drawn Zipf(1.0) over a 10k-doc corpus (workload.zipf_stream).  Every
+query's ordered 5-document combination is a *warm* cache entry (generated at
+queue time by the KV generator), so serving = load the composite prefix KV +
+prefill the 64 query tokens over it + first-token logits.
+
+A step = one batch of --batch queries per GPU through that path.
+  value  queries/s with the cached KV already resident in HBM (placement hit):
+         K3 unpack -> cached-prefix prefill -> LM head/argmax.
+  e2e    queries/s through the public API (prefill.prefill_batch) from the
+         pinned host memory tier: payload + token H2D copies, unpack, prefill,
+         D2H of the first tokens, all inside the timed region.
+N GPUs = N independent instances (one process each, weak scaling: each rank
+serves its own shard of the query stream, no data-path collective); timing is
+device-side, max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "RAG TTFT p50/p99 and queries/sec at 1/2/4/8 B200; KV load GB/s vs HBM peak"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--model", default="llama-3.2-1b")
+    ap.add_argument("--batch", type=int, default=32, help="queries per step per GPU")
+    ap.add_argument("--k", type=int, default=5)
+    ap.add_argument("--doc-tokens", type=int, default=512)
+    ap.add_argument("--q-tokens", type=int, default=64)
+    ap.add_argument("--no-extras", action="store_true", help="skip TTFT percentiles / cold / full-prefill legs")
+    return ap.parse_args()
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "bf16": d["bf16_tflops"], "bf16_sus": d.get("bf16_tflops_sustained"),
+                "src": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16": 1590.0, "bf16_sus": 1400.0, "src": "fallback"}
+
+
+def _config(a, n):
+    return {
+        "workload": f"C2 {a.model}-shaped random-init, {a.k} docs x {a.doc_tokens} tok + {a.q_tokens}-tok query, "
+                    f"warm composite-prefix KV cache, Zipf(1.0) over 10k docs",
+        "queries_per_step_per_gpu": a.batch, "global_queries_per_step": a.batch * n,
+        "docs_per_query": a.k, "doc_tokens": a.doc_tokens, "query_tokens": a.q_tokens,
+        "cached_tokens_per_query": a.k * a.doc_tokens, "parallelism": f"replicas x{n} (one instance per GPU)",
+        "l2_policy": "inputs exceed L2: each step reads >2 GB of KV plus 2.5 GB of weights (126 MB L2)",
+    }
+
+
+# ----------------------------------------------------------------- distributed plumbing
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        dist.init_process_group(backend=backend)
+    return ws, rank, local
+
+
+def _barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def _max_over_ranks(x: float, ws: int, device) -> float:
+    if ws == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """NVML sampling of SM clock and clock-event reasons during the timed
+    region (the B200_PROFILING.md clocks line, via pynvml instead of a pipe)."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, index: int, period_s: float = 0.02):
+        self.index, self.period, self.rows = index, period_s, []
+        self._stop = threading.Event()
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self.th = threading.Thread(target=self._run, daemon=True)
+            self.th.start()
+        except Exception:  # no NVML: report unavailable
+            self._nv = None
+        return self
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.rows.append((sm, rs))
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._nv is not None:
+            self.th.join(timeout=1)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        reasons = sorted({n for _, r in self.rows for n, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(sm for sm, _ in self.rows), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------- CPU baseline (oracle port)
+
+def cpu_reference_qps(spec, a, n_queries: int, weights=None, budget_s: float = 20.0):
+    """The reference path on the host CPU: memory-tier hit (no I/O, reference
+    store.py:254-258) + prefill of the query over the cached prefix, computed
+    by the fp32 oracle restatement (oracle/llama_ref.py) with all host threads."""
+    from oracle.llama_ref import OracleModel
+    from paper_2504_11765_b200.model import init_weights, query_tokens
+
+    cores = os.cpu_count() or 1
+    torch.set_num_threads(cores)
+    if weights is None:
+        weights = init_weights(spec, seed=0, device="cpu")
+    orc = OracleModel(weights)
+    n_cached = a.k * a.doc_tokens
+    g = torch.Generator().manual_seed(0)
+    past = torch.randn(spec.layers, 2, spec.kv_heads, n_cached, spec.head_dim, generator=g)
+    times = []
+    t_end = time.perf_counter() + budget_s
+    for i in range(n_queries):
+        toks = query_tokens(10_000 + i, a.q_tokens, spec.vocab)
+        t0 = time.perf_counter()
+        orc.forward(toks, past, n_cached)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end:
+            break
+    return {"qps": len(times) / sum(times), "cores": cores, "n": len(times),
+            "sample": f"{len(times)} queries, fp32 oracle port, {a.q_tokens} new tokens over {n_cached} cached"}
+
+
+def run_reference(a):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    from paper_2504_11765_b200.model import get_spec
+    spec = get_spec(a.model)
+    from paper_2504_11765_b200.model import init_weights
+    weights = init_weights(spec, seed=0, device="cpu")
+    cpu_reference_qps(spec, a, max(a.warmup, 1), weights, budget_s=30.0)  # warm-up
+    r = cpu_reference_qps(spec, a, a.steps, weights, budget_s=90.0)
+    qps = r["qps"]
+    line = {
+        "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": a.gpus, "steps": r["n"], "warmup": a.warmup,
+        "ms_per_step": 1e3 / qps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (random-init weights, splitmix64 token ids)",
+        "config": _config(a, 1), "impl": "reference",
+        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": r["cores"], "kind": "port",
+                         "sample": r["sample"]},
+        "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- our arm
+
+def run_ours(a):
+    from paper_2504_11765_b200.engine import Engine
+    from paper_2504_11765_b200.generator import KvGenerator
+    from paper_2504_11765_b200.model import get_spec, query_tokens
+    from paper_2504_11765_b200.prefill import PrefillRequest, prefill_batch
+    from paper_2504_11765_b200.store import KvKey, KvStore, LookupResult, Outcome
+    from paper_2504_11765_b200.workload import zipf_stream
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    spec = get_spec(a.model)
+    B, k = a.batch, a.k
+    n_ctx = k * a.doc_tokens + a.q_tokens
+    comp_bytes = spec.kv_bytes_per_token() * k * a.doc_tokens
+    eng = Engine(spec, seed=0, device=dev, pool_tokens=B * (n_ctx + 64) + 4096,
+                 device_cache_bytes=(B + 4) * comp_bytes)
+    gen = KvGenerator(eng, keep_on_device=True)
+    # this rank's shard of the query stream (weak scaling)
+    items = zipf_stream(10_000, 1.0, B * ws, seed=1, k=k, q_tokens=a.q_tokens, doc_tokens=a.doc_tokens)[rank::ws]
+    prof = spec.profile()
+    blobs, keys, qtoks = [], [], []
+    for it in items:
+        key = KvKey(prof.model_hash, it.doc_ids)
+        blobs.append(gen.generate(it.doc_ids, it.doc_tokens))     # warm: queue-time precompute
+        keys.append(key)
+        qtoks.append(query_tokens(it.query_id, a.q_tokens, spec.vocab))
+    torch.cuda.synchronize()
+
+    def requests(use_device_cache: bool, order):
+        return [PrefillRequest(LookupResult(Outcome.MEMORY_HIT, blobs[i], 0), None, qtoks[i],
+                               keys[i] if use_device_cache else None) for i in order]
+
+    rng = np.random.default_rng(rank)
+    orders = [rng.permutation(len(items)) for _ in range(a.warmup + a.steps)]
+
+    # ---------------- value: HBM-resident cached KV
+    for s in range(a.warmup):
+        prefill_batch(eng, requests(True, orders[s]), timed=False)
+    torch.cuda.synchronize()
+    unpack_ev = []
+    eng.model.collect()
+    eng.model.profile(True)
+    _barrier(ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        e0.record()
+        for s in range(a.steps):
+            prefill_batch(eng, requests(True, orders[a.warmup + s]), timed=False, unpack_events=unpack_ev)
+        e1.record()
+        torch.cuda.synchronize()
+    _barrier(ws)
+    eng.model.profile(False)
+    classes = eng.model.collect()
+    t_value = _max_over_ranks(e0.elapsed_time(e1) / 1e3, ws, dev)
+    unpack_ms = sum(x.elapsed_time(y) for x, y in unpack_ev)
+    unpack_bytes = 2 * comp_bytes * B * a.steps          # read + write, algorithmic
+    value = B * ws * a.steps / t_value
+
+    # ---------------- e2e: public API from the pinned host tier
+    for s in range(a.warmup):
+        r = prefill_batch(eng, requests(False, orders[s]), timed=False)
+        r.next_token.cpu()
+    _barrier(ws)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for s in range(a.steps):
+        r = prefill_batch(eng, requests(False, orders[a.warmup + s]), timed=False)
+        first = r.next_token.cpu()                          # D2H read of the step's result
+    torch.cuda.synchronize()
+    t_e2e = _max_over_ranks(time.perf_counter() - t0, ws, dev)
+    e2e = B * ws * a.steps / t_e2e
+    h2d = B * comp_bytes + 4 * (B * (a.q_tokens * 3 + 8)) + 24 * B
+    d2h = first.numel() * first.element_size()
+
+    # ---------------- roofline of the dominant kernel class
+    pk = _peaks()
+    shares = {c: v["ms"] for c, v in classes.items()}
+    shares["kv_unpack"] = unpack_ms
+    dom = max(shares, key=shares.get)
+    if dom == "kv_unpack":
+        ach = unpack_bytes / (unpack_ms / 1e3) / 1e9
+        roof = {"kernel": "K3 kv_unpack", "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s"}
+    else:
+        c = classes[dom]
+        ach = c["flops"] / (c["ms"] / 1e3) / 1e12
+        peak = pk["bf16_sus"] or pk["bf16"]
+        roof = {"kernel": f"{dom} ({c['launches']} launches)", "bound": "tensor", "achieved": ach, "peak": peak,
+                "unit": "TFLOP/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["peak_source"] = pk["src"] + (" sustained" if roof["bound"] == "tensor" else "")
+    roof["traffic"] = _traffic_from_profiles(roof["kernel"])
+    launches = sum(v["launches"] for v in classes.values()) + len(unpack_ev)
+
+    out = {
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": ws, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": t_value / a.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (random-init weights, splitmix64 token ids, Zipf doc ids)",
+        "config": _config(a, ws),
+        "e2e": {"value": e2e, "unit": "queries/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "roofline": roof,
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+        "kernel_ms_per_step": {c: v / a.steps for c, v in shares.items()},
+        "kv_load": {"unpack_gbps": unpack_bytes / (unpack_ms / 1e3) / 1e9 if unpack_ms else None,
+                    "hbm_peak_gbs": pk["hbm_gbs"],
+                    "unpack_frac": (unpack_bytes / (unpack_ms / 1e3) / 1e9) / pk["hbm_gbs"] if unpack_ms else None},
+    }
+    if not a.no_extras:
+        out.update(_extras(a, eng, gen, spec, items, blobs, keys, qtoks, ws, rank, dev))
+    if rank == 0 and ws == 1:
+        cb = cpu_reference_qps(spec, a, 6, eng.weights, budget_s=20.0) if os.environ.get("RDKV_SKIP_CPU") != "1" else None
+        out["cpu_baseline"] = ({"value": cb["qps"], "unit": "queries/s", "cores": cb["cores"], "kind": "port",
+                                "sample": cb["sample"]} if cb else None)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def _traffic_from_profiles(kernel: str):
+    """dram bytes per launch from a committed ncu --set full capture, if any."""
+    p = ROOT / "profiles" / "traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    for name, v in d.items():
+        if name.split()[0] in kernel:
+            return v
+    return None
+
+
+def _extras(a, eng, gen, spec, items, blobs, keys, qtoks, ws, rank, dev):
+    """Single-query TTFT percentiles (warm HBM / warm host / cold disk / full prefill)
+    and batched full-prompt throughput on the same GPU."""
+    from paper_2504_11765_b200.prefill import PrefillRequest, prefill_batch
+    from paper_2504_11765_b200.model import combo_tokens
+    from paper_2504_11765_b200.store import KvStore, LookupResult, Outcome
+    from paper_2504_11765_b200 import _lib
+
+    def pct(xs):
+        xs = np.asarray(xs) * 1e3
+        return {"p50": float(np.percentile(xs, 50)), "p99": float(np.percentile(xs, 99)), "n": int(len(xs))}
+
+    def one(req):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = prefill_batch(eng, [req], timed=False)
+        int(r.next_token[0])
+        return time.perf_counter() - t0
+
+    n = len(items)
+    res = {}
+    hit = lambda i, dc: PrefillRequest(LookupResult(Outcome.MEMORY_HIT, blobs[i], 0), None, qtoks[i],
+                                       keys[i] if dc else None)
+    for _ in range(3):
+        one(hit(0, True))
+    res["warm_hbm"] = pct([one(hit(i % n, True)) for i in range(40)])
+    res["warm_host"] = pct([one(hit(i % n, False)) for i in range(40)])
+    full = lambda i: PrefillRequest(LookupResult(Outcome.MISS), combo_tokens(items[i].doc_ids, items[i].doc_tokens,
+                                                                             spec.vocab), qtoks[i])
+    for _ in range(2):
+        one(full(0))
+    res["full_prefill"] = pct([one(full(i % n)) for i in range(20)])
+    # cold: DISK_HIT through the store after dropping the page cache (FNV-verified decode)
+    root = Path(tempfile.mkdtemp(prefix=f"rdkv_bench_{rank}_"))
+    try:
+        store = KvStore(root, memory_capacity_bytes=0)
+        cold = []
+        for i in range(min(4, n)):
+            store.put(keys[i], blobs[i])
+            p = str(store.path_of(keys[i])).encode()
+            _lib.lib().rdkv_drop_page_cache(p)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            look = store.get(keys[i])
+            r = prefill_batch(eng, [PrefillRequest(look, None, qtoks[i], None)], timed=False)
+            int(r.next_token[0])
+            cold.append(time.perf_counter() - t0)
+        res["cold_disk"] = pct(cold)
+    finally:
+        import shutil
+        shutil.rmtree(root, ignore_errors=True)
+    # batched full-prompt prefill throughput (the no-cache baseline on the same GPU)
+    fb = [full(i) for i in range(min(len(items), a.batch))]
+    prefill_batch(eng, fb, timed=False)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    reps = 2
+    for _ in range(reps):
+        prefill_batch(eng, fb, timed=False)
+    torch.cuda.synchronize()
+    full_qps = len(fb) * reps / (time.perf_counter() - t0)
+    return {"ttft_ms": res, "full_prefill_qps_per_gpu": full_qps}
+
+
+def main():
+    a = _args()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -225,6 +225,24 @@ RDKV_API size_t rdkv_workspace_bytes(const rdkv_model* model, int n_tokens, int 
 RDKV_API int rdkv_forward(rdkv_model* model, const rdkv_batch* batch, void* workspace,
                           size_t workspace_bytes, void* stream);
 
+/* ------------------------------------------------------------ measurement */
+
+/* Kernel classes of rdkv_forward for per-class device timing. */
+#define RDKV_PROF_GEMM 0 /* K1 layer GEMMs: QKV, O, gate/up, down           */
+#define RDKV_PROF_ATTN 1 /* K2/K4 attention                                  */
+#define RDKV_PROF_MISC 2 /* embedding gather, RMSNorm                         */
+#define RDKV_PROF_HEAD 3 /* K5 LM-head GEMM + argmax                          */
+#define RDKV_PROF_N 4
+
+/* With on != 0, every kernel rdkv_forward launches is bracketed by CUDA events
+ * on its stream.  Launch and algorithmic-FLOP counters run regardless. */
+RDKV_API int rdkv_profile_enable(rdkv_model* model, int on);
+
+/* Wait for the recorded launches and return, per class, the summed device
+ * milliseconds (ms), kernel launches and GEMM FLOPs (2*M*N*K) since the last
+ * collect; resets the counters.  Arrays hold RDKV_PROF_N entries. */
+RDKV_API int rdkv_profile_collect(rdkv_model* model, double* ms, int64_t* launches, double* flops);
+
 #ifdef __cplusplus
 }
 #endif

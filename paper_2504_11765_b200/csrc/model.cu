@@ -22,7 +22,53 @@ struct rdkv_model {
   std::vector<const void*> w;  // see rdkv.h for the order
   float* rope = nullptr;        // [max_pos][dh/2] (cos, sin)
   int device = 0;
+  // measurement (rdkv_profile_*)
+  bool prof = false;
+  struct Rec {
+    int cat;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> spare;
+  int64_t launches[RDKV_PROF_N] = {0, 0, 0, 0};
+  double flops[RDKV_PROF_N] = {0, 0, 0, 0};
+
+  cudaEvent_t event() {
+    if (!spare.empty()) {
+      cudaEvent_t e = spare.back();
+      spare.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
 };
+
+namespace {
+// Brackets one launch: counts it and, when profiling, records events around it.
+struct ProfScope {
+  rdkv_model* m;
+  int cat;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  ProfScope(rdkv_model* m_, int cat_, cudaStream_t st_, double fl = 0.0) : m(m_), cat(cat_), st(st_) {
+    m->launches[cat] += 1;
+    m->flops[cat] += fl;
+    if (m->prof) {
+      a = m->event();
+      cudaEventRecord(a, st);
+    }
+  }
+  ~ProfScope() {
+    if (m->prof) {
+      cudaEvent_t b = m->event();
+      cudaEventRecord(b, st);
+      m->recs.push_back({cat, a, b});
+    }
+  }
+};
+}  // namespace
 
 namespace rdkv {
 namespace {
@@ -64,6 +110,12 @@ inline const float* G(const rdkv_model* m, int i) { return static_cast<const flo
 }  // namespace rdkv
 
 using namespace rdkv;
+
+#define LAUNCH(cat, fl, expr)            \
+  do {                                   \
+    ProfScope _ps(m, (cat), st, (fl));   \
+    RDKV_TRY(expr);                      \
+  } while (0)
 
 extern "C" {
 
@@ -107,6 +159,11 @@ int rdkv_model_create(const rdkv_model_desc* desc, const void* const* weights, s
 
 void rdkv_model_destroy(rdkv_model* m) {
   if (!m) return;
+  for (auto& r : m->recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : m->spare) cudaEventDestroy(e);
   cudaFree(m->rope);
   delete m;
 }
@@ -130,13 +187,13 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
   const long long plane = (long long)hkv * b->kv_slots * dh;  // elements per (layer, k|v) plane
   auto* kv = static_cast<__nv_bfloat16*>(b->kv_base);
 
-  RDKV_TRY(launch_embed(b->tokens, W(m, 0), ws.x, T, d.hidden, d.vocab, st));
+  LAUNCH(RDKV_PROF_MISC, 0.0, launch_embed(b->tokens, W(m, 0), ws.x, T, d.hidden, d.vocab, st));
   for (int l = 0; l < d.layers; ++l) {
     const int wb = 1 + RDKV_WEIGHTS_PER_LAYER * l;
     __nv_bfloat16* kpl = kv + (2LL * l) * plane;
     __nv_bfloat16* vpl = kv + (2LL * l + 1) * plane;
     // attention block
-    RDKV_TRY(launch_rmsnorm(ws.x, d.hidden, nullptr, G(m, wb + 0), ws.h, d.hidden, T, d.hidden, d.norm_eps, st));
+    LAUNCH(RDKV_PROF_MISC, 0.0, launch_rmsnorm(ws.x, d.hidden, nullptr, G(m, wb + 0), ws.h, d.hidden, T, d.hidden, d.norm_eps, st));
     GemmEpi eq{};
     eq.q = ws.q;
     eq.ldq = qd;
@@ -148,7 +205,8 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     eq.rope = m->rope;
     eq.hq = hq;
     eq.hkv = hkv;
-    RDKV_TRY(launch_gemm(ws.h, d.hidden, W(m, wb + 1), d.hidden, T, (int)((hq + 2 * hkv) * dh), d.hidden, EPI_QKV, dh,
+    LAUNCH(RDKV_PROF_GEMM, 2.0 * T * (hq + 2 * hkv) * dh * d.hidden,
+           launch_gemm(ws.h, d.hidden, W(m, wb + 1), d.hidden, T, (int)((hq + 2 * hkv) * dh), d.hidden, EPI_QKV, dh,
                          eq, st));
     AttnParams ap{};
     ap.q = ws.q;
@@ -167,30 +225,58 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     ap.hq = hq;
     ap.hkv = hkv;
     ap.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)dh));
-    RDKV_TRY(launch_attention(ap, dh, S, b->max_new, st));
+    LAUNCH(RDKV_PROF_ATTN, 0.0, launch_attention(ap, dh, S, b->max_new, st));
     GemmEpi er{};
     er.out = ws.x;
     er.ldo = d.hidden;
     er.resid = ws.x;
     er.ldr = d.hidden;
-    RDKV_TRY(launch_gemm(ws.o, qd, W(m, wb + 2), qd, T, d.hidden, (int)qd, EPI_RESID, 0, er, st));
+    LAUNCH(RDKV_PROF_GEMM, 2.0 * T * qd * d.hidden, launch_gemm(ws.o, qd, W(m, wb + 2), qd, T, d.hidden, (int)qd, EPI_RESID, 0, er, st));
     // MLP block
-    RDKV_TRY(launch_rmsnorm(ws.x, d.hidden, nullptr, G(m, wb + 3), ws.h, d.hidden, T, d.hidden, d.norm_eps, st));
+    LAUNCH(RDKV_PROF_MISC, 0.0, launch_rmsnorm(ws.x, d.hidden, nullptr, G(m, wb + 3), ws.h, d.hidden, T, d.hidden, d.norm_eps, st));
     GemmEpi eg{};
     eg.out = ws.a;
     eg.ldo = d.ffn;
-    RDKV_TRY(launch_gemm(ws.h, d.hidden, W(m, wb + 4), d.hidden, T, 2 * d.ffn, d.hidden, EPI_SWIGLU, 0, eg, st));
-    RDKV_TRY(launch_gemm(ws.a, d.ffn, W(m, wb + 5), d.ffn, T, d.hidden, d.ffn, EPI_RESID, 0, er, st));
+    LAUNCH(RDKV_PROF_GEMM, 4.0 * T * d.ffn * d.hidden, launch_gemm(ws.h, d.hidden, W(m, wb + 4), d.hidden, T, 2 * d.ffn, d.hidden, EPI_SWIGLU, 0, eg, st));
+    LAUNCH(RDKV_PROF_GEMM, 2.0 * T * d.ffn * d.hidden, launch_gemm(ws.a, d.ffn, W(m, wb + 5), d.ffn, T, d.hidden, d.ffn, EPI_RESID, 0, er, st));
   }
   if (b->want_logits) {
     if (!b->logits || !b->last_row) return set_error(RDKV_ERR_ARG, "forward: logits requested without buffers");
     const int fn = 1 + RDKV_WEIGHTS_PER_LAYER * d.layers;
-    RDKV_TRY(launch_rmsnorm(ws.x, d.hidden, b->last_row, G(m, fn), ws.hl, d.hidden, S, d.hidden, d.norm_eps, st));
+    LAUNCH(RDKV_PROF_HEAD, 0.0, launch_rmsnorm(ws.x, d.hidden, b->last_row, G(m, fn), ws.hl, d.hidden, S, d.hidden, d.norm_eps, st));
     GemmEpi el{};
     el.out = b->logits;
     el.ldo = d.vocab;
-    RDKV_TRY(launch_gemm(ws.hl, d.hidden, W(m, fn + 1), d.hidden, S, d.vocab, d.hidden, EPI_STORE_F32, 0, el, st));
-    if (b->next_token) RDKV_TRY(launch_argmax(b->logits, d.vocab, S, d.vocab, b->next_token, st));
+    LAUNCH(RDKV_PROF_HEAD, 2.0 * S * d.vocab * d.hidden, launch_gemm(ws.hl, d.hidden, W(m, fn + 1), d.hidden, S, d.vocab, d.hidden, EPI_STORE_F32, 0, el, st));
+    if (b->next_token) LAUNCH(RDKV_PROF_HEAD, 0.0, launch_argmax(b->logits, d.vocab, S, d.vocab, b->next_token, st));
+  }
+  return 0;
+}
+
+int rdkv_profile_enable(rdkv_model* m, int on) {
+  if (!m) return set_error(RDKV_ERR_ARG, "profile_enable: null model");
+  m->prof = on != 0;
+  return 0;
+}
+
+int rdkv_profile_collect(rdkv_model* m, double* ms, int64_t* launches, double* flops) {
+  if (!m) return set_error(RDKV_ERR_ARG, "profile_collect: null model");
+  double acc[RDKV_PROF_N] = {0, 0, 0, 0};
+  for (auto& r : m->recs) {
+    CUDA_TRY(cudaEventSynchronize(r.b));
+    float t = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&t, r.a, r.b));
+    acc[r.cat] += t;
+    m->spare.push_back(r.a);
+    m->spare.push_back(r.b);
+  }
+  m->recs.clear();
+  for (int c = 0; c < RDKV_PROF_N; ++c) {
+    if (ms) ms[c] = acc[c];
+    if (launches) launches[c] = m->launches[c];
+    if (flops) flops[c] = m->flops[c];
+    m->launches[c] = 0;
+    m->flops[c] = 0;
   }
   return 0;
 }

@@ -21,8 +21,10 @@ All GPU work goes through librdkv's C ABI; there is no PyTorch compute path.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
-from collections import deque
+import threading
+from collections import OrderedDict, deque
 from dataclasses import dataclass
 from typing import Sequence
 
@@ -62,7 +64,12 @@ _N_SIG = {
     "rdkv_forward": (C.c_int, [C.c_void_p, C.POINTER(RdkvBatch), C.c_void_p, C.c_size_t, C.c_void_p]),
     "rdkv_kv_unpack": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int,
                                  C.c_int, C.c_int64, C.c_int, C.c_void_p]),
+    "rdkv_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
+    "rdkv_profile_collect": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                                       C.POINTER(C.c_double)]),
 }
+
+PROF_CLASSES = ("gemm", "attention", "norm_embed", "lm_head")
 
 
 def _L():
@@ -73,6 +80,10 @@ def _L():
             fn.restype, fn.argtypes = res, args
         lib._engine_sigs = True
     return lib
+
+
+def _nullctx():
+    return contextlib.nullcontext()
 
 
 def _stream_ptr(stream: torch.cuda.Stream | None) -> int:
@@ -225,6 +236,15 @@ class DeviceModel:
             self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
         return self._ws
 
+    def profile(self, on: bool) -> None:
+        _lib.check(_L().rdkv_profile_enable(self._h, 1 if on else 0))
+
+    def collect(self) -> dict[str, dict]:
+        """Per kernel class since the last collect: device ms, launches, GEMM FLOPs."""
+        ms, n, fl = (C.c_double * 4)(), (C.c_int64 * 4)(), (C.c_double * 4)()
+        _lib.check(_L().rdkv_profile_collect(self._h, ms, n, fl))
+        return {k: {"ms": ms[i], "launches": int(n[i]), "flops": fl[i]} for i, k in enumerate(PROF_CLASSES)}
+
     def forward(self, plan: BatchPlan, kv_base: int, kv_slots: int, logits=None, next_token=None,
                 stream: torch.cuda.Stream | None = None) -> None:
         ws = self.workspace(plan.n_tokens, plan.n_seqs)
@@ -266,17 +286,62 @@ class QueryRequest:
     n_cached: int = 0
 
 
+class DeviceKvCache:
+    """HBM placement cache: KvKey -> device payload, byte-bounded LRU.
+
+    Purely a *placement* layer under the store: the logical outcome of every
+    access (MEMORY_HIT / DISK_HIT / MISS and its accounting) is still decided
+    by the KvStore; this only changes where the bytes are copied from
+    (SURVEY §8e invariant)."""
+
+    def __init__(self, capacity_bytes: int) -> None:
+        self.capacity = capacity_bytes
+        self.used = 0
+        self._d: "OrderedDict" = OrderedDict()
+        self._lock = threading.Lock()
+
+    def get(self, key) -> torch.Tensor | None:
+        with self._lock:
+            t = self._d.get(key)
+            if t is not None:
+                self._d.move_to_end(key)
+            return t
+
+    def put(self, key, t: torch.Tensor) -> None:
+        n = t.numel() * t.element_size()
+        with self._lock:
+            if key in self._d or n > self.capacity:
+                return
+            while self._d and self.used + n > self.capacity:
+                _, old = self._d.popitem(last=False)
+                self.used -= old.numel() * old.element_size()
+            self._d[key] = t
+            self.used += n
+
+    def __contains__(self, key) -> bool:
+        with self._lock:
+            return key in self._d
+
+
 class Engine:
     """Model instance bound to one GPU."""
 
     def __init__(self, spec: ModelSpec, weights: ModelWeights | None = None, seed: int = 0, device="cuda",
-                 pool_tokens: int = 1 << 16, block_size: int = 64) -> None:
+                 pool_tokens: int = 1 << 16, block_size: int = 64, device_cache_bytes: int = 0) -> None:
         self.device = torch.device(device)
         self.spec = spec
         self.weights = weights if weights is not None else init_weights(spec, seed, self.device)
         self.model = DeviceModel(self.weights)
         self.pool = KvPool(spec, (pool_tokens + block_size - 1) // block_size, block_size, self.device)
         self.copy_stream = torch.cuda.Stream(device=self.device)
+        self.device_cache = DeviceKvCache(device_cache_bytes)
+
+    def stage(self, payload: torch.Tensor, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """Async H2D copy of a pinned host payload; returns the device bf16 view."""
+        dev = torch.empty(payload.numel(), dtype=torch.uint8, device=self.device)
+        with torch.cuda.stream(stream) if stream is not None else _nullctx():
+            dev.copy_(payload, non_blocking=True)
+        return dev.view(torch.bfloat16)
 
     # -------------------------------------------------------------- generation
     def generate_doc_kv(self, tokens: np.ndarray, out: torch.Tensor | None = None,

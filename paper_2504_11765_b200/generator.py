@@ -1,0 +1,64 @@
+"""The KV generator plugin: ``generate() -> KvBlob`` backed by B200 prefill.
+
+Replaces the reference's generator stand-in ``synth_blob`` (codec.py:188-224)
+at its two call sites, ``prefetch.prepare`` (prefetch.py:150-152) and
+``cli precompute`` (cli.py:161), under the plugin contract of
+``SharedCacheService.get_or_generate`` (service.py:87-92): deterministic per
+key, header matching the key, exceptions propagate to every waiter.
+
+A call runs the document prefill over the ordered combination's concatenated
+tokens (positions 0..n-1, prefetch.py:6-8) on the engine's GPU; the payload is
+written by the QKV epilogue directly in the `.rdkv` layout, copied once into
+pinned host memory (the memory tier's DMA-ready form), FNV-1a-hashed natively
+and wrapped without re-hashing.  The device copy stays in the engine's HBM
+placement cache so a query dispatched to the same GPU skips the H2D copy.
+"""
+
+from __future__ import annotations
+
+from typing import Callable, Sequence
+
+import numpy as np
+import torch
+
+from .codec import KvBlob, fnv1a64, make_header
+from .engine import Engine
+from .model import combo_tokens
+from .store import KvKey
+
+
+class KvGenerator:
+    def __init__(self, engine: Engine, token_seed: int = 0, keep_on_device: bool = True) -> None:
+        self.engine = engine
+        self.profile = engine.spec.profile()
+        self.token_seed = token_seed
+        self.keep_on_device = keep_on_device
+
+    def tokens(self, doc_ids: Sequence[int], doc_token_counts: Sequence[int]) -> np.ndarray:
+        return combo_tokens(doc_ids, doc_token_counts, self.engine.spec.vocab, self.token_seed)
+
+    def generate(self, doc_ids: Sequence[int], doc_token_counts: Sequence[int]) -> KvBlob:
+        ids = tuple(int(d) for d in doc_ids)
+        if not ids:
+            raise ValueError("doc_ids must be non-empty")
+        toks = self.tokens(ids, doc_token_counts)
+        if len(toks) < 1:
+            raise ValueError("token_count must be >= 1")
+        eng = self.engine
+        with torch.cuda.device(eng.device):
+            kv = eng.generate_doc_kv(toks)
+            raw = kv.view(torch.uint8)
+            host = torch.empty(raw.numel(), dtype=torch.uint8, pin_memory=True)
+            host.copy_(raw, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        header = make_header(self.profile, ids, len(toks), fnv1a64(host))
+        if self.keep_on_device:
+            eng.device_cache.put(KvKey(self.profile.model_hash, ids), kv)
+        return KvBlob.trusted(header, host)
+
+    def for_prefix(self, doc_ids: Sequence[int], doc_token_counts: Sequence[int]) -> Callable[[], KvBlob]:
+        """The ``generate`` callable for one key (prefetch.prepare / get_or_generate)."""
+        ids, counts = tuple(doc_ids), tuple(doc_token_counts)
+        return lambda: self.generate(ids, counts)
+
+    __call__ = for_prefix

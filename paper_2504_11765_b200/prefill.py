@@ -1,0 +1,113 @@
+"""Prefill-with-cached-prefix: the measured counterpart of ``costs.ttft``.
+
+Reference semantics (costs.py:121-144, sim.py:414-436): the longest cached
+prefix of the query's ordered document combination is loaded from the tier
+the lookup reports, and only the *new* tokens — the uncached documents, then
+the query (sim.py:420-422) — are prefilled, attending over the whole context
+(costs.py:89-99).  On a MISS the would-be-cached tokens are plain text and join
+the prefill (costs.py:136-138).
+
+Here the load is real (pinned host payload -> HBM on a side stream, then the
+K3 unpack into the paged pool; or straight from the HBM placement cache) and
+so is the prefill (tcgen05 GEMMs + attention + LM head).  Both halves are
+timed with CUDA events and returned as the reference's
+``(seconds, TtftBreakdown(kv_load, prefill))`` plus the first-token logits.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from .costs import TtftBreakdown
+from .engine import BatchPlan, Engine, SeqPlan, _bt_view, kv_unpack
+from .store import KvKey, LookupResult, Outcome
+
+
+@dataclass
+class PrefillRequest:
+    lookup: LookupResult              # outcome of store.get for the longest cached prefix (MISS if none)
+    prefix_tokens: np.ndarray         # tokens of that prefix combination (raw text on a miss)
+    new_tokens: np.ndarray            # remaining documents, then the query
+    key: KvKey | None = None          # enables the HBM placement cache
+
+
+@dataclass
+class PrefillResult:
+    ttft: float
+    breakdown: TtftBreakdown
+    logits: torch.Tensor              # [S, V] fp32 on the device
+    next_token: torch.Tensor          # [S] int32 on the device
+
+
+def prefill_batch(engine: Engine, requests: Sequence[PrefillRequest], timed: bool = True,
+                  unpack_events: list | None = None) -> PrefillResult:
+    """Serve a batch of queries on one engine; kv_load / prefill are the
+    device-measured durations of the whole batch's load and prefill phases.
+    ``unpack_events`` collects (start, end) CUDA events around the K3 launch."""
+    pool = engine.pool
+    main = torch.cuda.current_stream(engine.device)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if timed else None
+    if timed:
+        ev[0].record(main)
+    seqs, owned, jobs, staged = [], [], [], []
+    # staging buffers are allocated on `main`; the copy stream must not write
+    # them before main's earlier users of that memory are done
+    engine.copy_stream.wait_stream(main)
+    try:
+        for i, r in enumerate(requests):
+            hit = r.lookup.outcome is not Outcome.MISS
+            n_cached = int(r.lookup.blob.header.token_count) if hit else 0
+            new = np.asarray(r.new_tokens, np.int32) if hit else np.concatenate(
+                [np.asarray(r.prefix_tokens, np.int32), np.asarray(r.new_tokens, np.int32)])
+            blocks = pool.alloc(n_cached + len(new))
+            owned.append(blocks)
+            seqs.append(SeqPlan(new, n_cached, blocks))
+            if hit:
+                dev = engine.device_cache.get(r.key) if r.key is not None else None
+                if dev is None:
+                    dev = engine.stage(r.lookup.blob.payload_tensor(), stream=engine.copy_stream)
+                    staged.append(dev)
+                jobs.append((dev, n_cached, i))
+        plan = BatchPlan(seqs, pool.block_size, engine.device)
+        if staged:
+            main.wait_stream(engine.copy_stream)
+        if jobs:
+            if unpack_events is not None:
+                ua, ub = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ua.record(main)
+            kv_unpack(pool, [(d, n, i * plan.bt_stride) for d, n, i in jobs], _bt_view(plan),
+                      elem_width=2, stream=main)
+            if unpack_events is not None:
+                ub.record(main)
+                unpack_events.append((ua, ub))
+        if timed:
+            ev[1].record(main)
+        S = len(requests)
+        logits = torch.empty(S, engine.spec.vocab, dtype=torch.float32, device=engine.device)
+        nxt = torch.empty(S, dtype=torch.int32, device=engine.device)
+        engine.model.forward(plan, pool.data.data_ptr(), pool.slots, logits, nxt, stream=main)
+        if timed:
+            ev[2].record(main)
+            ev[2].synchronize()
+            kv_load = ev[0].elapsed_time(ev[1]) / 1e3
+            prefill = ev[1].elapsed_time(ev[2]) / 1e3
+        else:
+            kv_load = prefill = 0.0
+        for d in staged:  # keep staging buffers alive until the stream has consumed them
+            d.record_stream(main)
+        bd = TtftBreakdown(kv_load, prefill)
+        return PrefillResult(bd.total, bd, logits, nxt)
+    finally:
+        for b in owned:
+            pool.release(b)
+
+
+def prefill_with_cached_prefix(engine: Engine, lookup: LookupResult, prefix_tokens, new_tokens,
+                               key: KvKey | None = None) -> tuple[float, TtftBreakdown, torch.Tensor, int]:
+    """Single query: (ttft seconds, TtftBreakdown, logits [V], first token)."""
+    r = prefill_batch(engine, [PrefillRequest(lookup, prefix_tokens, new_tokens, key)])
+    return r.ttft, r.breakdown, r.logits[0], int(r.next_token[0])
