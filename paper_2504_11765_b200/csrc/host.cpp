@@ -253,7 +253,8 @@ int rdkv_blob_read(const char* path, void* buf, size_t cap, size_t align, int ve
     }
     hl = kFixed + 8 * (size_t)load_le<uint16_t>(head + 14) + kTail;
   }
-  const size_t pad = (align - (hl % align)) % align;
+  // pad so that the payload lands on an absolute `align` boundary
+  const size_t pad = (align - ((reinterpret_cast<uintptr_t>(buf) + hl) % align)) % align;
   if (cap < pad + size) {
     ::close(fd);
     return set_error(RDKV_ERR_ARG, "buffer too small for %s (%zu < %zu)", path, cap, pad + size);
