@@ -8,10 +8,14 @@
 // at slot block_table[s][p / bs] * bs + p % bs, so the same code reads a
 // contiguous document blob (one block) or a paged pool.
 //
-// Tiling (FlashAttention-2 style): CTA = 64 query rows of one head, 4 warps x
-// 16 rows; K/V tiles of 64 positions double-buffered in XOR-swizzled smem via
-// cp.async; S = Q.K^T and O += P.V on mma.sync m16n8k16 bf16 with fp32
-// accumulation and an exp2-domain online softmax.
+// Tiling: a CTA owns 128 query *rows* of ONE kv head, where row r is
+// (token t0 + r / G, q-head kvh*G + r % G) and G = hq / hkv.  All G query
+// heads that share a K/V head therefore read each K/V tile once (GQA
+// packing: 4x less KV traffic than one CTA per q head).  8 warps x 16 rows;
+// K/V tiles of 64 positions in a 3-stage cp.async ring with XOR-swizzled
+// smem; S = Q.K^T and O += P.V on mma.sync m16n8k16 bf16 (fp32 accumulate)
+// with an exp2-domain online softmax.  CTAs are issued longest-first so the
+// causal tail does not straggle.
 #include <cuda_bf16.h>
 #include <cstdint>
 
@@ -21,8 +25,10 @@
 namespace rdkv {
 namespace {
 
-constexpr int BM = 64;   // query rows per CTA
-constexpr int BN = 64;   // key positions per tile
+constexpr int ROWS = 128;  // query rows per CTA
+constexpr int BN = 64;     // key positions per tile
+constexpr int STAGES = 3;
+constexpr int THREADS = 256;
 
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -62,55 +68,66 @@ __device__ __forceinline__ uint32_t swz(int row, int chunk) {
 }
 
 template <int DH>
-__global__ void __launch_bounds__(128) attn_prefill_kernel(AttnParams p) {
+__global__ void __launch_bounds__(THREADS, DH == 64 ? 2 : 1) attn_prefill_kernel(AttnParams p) {
   constexpr int CH = DH / 8;  // 16-B chunks per row
+  constexpr uint32_t TILE = BN * DH * 2;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* sQ = smem;
-  uint8_t* sK = sQ + BM * DH * 2;        // [2][BN][DH]
-  uint8_t* sV = sK + 2 * BN * DH * 2;    // [2][BN][DH]
+  uint8_t* sK = sQ + ROWS * DH * 2;        // [STAGES][BN][DH]
+  uint8_t* sV = sK + STAGES * TILE;        // [STAGES][BN][DH]
 
-  const int s = blockIdx.z, h = blockIdx.y, qb = blockIdx.x;
+  const int G = p.hq / p.hkv;
+  const int s = blockIdx.z, kvh = blockIdx.y;
+  const int qb = gridDim.x - 1 - blockIdx.x;  // longest causal rows first
   const int n_new = p.seq_new[s];
-  if (qb * BM >= n_new) return;
+  const int tok_per_cta = ROWS / G;
+  const int tok0 = qb * tok_per_cta;
+  if (tok0 >= n_new) return;
+  const int ntok = min(tok_per_cta, n_new - tok0);
+  const int nrows = ntok * G;
   const int n_cached = p.seq_cached[s];
-  const int row0 = p.seq_start[s] + qb * BM;
-  const int rows = min(BM, n_new - qb * BM);
-  const int pos0 = n_cached + qb * BM;           // position of the CTA's first row
-  const int kv_len = pos0 + rows;                // positions [0, kv_len) are needed
+  const int row_base = p.seq_start[s] + tok0;    // first token row in T
+  const int pos0 = n_cached + tok0;              // position of the CTA's first token
+  const int kv_len = pos0 + ntok;                // positions [0, kv_len) are needed
   const int n_tiles = (kv_len + BN - 1) / BN;
-  const int kvh = h / (p.hq / p.hkv);
   const __nv_bfloat16* kp = p.kplane + (long long)kvh * p.head_stride;
   const __nv_bfloat16* vp = p.vplane + (long long)kvh * p.head_stride;
   const int* bt = p.block_table + (long long)s * p.bt_stride;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  // ---- Q tile -> smem (rows beyond `rows` zero-filled)
-  for (int i = tid; i < BM * CH; i += 128) {
+  // ---- Q tile -> smem: row r = (token r/G, head kvh*G + r%G); rows >= nrows zero-filled
+  for (int i = tid; i < ROWS * CH; i += THREADS) {
     const int r = i / CH, c = i % CH;
-    const bool ok = r < rows;
-    const __nv_bfloat16* src = p.q + (long long)(row0 + (ok ? r : 0)) * p.ldq + (long long)h * DH + c * 8;
+    const bool ok = r < nrows;
+    const int rr = ok ? r : 0;
+    const __nv_bfloat16* src =
+        p.q + (long long)(row_base + rr / G) * p.ldq + (long long)(kvh * G + rr % G) * DH + c * 8;
     cp_async16(saddr(sQ) + swz<DH>(r, c), src, ok);
   }
   auto load_kv = [&](int tile, int buf) {
-    for (int i = tid; i < BN * CH; i += 128) {
+    for (int i = tid; i < BN * CH; i += THREADS) {
       const int r = i / CH, c = i % CH;
       const int pos = tile * BN + r;
       const bool ok = pos < kv_len;
       long long slot = 0;
       if (ok) slot = (long long)bt[pos / p.block_size] * p.block_size + pos % p.block_size;
-      const uint32_t off = (uint32_t)(buf * BN * DH * 2) + swz<DH>(r, c);
+      const uint32_t off = (uint32_t)buf * TILE + swz<DH>(r, c);
       cp_async16(saddr(sK) + off, kp + slot * DH + c * 8, ok);
       cp_async16(saddr(sV) + off, vp + slot * DH + c * 8, ok);
     }
   };
   load_kv(0, 0);
-  cp_commit();
+  cp_commit();                       // group: Q + tile 0
+  if (n_tiles > 1) load_kv(1, 1);
+  cp_commit();                       // group: tile 1 (possibly empty)
 
-  // ---- per-warp state
+  // ---- per-warp state: rows g and g+8 of this warp's 16
   const int g = lane >> 2, c4 = lane & 3;
-  const int qpos_a = pos0 + warp * 16 + g;     // rows g and g+8 of this warp
-  const int qpos_b = qpos_a + 8;
-  const int warp_max_pos = pos0 + warp * 16 + 15;
+  const int wr = warp * 16;
+  const int qpos_a = pos0 + (wr + g) / G;
+  const int qpos_b = pos0 + (wr + g + 8) / G;
+  const int warp_min_pos = pos0 + wr / G;
+  const int warp_max_pos = pos0 + (wr + 15) / G;
   float m_a = -INFINITY, m_b = -INFINITY, l_a = 0.f, l_b = 0.f;
   float o[DH / 8][4];
 #pragma unroll
@@ -118,27 +135,25 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(AttnParams p) {
   uint32_t qf[DH / 16][4];
 
   for (int tile = 0; tile < n_tiles; ++tile) {
-    const int buf = tile & 1;
-    if (tile + 1 < n_tiles) load_kv(tile + 1, buf ^ 1);
+    const int buf = tile % STAGES;
+    if (tile + 2 < n_tiles) load_kv(tile + 2, (tile + 2) % STAGES);
     cp_commit();
-    cp_wait<1>();
+    cp_wait<2>();
     __syncthreads();
     if (tile == 0) {
-      // Q fragments: 16 rows x DH for this warp
 #pragma unroll
       for (int kk = 0; kk < DH / 16; ++kk) {
-        const int r = warp * 16 + (lane & 15);
+        const int r = wr + (lane & 15);
         const int c = kk * 2 + (lane >> 4);
         ldsm_x4(saddr(sQ) + swz<DH>(r, c), qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3]);
       }
     }
-    if (tile * BN <= warp_max_pos) {  // tile has keys visible to this warp
-      const uint32_t kb = saddr(sK) + buf * BN * DH * 2;
-      const uint32_t vb = saddr(sV) + buf * BN * DH * 2;
+    if (tile * BN <= warp_max_pos && wr < nrows) {  // this tile holds keys visible to the warp
+      const uint32_t kb = saddr(sK) + buf * TILE;
+      const uint32_t vb = saddr(sV) + buf * TILE;
       float sc[BN / 8][4];
 #pragma unroll
       for (int j = 0; j < BN / 8; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
-      // S = Q K^T
 #pragma unroll
       for (int kk = 0; kk < DH / 16; ++kk) {
 #pragma unroll
@@ -151,8 +166,7 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(AttnParams p) {
           mma16816(sc[2 * jj + 1], qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3], b2, b3);
         }
       }
-      // causal + length mask, only where the tile crosses this warp's rows
-      const bool need_mask = (tile * BN + BN - 1) > (pos0 + warp * 16) || (tile * BN + BN) > kv_len;
+      const bool need_mask = (tile * BN + BN - 1) > warp_min_pos || (tile * BN + BN) > kv_len;
       float mx_a = m_a, mx_b = m_b;
 #pragma unroll
       for (int j = 0; j < BN / 8; ++j) {
@@ -198,7 +212,6 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(AttnParams p) {
         o[i][2] *= corr_b;
         o[i][3] *= corr_b;
       }
-      // O += P V
 #pragma unroll
       for (int kk = 0; kk < BN / 16; ++kk) {
         const uint32_t a0 = pack2(sc[2 * kk][0], sc[2 * kk][1]);
@@ -227,27 +240,29 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(AttnParams p) {
   l_b += __shfl_xor_sync(0xffffffff, l_b, 2);
   const float inv_a = l_a > 0.f ? 1.f / l_a : 0.f;
   const float inv_b = l_b > 0.f ? 1.f / l_b : 0.f;
-  const int ra = warp * 16 + g, rb = ra + 8;
-  __nv_bfloat16* oa = p.o + (long long)(row0 + ra) * p.ldo + (long long)h * DH;
-  __nv_bfloat16* ob = p.o + (long long)(row0 + rb) * p.ldo + (long long)h * DH;
+  const int ra = wr + g, rb = ra + 8;
+  __nv_bfloat16* oa = p.o + (long long)(row_base + ra / G) * p.ldo + (long long)(kvh * G + ra % G) * DH;
+  __nv_bfloat16* ob = p.o + (long long)(row_base + rb / G) * p.ldo + (long long)(kvh * G + rb % G) * DH;
 #pragma unroll
   for (int i = 0; i < DH / 8; ++i) {
     const int col = i * 8 + c4 * 2;
-    if (ra < rows) *reinterpret_cast<uint32_t*>(oa + col) = pack2(o[i][0] * inv_a, o[i][1] * inv_a);
-    if (rb < rows) *reinterpret_cast<uint32_t*>(ob + col) = pack2(o[i][2] * inv_b, o[i][3] * inv_b);
+    if (ra < nrows) *reinterpret_cast<uint32_t*>(oa + col) = pack2(o[i][0] * inv_a, o[i][1] * inv_a);
+    if (rb < nrows) *reinterpret_cast<uint32_t*>(ob + col) = pack2(o[i][2] * inv_b, o[i][3] * inv_b);
   }
 }
 
 template <int DH>
 int launch_dh(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
-  constexpr size_t smem = (size_t)BM * DH * 2 + 4 * (size_t)BN * DH * 2;
+  constexpr size_t smem = (size_t)ROWS * DH * 2 + 2 * STAGES * (size_t)BN * DH * 2;
   static bool attr = false;
   if (!attr) {
     CUDA_TRY(cudaFuncSetAttribute(attn_prefill_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  dim3 grid((max_new + BM - 1) / BM, p.hq, n_seqs);
-  attn_prefill_kernel<DH><<<grid, 128, smem, st>>>(p);
+  const int G = p.hq / p.hkv;
+  const int tok_per_cta = ROWS / G;
+  dim3 grid((max_new + tok_per_cta - 1) / tok_per_cta, p.hkv, n_seqs);
+  attn_prefill_kernel<DH><<<grid, THREADS, smem, st>>>(p);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -257,6 +272,8 @@ int launch_dh(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
 int launch_attention(const AttnParams& p, int head_dim, int n_seqs, int max_new, cudaStream_t st) {
   if (n_seqs <= 0 || max_new <= 0) return 0;
   if (p.hq % p.hkv != 0) return set_error(RDKV_ERR_ARG, "attention: hq %% hkv != 0");
+  const int G = p.hq / p.hkv;
+  if (G > 128 || 128 % G != 0) return set_error(RDKV_ERR_ARG, "attention: group size %d must divide 128", G);
   if (head_dim == 64) return launch_dh<64>(p, n_seqs, max_new, st);
   if (head_dim == 128) return launch_dh<128>(p, n_seqs, max_new, st);
   return set_error(RDKV_ERR_ARG, "attention: head_dim %d unsupported", head_dim);
