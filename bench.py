@@ -266,6 +266,9 @@ def run_ours(a):
     _barrier(ws)
     eng.model.profile(False)
     classes = eng.model.collect()
+    # attention FLOPs (4*dh*Hq per visible query-key pair per layer), from the host batch plan
+    pairs = B * (a.q_tokens * k * a.doc_tokens + a.q_tokens * (a.q_tokens + 1) / 2)
+    classes["attention"]["flops"] = 4.0 * spec.head_dim * spec.n_heads * pairs * spec.layers * a.steps
     t_value = _max_over_ranks(e0.elapsed_time(e1) / 1e3, ws, dev)
     unpack_ms = sum(x.elapsed_time(y) for x, y in unpack_ev)
     unpack_bytes = 2 * comp_bytes * B * a.steps          # read + write, algorithmic

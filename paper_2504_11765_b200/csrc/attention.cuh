@@ -20,8 +20,13 @@ struct AttnParams {
   int block_size;
   int hq, hkv;
   float scale_log2;             // log2(e) / sqrt(dh)
+  int contiguous;               // 1: each sequence's KV is one block (blob layout)
 };
 
+// mma.sync kernel (any group size dividing 128, any block size)
 int launch_attention(const AttnParams& p, int head_dim, int n_seqs, int max_new, cudaStream_t st);
+// tcgen05 kernel (block_size % 64 == 0 or contiguous)
+bool attention_tc_supported(const AttnParams& p, int head_dim);
+int launch_attention_tc(const AttnParams& p, int head_dim, int n_seqs, int max_new, cudaStream_t st);
 
 }  // namespace rdkv

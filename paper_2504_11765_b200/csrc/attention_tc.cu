@@ -1,0 +1,389 @@
+// K2/K4 on the 5th-generation tensor cores: causal prefill attention over a
+// (possibly cached) KV prefix with grouped-query packing.
+//
+// Semantics are those of attention.cu (reference: cached_prefill_work,
+// costs.py:89-99 — new tokens at positions [n_cached, n_cached+n_new) attend
+// over every position <= their own).  A CTA owns 128 query rows of ONE kv
+// head, row r = (token t0 + r / G, q-head kvh*G + r % G), so the G query heads
+// sharing a K/V head read each K/V tile once.
+//
+// Warp roles (256 threads, one CTA per SM):
+//   warp 0      TMA producer: K and V tiles of 128 positions (two 64-row boxes
+//               each, one per KV block of the paged pool / blob) into a
+//               STAGES-deep smem ring, 128-byte swizzle
+//   warp 1      MMA issuer (one thread): S[b] = Q.K^T  (M=128, N=128, K=dh) into
+//               TMEM, then O_tile[b] = P.V (M=128, N=dh, K=128; V is the
+//               MN-major B operand) into TMEM; order QK0, QK1, PV0, QK2, PV1, ...
+//   warp 2      TMEM allocator (512 columns: S x2, O_tile x2)
+//   warps 4..7  softmax (one query row per thread = one TMEM lane): load Q,
+//               then per tile: tcgen05.ld S, mask, online max / exp2 / sum,
+//               write P (bf16, swizzled K-major) to smem; fold the previous
+//               tile's O_tile into a register accumulator with the running
+//               rescale; finally normalise and store O.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+#include <cstdint>
+
+#include "attention.cuh"
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace rdkv {
+
+int make_tmap(CUtensorMap* m, const void* base, long long rows, long long K, long long ld, int box_rows);
+
+namespace {
+
+constexpr int ROWS = 128;
+constexpr int BKV = 128;  // key positions per tile
+constexpr int HALF = 64;  // rows per TMA box (= one KV block of the pool)
+
+template <int DH>
+struct TcCfg {
+  static constexpr int STAGES = DH == 64 ? 3 : 2;
+  static constexpr uint32_t QB = ROWS * DH * 2;    // Q tile bytes
+  static constexpr uint32_t KB = BKV * DH * 2;     // one K (or V) tile
+  static constexpr uint32_t PB = ROWS * BKV * 2;   // one P tile
+  static constexpr uint32_t OFF_Q = 0;
+  static constexpr uint32_t OFF_K = OFF_Q + QB;
+  static constexpr uint32_t OFF_V = OFF_K + STAGES * KB;
+  static constexpr uint32_t OFF_P = OFF_V + STAGES * KB;
+  static constexpr uint32_t OFF_BAR = OFF_P + 2 * PB;
+  static constexpr size_t SMEM = 1024 + OFF_BAR + 256;
+};
+
+// K-major SW128 operand (rows of 128 B, 8-row atoms 1024 B apart)
+__device__ __forceinline__ uint64_t desc_k(uint32_t saddr) { return sdesc_k_sw128(saddr); }
+
+// MN-major SW128 operand: 64 MN elements (128 B) per swizzle row, 8 K rows per
+// 1024-B atom (SBO), next 64 MN elements `lbo` bytes away (LBO).
+__device__ __forceinline__ uint64_t desc_mn(uint32_t saddr, uint32_t lbo) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+template <int DH>
+__global__ void __launch_bounds__(256, 1)
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnParams p) {
+  using C = TcCfg<DH>;
+  constexpr int ST = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sb = smem_u32(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;             // [ST]
+  uint64_t* v_full = k_full + ST;          // [ST]
+  uint64_t* kv_empty = v_full + ST;        // [ST]
+  uint64_t* s_full = kv_empty + ST;        // [2]
+  uint64_t* s_empty = s_full + 2;          // [2]
+  uint64_t* p_full = s_empty + 2;          // [2]
+  uint64_t* p_empty = p_full + 2;          // [2]
+  uint64_t* o_full = p_empty + 2;          // [2]
+  uint64_t* o_empty = o_full + 2;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
+
+  const int G = p.hq / p.hkv;
+  const int s = blockIdx.z, kvh = blockIdx.y;
+  const int qb = gridDim.x - 1 - blockIdx.x;  // longest causal rows first
+  const int n_new = p.seq_new[s];
+  const int tok_per_cta = ROWS / G;
+  const int tok0 = qb * tok_per_cta;
+  if (tok0 >= n_new) return;
+  const int ntok = min(tok_per_cta, n_new - tok0);
+  const int nrows = ntok * G;
+  const int pos0 = p.seq_cached[s] + tok0;
+  const int kv_len = pos0 + ntok;
+  const int n_tiles = (kv_len + BKV - 1) / BKV;
+  const int row_base = p.seq_start[s] + tok0;
+  const int* bt = p.block_table + (long long)s * p.bt_stride;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+  }
+  if (warp == 1 && lane == 0) {
+    mbar_init(q_full, 128);
+    for (int i = 0; i < ST; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&p_empty[i], 1);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_empty[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem;             // S buffers at columns [0,128) and [128,256)
+  const uint32_t tO = tmem + 2 * BKV;   // O_tile buffers at 256 and 256 + DH
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const long long row0 = (long long)kvh * (p.head_stride / DH);  // first row of this head in the plane view
+      for (int j = 0; j < n_tiles; ++j) {
+        const int st = j % ST;
+        mbar_wait_sleep(&kv_empty[st], ((j / ST) & 1) ^ 1);
+        int rows[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          int pos = j * BKV + h * HALF;
+          if (pos >= kv_len) pos = j * BKV;  // masked half: any valid, finite block
+          rows[h] = (int)(row0 + (long long)bt[pos / p.block_size] * p.block_size + pos % p.block_size);
+        }
+        mbar_arrive_expect_tx(&k_full[st], C::KB);
+#pragma unroll
+        for (int c = 0; c < DH / 64; ++c)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            tma_load_2d_nohint(&tmK, &k_full[st], smem + C::OFF_K + st * C::KB + c * (BKV * 128) + h * (HALF * 128),
+                               c * 64, rows[h]);
+        mbar_arrive_expect_tx(&v_full[st], C::KB);
+#pragma unroll
+        for (int c = 0; c < DH / 64; ++c)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            tma_load_2d_nohint(&tmV, &v_full[st], smem + C::OFF_V + st * C::KB + c * (BKV * 128) + h * (HALF * 128),
+                               c * 64, rows[h]);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_qk = idesc_bf16_f32(ROWS, BKV);
+      constexpr uint32_t idesc_pv = idesc_bf16_f32(ROWS, DH) | (1u << 16);  // B (V) is MN-major
+      mbar_wait_sleep(q_full, 0);
+      tc_fence_after();
+      auto issue_qk = [&](int j) {
+        const int st = j % ST, b = j & 1;
+        mbar_wait_sleep(&k_full[st], (j / ST) & 1);
+        mbar_wait_sleep(&s_empty[b], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t qa = sb + C::OFF_Q, ka = sb + C::OFF_K + st * C::KB;
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t blk = (kk >> 2) * (ROWS * 128), sub = (kk & 3) * 32;
+          umma_bf16(tS + b * BKV, desc_k(qa + blk + sub), desc_k(ka + (kk >> 2) * (BKV * 128) + sub), idesc_qk,
+                    kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[b]);
+      };
+      auto issue_pv = [&](int j) {
+        const int st = j % ST, b = j & 1;
+        mbar_wait_sleep(&v_full[st], (j / ST) & 1);
+        mbar_wait_sleep(&p_full[b], (j >> 1) & 1);
+        mbar_wait_sleep(&o_empty[b], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t pa = sb + C::OFF_P + b * C::PB, va = sb + C::OFF_V + st * C::KB;
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk) {
+          const uint32_t a_off = (kk >> 2) * (ROWS * 128) + (kk & 3) * 32;
+          umma_bf16(tO + b * DH, desc_k(pa + a_off), desc_mn(va + kk * 2048, BKV * 128), idesc_pv, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&o_full[b]);
+        umma_commit(&p_empty[b]);
+        umma_commit(&kv_empty[st]);
+      };
+      issue_qk(0);
+      for (int j = 0; j < n_tiles; ++j) {
+        if (j + 1 < n_tiles) issue_qk(j + 1);
+        issue_pv(j);
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax warps
+    const int r = (warp - 4) * 32 + lane;  // query row == TMEM lane
+    const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
+    // Q row -> smem (K-major SW128, DH/64 column blocks of [128 rows][128 B])
+    {
+      const bool ok = r < nrows;
+      const int rr = ok ? r : 0;
+      const uint4* src = reinterpret_cast<const uint4*>(p.q + (long long)(row_base + rr / G) * p.ldq +
+                                                        (long long)(kvh * G + rr % G) * DH);
+#pragma unroll
+      for (int c = 0; c < DH / 8; ++c) {
+        const uint4 v = ok ? src[c] : make_uint4(0, 0, 0, 0);
+        const uint32_t a = sb + C::OFF_Q + (c >> 3) * (ROWS * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4);
+        st_shared_v4(a, v.x, v.y, v.z, v.w);
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(q_full);
+    }
+    // padded rows pretend to be the last valid position so no row is fully masked
+    const int qpos = (r < nrows) ? pos0 + r / G : kv_len - 1;
+    const float sl2 = p.scale_log2;
+    float o_acc[DH];
+#pragma unroll
+    for (int i = 0; i < DH; ++i) o_acc[i] = 0.f;
+    float m_run = -INFINITY;   // max used for the newest P
+    float m_acc = -INFINITY;   // scale of o_acc
+    float m_pend = -INFINITY;  // max of the tile whose O_tile is pending
+    float l = 0.f;
+
+    auto consume = [&](int t, float m_t) {
+      const int b = t & 1;
+      mbar_wait(&o_full[b], (t >> 1) & 1);
+      tc_fence_after();
+      const float f = ex2_approx(m_acc - m_t);
+#pragma unroll
+      for (int c = 0; c < DH / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tO + b * DH + c * 32 + lane_off, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o_acc[c * 32 + i] = o_acc[c * 32 + i] * f + __uint_as_float(v[i]);
+      }
+      m_acc = m_t;
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_empty[b]);
+    };
+
+    // last visible position of this row; keys beyond it are masked
+    const int kmax = min(qpos, kv_len - 1);
+    for (int j = 0; j < n_tiles; ++j) {
+      const int b = j & 1;
+      mbar_wait(&s_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      const int kbase = j * BKV;
+      const bool need_mask = kbase + BKV - 1 > kmax;
+      // pass 1: raw row max (the positive scale commutes with max)
+      float mraw = -INFINITY;
+#pragma unroll 1
+      for (int c = 0; c < BKV / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tS + b * BKV + c * 32 + lane_off, v);
+        tmem_ld_wait();
+        if (!need_mask) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 2)
+            mraw = fmaxf(mraw, fmaxf(__uint_as_float(v[i]), __uint_as_float(v[i + 1])));
+        } else {
+          const int lim = kmax - (kbase + c * 32);  // elements i <= lim are visible
+#pragma unroll
+          for (int i = 0; i < 32; ++i) mraw = fmaxf(mraw, i <= lim ? __uint_as_float(v[i]) : -INFINITY);
+        }
+      }
+      const float mx = fmaxf(m_run, mraw * sl2);
+      const float nmx = -mx;
+      // pass 2: P = exp2(S*scale - max) -> smem (bf16, swizzled K-major), row sum
+      mbar_wait(&p_empty[b], ((j >> 1) & 1) ^ 1);
+      float sum = 0.f;
+      const uint32_t pbase = sb + C::OFF_P + b * C::PB + r * 128;
+#pragma unroll 1
+      for (int c = 0; c < BKV / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tS + b * BKV + c * 32 + lane_off, v);
+        tmem_ld_wait();
+        uint32_t w[16];
+        if (!need_mask) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float e0 = ex2_approx(fmaf(__uint_as_float(v[2 * i]), sl2, nmx));
+            const float e1 = ex2_approx(fmaf(__uint_as_float(v[2 * i + 1]), sl2, nmx));
+            sum += e0 + e1;
+            w[i] = pack_bf16(e0, e1);
+          }
+        } else {
+          const int lim = kmax - (kbase + c * 32);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float e0 = 2 * i <= lim ? ex2_approx(fmaf(__uint_as_float(v[2 * i]), sl2, nmx)) : 0.f;
+            const float e1 = 2 * i + 1 <= lim ? ex2_approx(fmaf(__uint_as_float(v[2 * i + 1]), sl2, nmx)) : 0.f;
+            sum += e0 + e1;
+            w[i] = pack_bf16(e0, e1);
+          }
+        }
+        const uint32_t blk = (c >> 1) * (ROWS * 128);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int chunk = (c & 1) * 4 + q;
+          st_shared_v4(pbase + blk + ((chunk ^ (r & 7)) << 4), w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+        }
+      }
+      tc_fence_before();
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&s_empty[b]);
+        mbar_arrive(&p_full[b]);
+      }
+      l = l * ex2_approx(m_run - mx) + sum;
+      m_run = mx;
+      if (j >= 1) consume(j - 1, m_pend);
+      m_pend = mx;
+    }
+    consume(n_tiles - 1, m_pend);
+    // normalise and store this row
+    if (r < nrows) {
+      const float inv = 1.f / l;
+      uint4* dst = reinterpret_cast<uint4*>(p.o + (long long)(row_base + r / G) * p.ldo +
+                                            (long long)(kvh * G + r % G) * DH);
+#pragma unroll
+      for (int c = 0; c < DH / 8; ++c)
+        dst[c] = make_uint4(pack_bf16(o_acc[8 * c] * inv, o_acc[8 * c + 1] * inv),
+                            pack_bf16(o_acc[8 * c + 2] * inv, o_acc[8 * c + 3] * inv),
+                            pack_bf16(o_acc[8 * c + 4] * inv, o_acc[8 * c + 5] * inv),
+                            pack_bf16(o_acc[8 * c + 6] * inv, o_acc[8 * c + 7] * inv));
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int DH>
+int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
+  using C = TcCfg<DH>;
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(attn_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    attr = true;
+  }
+  // plane view: rows = hkv * slots, cols = dh
+  const long long rows = (long long)p.hkv * (p.head_stride / DH);
+  CUtensorMap tk, tv;
+  RDKV_TRY(make_tmap(&tk, p.kplane, rows, DH, DH, HALF));
+  RDKV_TRY(make_tmap(&tv, p.vplane, rows, DH, DH, HALF));
+  const int tok_per_cta = ROWS / (p.hq / p.hkv);
+  dim3 grid((max_new + tok_per_cta - 1) / tok_per_cta, p.hkv, n_seqs);
+  attn_tc_kernel<DH><<<grid, 256, C::SMEM, st>>>(tk, tv, p);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace
+
+bool attention_tc_supported(const AttnParams& p, int head_dim) {
+  const int G = p.hq / p.hkv;
+  return (head_dim == 64 || head_dim == 128) && 128 % G == 0 && (p.block_size % HALF == 0 || p.contiguous);
+}
+
+int launch_attention_tc(const AttnParams& p, int head_dim, int n_seqs, int max_new, cudaStream_t st) {
+  if (n_seqs <= 0 || max_new <= 0) return 0;
+  if (!attention_tc_supported(p, head_dim))
+    return set_error(RDKV_ERR_ARG, "attention_tc: unsupported shape (dh %d, group %d, block %d)", head_dim,
+                     p.hq / p.hkv, p.block_size);
+  if (head_dim == 64) return launch_tc<64>(p, n_seqs, max_new, st);
+  return launch_tc<128>(p, n_seqs, max_new, st);
+}
+
+}  // namespace rdkv

@@ -253,6 +253,25 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+template <int BN, int EPI, int DH>
+int launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const GemmEpi& ep,
+                cudaStream_t stream) {
+  using C = GemmCfg<BN>;
+  auto kern = gemm_bf16_tc_kernel<BN, EPI, DH>;
+  static bool attr_set = false;  // per template instance
+  if (!attr_set) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    attr_set = true;
+  }
+  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  kern<<<grid, 256, C::SMEM, stream>>>(ta, tb, M, N, K, ep);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -280,25 +299,6 @@ int make_tmap(CUtensorMap* m, const void* base, long long rows, long long K, lon
   if (r != CUDA_SUCCESS) return set_error(RDKV_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return 0;
 }
-
-template <int BN, int EPI, int DH>
-int launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const GemmEpi& ep,
-                cudaStream_t stream) {
-  using C = GemmCfg<BN>;
-  auto kern = gemm_bf16_tc_kernel<BN, EPI, DH>;
-  static bool attr_set = false;  // per template instance
-  if (!attr_set) {
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-    attr_set = true;
-  }
-  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, 256, C::SMEM, stream>>>(ta, tb, M, N, K, ep);
-  CUDA_TRY(cudaGetLastError());
-  return 0;
-}
-
-}  // namespace
 
 int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long long ldb, int M, int N,
                 int K, int kind, int dh, const GemmEpi& ep, cudaStream_t stream) {

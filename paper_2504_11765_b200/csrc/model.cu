@@ -186,6 +186,10 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
   const long long qd = (long long)hq * dh;
   const long long plane = (long long)hkv * b->kv_slots * dh;  // elements per (layer, k|v) plane
   auto* kv = static_cast<__nv_bfloat16*>(b->kv_base);
+  static const bool use_tc_attn = [] {
+    const char* e = std::getenv("RDKV_ATTN");  // "mma" forces the legacy kernel (A/B measurements)
+    return !(e && e[0] == 'm');
+  }();
 
   LAUNCH(RDKV_PROF_MISC, 0.0, launch_embed(b->tokens, W(m, 0), ws.x, T, d.hidden, d.vocab, st));
   for (int l = 0; l < d.layers; ++l) {
@@ -225,7 +229,11 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     ap.hq = hq;
     ap.hkv = hkv;
     ap.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)dh));
-    LAUNCH(RDKV_PROF_ATTN, 0.0, launch_attention(ap, dh, S, b->max_new, st));
+    ap.contiguous = b->bt_stride == 1 ? 1 : 0;
+    if (use_tc_attn && attention_tc_supported(ap, dh))
+      LAUNCH(RDKV_PROF_ATTN, 0.0, launch_attention_tc(ap, dh, S, b->max_new, st));
+    else
+      LAUNCH(RDKV_PROF_ATTN, 0.0, launch_attention(ap, dh, S, b->max_new, st));
     GemmEpi er{};
     er.out = ws.x;
     er.ldo = d.hidden;

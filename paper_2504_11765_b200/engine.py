@@ -107,7 +107,10 @@ class KvPool:
         self.spec, self.block_size, self.n_blocks = spec, block_size, n_blocks
         self.slots = n_blocks * block_size
         numel = spec.layers * 2 * spec.kv_heads * self.slots * spec.head_dim
-        self.data = torch.empty(numel, dtype=torch.bfloat16, device=device)
+        # zero-initialised: the tensor-core attention reads whole 64-slot blocks and
+        # masks positions past a sequence's length, so every slot must hold finite
+        # values (0 * NaN would poison P.V); later contents are always written KV.
+        self.data = torch.zeros(numel, dtype=torch.bfloat16, device=device)
         self._free: deque[int] = deque(range(n_blocks))
 
     def blocks_for(self, n_tokens: int) -> int:
