@@ -49,8 +49,10 @@ struct TcCfg {
   static constexpr uint32_t OFF_K = OFF_Q + QB;
   static constexpr uint32_t OFF_V = OFF_K + STAGES * KB;
   static constexpr uint32_t OFF_P = OFF_V + STAGES * KB;
-  static constexpr uint32_t OFF_BAR = OFF_P + 2 * PB;
-  static constexpr size_t SMEM = 1024 + OFF_BAR + 256;
+  static constexpr uint32_t OFF_RED = OFF_P + 2 * PB;  // [2 parity][2 half][128] fp32 row-max / row-sum exchange
+  static constexpr uint32_t OFF_BAR = OFF_RED + 4 * ROWS * 4;
+  // no alignment slack: DH=128 uses all but ~0.6 KB of the 227 KB; the base is checked at run time
+  static constexpr size_t SMEM = OFF_BAR + 8 * (1 + 3 * STAGES + 12) + 16;
 };
 
 // K-major SW128 operand (rows of 128 B, 8-row atoms 1024 B apart)
@@ -68,13 +70,14 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
 }
 
 template <int DH>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnParams p) {
   using C = TcCfg<DH>;
   constexpr int ST = C::STAGES;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
   const uint32_t sb = smem_u32(smem);
+  if (sb & 1023) __trap();  // SW128 operands need 1024-B alignment
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bars + 0;
   uint64_t* k_full = bars + 1;             // [ST]
@@ -109,7 +112,7 @@ __global__ void __launch_bounds__(256, 1)
     tma_prefetch_desc(&tmV);
   }
   if (warp == 1 && lane == 0) {
-    mbar_init(q_full, 128);
+    mbar_init(q_full, 8);
     for (int i = 0; i < ST; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&v_full[i], 1);
@@ -117,11 +120,11 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 4);
-      mbar_init(&p_full[i], 4);
+      mbar_init(&s_empty[i], 8);
+      mbar_init(&p_full[i], 8);
       mbar_init(&p_empty[i], 1);
       mbar_init(&o_full[i], 1);
-      mbar_init(&o_empty[i], 4);
+      mbar_init(&o_empty[i], 8);
     }
     fence_barrier_init();
   }
@@ -208,33 +211,43 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax warps
-    const int r = (warp - 4) * 32 + lane;  // query row == TMEM lane
-    const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
-    // Q row -> smem (K-major SW128, DH/64 column blocks of [128 rows][128 B])
+    // 8 warps: warp 4+q and warp 8+q both own TMEM lanes [32q, 32q+32) (query
+    // rows); half h = (warp-4)/4 takes S columns [64h, 64h+64) and O columns
+    // [h*DH/2, (h+1)*DH/2).  The pair exchanges the row max per tile.
+    const int quad = (warp - 4) & 3, h = (warp - 4) >> 2;
+    const int r = quad * 32 + lane;  // query row == TMEM lane
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    float* red = reinterpret_cast<float*>(smem + C::OFF_RED);  // [2 parity][2 half][128 rows]
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory"); };
+    // Q row half -> smem (K-major SW128, DH/64 column blocks of [128 rows][128 B])
     {
       const bool ok = r < nrows;
       const int rr = ok ? r : 0;
       const uint4* src = reinterpret_cast<const uint4*>(p.q + (long long)(row_base + rr / G) * p.ldq +
                                                         (long long)(kvh * G + rr % G) * DH);
 #pragma unroll
-      for (int c = 0; c < DH / 8; ++c) {
+      for (int cc = 0; cc < DH / 16; ++cc) {
+        const int c = h * (DH / 16) + cc;
         const uint4 v = ok ? src[c] : make_uint4(0, 0, 0, 0);
         const uint32_t a = sb + C::OFF_Q + (c >> 3) * (ROWS * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4);
         st_shared_v4(a, v.x, v.y, v.z, v.w);
       }
       fence_proxy_async_smem();
-      mbar_arrive(q_full);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(q_full);
     }
     // padded rows pretend to be the last valid position so no row is fully masked
     const int qpos = (r < nrows) ? pos0 + r / G : kv_len - 1;
+    const int kmax = min(qpos, kv_len - 1);  // last visible key position of this row
     const float sl2 = p.scale_log2;
-    float o_acc[DH];
+    constexpr int OD = DH / 2;  // O columns owned by this half
+    float o_acc[OD];
 #pragma unroll
-    for (int i = 0; i < DH; ++i) o_acc[i] = 0.f;
+    for (int i = 0; i < OD; ++i) o_acc[i] = 0.f;
     float m_run = -INFINITY;   // max used for the newest P
     float m_acc = -INFINITY;   // scale of o_acc
     float m_pend = -INFINITY;  // max of the tile whose O_tile is pending
-    float l = 0.f;
+    float l = 0.f;             // this half's share of the row sum (same scale as o_acc after the last fold)
 
     auto consume = [&](int t, float m_t) {
       const int b = t & 1;
@@ -242,12 +255,12 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_after();
       const float f = ex2_approx(m_acc - m_t);
 #pragma unroll
-      for (int c = 0; c < DH / 32; ++c) {
+      for (int c = 0; c < OD / 32; ++c) {
         uint32_t v[32];
-        tmem_ld32(tO + b * DH + c * 32 + lane_off, v);
+        tmem_ld32(tO + b * DH + h * OD + c * 32 + lane_off, v);
         tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) o_acc[c * 32 + i] = o_acc[c * 32 + i] * f + __uint_as_float(v[i]);
+        for (int i = 0; i < 32; ++i) o_acc[c * 32 + i] = fmaf(o_acc[c * 32 + i], f, __uint_as_float(v[i]));
       }
       m_acc = m_t;
       tc_fence_before();
@@ -255,66 +268,66 @@ __global__ void __launch_bounds__(256, 1)
       if (lane == 0) mbar_arrive(&o_empty[b]);
     };
 
-    // last visible position of this row; keys beyond it are masked
-    const int kmax = min(qpos, kv_len - 1);
     for (int j = 0; j < n_tiles; ++j) {
       const int b = j & 1;
       mbar_wait(&s_full[b], (j >> 1) & 1);
       tc_fence_after();
-      const int kbase = j * BKV;
-      const bool need_mask = kbase + BKV - 1 > kmax;
-      // pass 1: raw row max (the positive scale commutes with max)
-      float mraw = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < BKV / 32; ++c) {
+      const int kbase = j * BKV + h * 64;       // first key of this half
+      const int lim0 = kmax - kbase;            // element e visible iff e <= lim0
+      const bool need_mask = lim0 < 63;
+      const uint32_t scol = tS + b * BKV + h * 64 + lane_off;
+      // pass 1: raw max of this half (scale > 0 commutes with max), 4 chains
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
         uint32_t v[32];
-        tmem_ld32(tS + b * BKV + c * 32 + lane_off, v);
+        tmem_ld32(scol + c * 32, v);
         tmem_ld_wait();
         if (!need_mask) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 2)
-            mraw = fmaxf(mraw, fmaxf(__uint_as_float(v[i]), __uint_as_float(v[i + 1])));
-        } else {
-          const int lim = kmax - (kbase + c * 32);  // elements i <= lim are visible
+          for (int i = 0; i < 32; i += 4)
 #pragma unroll
-          for (int i = 0; i < 32; ++i) mraw = fmaxf(mraw, i <= lim ? __uint_as_float(v[i]) : -INFINITY);
+            for (int u = 0; u < 4; ++u) m4[u] = fmaxf(m4[u], __uint_as_float(v[i + u]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              m4[u] = fmaxf(m4[u], (c * 32 + i + u) <= lim0 ? __uint_as_float(v[i + u]) : -INFINITY);
         }
       }
-      const float mx = fmaxf(m_run, mraw * sl2);
+      const float mine = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+      red[((j & 1) * 2 + h) * ROWS + r] = mine;
+      pair_sync();
+      const float other = red[((j & 1) * 2 + (h ^ 1)) * ROWS + r];
+      const float mx = fmaxf(m_run, fmaxf(mine, other) * sl2);
       const float nmx = -mx;
-      // pass 2: P = exp2(S*scale - max) -> smem (bf16, swizzled K-major), row sum
+      // pass 2: P = exp2(S*scale - max) -> smem (bf16, swizzled K-major), partial row sum
       mbar_wait(&p_empty[b], ((j >> 1) & 1) ^ 1);
-      float sum = 0.f;
-      const uint32_t pbase = sb + C::OFF_P + b * C::PB + r * 128;
-#pragma unroll 1
-      for (int c = 0; c < BKV / 32; ++c) {
+      float s4[4] = {0.f, 0.f, 0.f, 0.f};
+      const uint32_t pbase = sb + C::OFF_P + b * C::PB + h * (ROWS * 128) + r * 128;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
         uint32_t v[32];
-        tmem_ld32(tS + b * BKV + c * 32 + lane_off, v);
+        tmem_ld32(scol + c * 32, v);
         tmem_ld_wait();
         uint32_t w[16];
-        if (!need_mask) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float e0 = ex2_approx(fmaf(__uint_as_float(v[2 * i]), sl2, nmx));
-            const float e1 = ex2_approx(fmaf(__uint_as_float(v[2 * i + 1]), sl2, nmx));
-            sum += e0 + e1;
-            w[i] = pack_bf16(e0, e1);
+        for (int i = 0; i < 16; ++i) {
+          const int e = c * 32 + 2 * i;
+          float e0 = ex2_approx(fmaf(__uint_as_float(v[2 * i]), sl2, nmx));
+          float e1 = ex2_approx(fmaf(__uint_as_float(v[2 * i + 1]), sl2, nmx));
+          if (need_mask) {
+            e0 = e <= lim0 ? e0 : 0.f;
+            e1 = e + 1 <= lim0 ? e1 : 0.f;
           }
-        } else {
-          const int lim = kmax - (kbase + c * 32);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float e0 = 2 * i <= lim ? ex2_approx(fmaf(__uint_as_float(v[2 * i]), sl2, nmx)) : 0.f;
-            const float e1 = 2 * i + 1 <= lim ? ex2_approx(fmaf(__uint_as_float(v[2 * i + 1]), sl2, nmx)) : 0.f;
-            sum += e0 + e1;
-            w[i] = pack_bf16(e0, e1);
-          }
+          s4[i & 3] += e0 + e1;
+          w[i] = pack_bf16(e0, e1);
         }
-        const uint32_t blk = (c >> 1) * (ROWS * 128);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const int chunk = (c & 1) * 4 + q;
-          st_shared_v4(pbase + blk + ((chunk ^ (r & 7)) << 4), w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+          const int chunk = c * 4 + q;
+          st_shared_v4(pbase + ((chunk ^ (r & 7)) << 4), w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
         }
       }
       tc_fence_before();
@@ -324,19 +337,24 @@ __global__ void __launch_bounds__(256, 1)
         mbar_arrive(&s_empty[b]);
         mbar_arrive(&p_full[b]);
       }
-      l = l * ex2_approx(m_run - mx) + sum;
+      l = l * ex2_approx(m_run - mx) + ((s4[0] + s4[1]) + (s4[2] + s4[3]));
       m_run = mx;
       if (j >= 1) consume(j - 1, m_pend);
       m_pend = mx;
     }
     consume(n_tiles - 1, m_pend);
-    // normalise and store this row
+    // total row sum = both halves; then normalise and store this half of the row
+    // the parity slot the last tile did NOT use is free (its readers passed the last pair_sync)
+    const int fs = n_tiles & 1;
+    red[(fs * 2 + h) * ROWS + r] = l;
+    pair_sync();
+    const float lt = l + red[(fs * 2 + (h ^ 1)) * ROWS + r];
     if (r < nrows) {
-      const float inv = 1.f / l;
+      const float inv = 1.f / lt;
       uint4* dst = reinterpret_cast<uint4*>(p.o + (long long)(row_base + r / G) * p.ldo +
-                                            (long long)(kvh * G + r % G) * DH);
+                                            (long long)(kvh * G + r % G) * DH + h * OD);
 #pragma unroll
-      for (int c = 0; c < DH / 8; ++c)
+      for (int c = 0; c < OD / 8; ++c)
         dst[c] = make_uint4(pack_bf16(o_acc[8 * c] * inv, o_acc[8 * c + 1] * inv),
                             pack_bf16(o_acc[8 * c + 2] * inv, o_acc[8 * c + 3] * inv),
                             pack_bf16(o_acc[8 * c + 4] * inv, o_acc[8 * c + 5] * inv),
@@ -365,7 +383,7 @@ int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
   RDKV_TRY(make_tmap(&tv, p.vplane, rows, DH, DH, HALF));
   const int tok_per_cta = ROWS / (p.hq / p.hkv);
   dim3 grid((max_new + tok_per_cta - 1) / tok_per_cta, p.hkv, n_seqs);
-  attn_tc_kernel<DH><<<grid, 256, C::SMEM, st>>>(tk, tv, p);
+  attn_tc_kernel<DH><<<grid, 384, C::SMEM, st>>>(tk, tv, p);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
