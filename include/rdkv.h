@@ -243,6 +243,11 @@ RDKV_API int rdkv_profile_enable(rdkv_model* model, int on);
  * collect; resets the counters.  Arrays hold RDKV_PROF_N entries. */
 RDKV_API int rdkv_profile_collect(rdkv_model* model, double* ms, int64_t* launches, double* flops);
 
+/* rdkv_gemm_bf16 with an explicit tile N (128 or 256; 0 = automatic). */
+RDKV_API int rdkv_gemm_bf16_tiled(const void* A, int64_t lda, const void* B, int64_t ldb, void* D,
+                                  int64_t ldd, const void* R, int64_t ldr, int M, int N, int K,
+                                  int epilogue, int tile_n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

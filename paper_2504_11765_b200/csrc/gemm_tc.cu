@@ -176,14 +176,15 @@ __global__ void __launch_bounds__(256, 1)
           }
         }
       } else if constexpr (EPI == EPI_SWIGLU) {
-        constexpr int HALF = BN / 2;
+        // weights interleaved in 64-row blocks: tile column block 2i = gate, 2i+1 = up
 #pragma unroll 1
-        for (int c = 0; c < HALF / 32; ++c) {
+        for (int c = 0; c < BN / 64; ++c) {
+          const int pb = c >> 1, half = c & 1;  // pair of 64-blocks, 32-col half inside it
           uint32_t g[32], u[32];
-          tmem_ld32(taddr + c * 32, g);
-          tmem_ld32(taddr + HALF + c * 32, u);
+          tmem_ld32(taddr + pb * 128 + half * 32, g);
+          tmem_ld32(taddr + pb * 128 + 64 + half * 32, u);
           tmem_ld_wait();
-          const int col = nb * HALF + c * 32;  // output column
+          const int col = nb * (BN / 2) + pb * 64 + half * 32;  // output column
           if (row_ok && col < N / 2) {
             uint32_t w[16];
 #pragma unroll
@@ -300,33 +301,50 @@ int make_tmap(CUtensorMap* m, const void* base, long long rows, long long K, lon
   return 0;
 }
 
-int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long long ldb, int M, int N,
-                int K, int kind, int dh, const GemmEpi& ep, cudaStream_t stream) {
-  if (M <= 0 || N <= 0) return 0;
-  if (K <= 0 || K % BK != 0) return set_error(RDKV_ERR_ARG, "gemm: K=%d must be a positive multiple of 64", K);
-  if (N % 32 != 0) return set_error(RDKV_ERR_ARG, "gemm: N=%d must be a multiple of 32", N);
-  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15)
-    return set_error(RDKV_ERR_ARG, "gemm: operands must be 16-byte aligned");
-  if ((lda | ldb) & 7) return set_error(RDKV_ERR_ARG, "gemm: leading dims must be multiples of 8");
-  constexpr int BN = 128;
+// Tile-N choice: fewer, larger tiles are cheaper per FLOP (smem traffic per MMA
+// drops from 128 to 96 B/clk) but quantise worse on 148 SMs; estimate both.
+int pick_bn(int M, int N) {
+  const int m_tiles = (M + BM - 1) / BM, sms = num_sms();
+  auto cost = [&](int bn, double eff) {
+    const long long tiles = (long long)m_tiles * ((N + bn - 1) / bn);
+    return (double)((tiles + sms - 1) / sms) * bn * eff;
+  };
+  return cost(256, 1.0) <= cost(128, 1.15) ? 256 : 128;
+}
+
+template <int BN>
+int dispatch(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long long ldb, int M, int N, int K,
+             int kind, int dh, const GemmEpi& ep, cudaStream_t stream) {
   CUtensorMap ta, tb;
-  int rc = make_tmap(&ta, A, M, K, lda, BM);
-  if (rc) return rc;
-  rc = make_tmap(&tb, B, N, K, ldb, BN);
-  if (rc) return rc;
+  RDKV_TRY(make_tmap(&ta, A, M, K, lda, BM));
+  RDKV_TRY(make_tmap(&tb, B, N, K, ldb, BN));
   switch (kind) {
     case EPI_STORE: return launch_impl<BN, EPI_STORE, 0>(ta, tb, M, N, K, ep, stream);
     case EPI_STORE_F32: return launch_impl<BN, EPI_STORE_F32, 0>(ta, tb, M, N, K, ep, stream);
     case EPI_RESID: return launch_impl<BN, EPI_RESID, 0>(ta, tb, M, N, K, ep, stream);
-    case EPI_SWIGLU:
-      if (N % BN != 0) return set_error(RDKV_ERR_ARG, "swiglu: N must be a multiple of %d", BN);
-      return launch_impl<BN, EPI_SWIGLU, 0>(ta, tb, M, N, K, ep, stream);
+    case EPI_SWIGLU: return launch_impl<BN, EPI_SWIGLU, 0>(ta, tb, M, N, K, ep, stream);
     case EPI_QKV:
       if (dh == 64) return launch_impl<BN, EPI_QKV, 64>(ta, tb, M, N, K, ep, stream);
       if (dh == 128) return launch_impl<BN, EPI_QKV, 128>(ta, tb, M, N, K, ep, stream);
       return set_error(RDKV_ERR_ARG, "qkv: head_dim %d unsupported (64 or 128)", dh);
     default: return set_error(RDKV_ERR_ARG, "gemm: unknown epilogue %d", kind);
   }
+}
+
+int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long long ldb, int M, int N,
+                int K, int kind, int dh, const GemmEpi& ep, cudaStream_t stream, int bn) {
+  if (M <= 0 || N <= 0) return 0;
+  if (K <= 0 || K % BK != 0) return set_error(RDKV_ERR_ARG, "gemm: K=%d must be a positive multiple of 64", K);
+  if (N % 32 != 0) return set_error(RDKV_ERR_ARG, "gemm: N=%d must be a multiple of 32", N);
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15)
+    return set_error(RDKV_ERR_ARG, "gemm: operands must be 16-byte aligned");
+  if ((lda | ldb) & 7) return set_error(RDKV_ERR_ARG, "gemm: leading dims must be multiples of 8");
+  if (bn != 0 && bn != 128 && bn != 256) return set_error(RDKV_ERR_ARG, "gemm: tile N %d must be 128 or 256", bn);
+  if (kind == EPI_SWIGLU && N % 128 != 0) return set_error(RDKV_ERR_ARG, "swiglu: N must be a multiple of 128");
+  if (bn == 0) bn = pick_bn(M, N);
+  if (kind == EPI_SWIGLU && N % bn != 0) bn = 128;
+  if (bn == 128) return dispatch<128>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
+  return dispatch<256>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
 }
 
 }  // namespace rdkv

@@ -40,7 +40,8 @@ struct GemmEpi {
   int hq, hkv;
 };
 
+// bn = tile N (128 or 256), 0 = choose by wave quantisation
 int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long long ldb, int M,
-                int N, int K, int kind, int dh, const GemmEpi& ep, cudaStream_t stream);
+                int N, int K, int kind, int dh, const GemmEpi& ep, cudaStream_t stream, int bn = 0);
 
 }  // namespace rdkv

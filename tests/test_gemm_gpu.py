@@ -1,4 +1,5 @@
-"""K1 tcgen05 GEMM parity against a plain PyTorch fp32 reference of the same op."""
+"""K1 tcgen05 GEMM parity against a plain PyTorch fp32 reference of the same op,
+for both tile widths (N=128, N=256) and every exposed epilogue."""
 
 import pytest
 import torch
@@ -7,18 +8,20 @@ from paper_2504_11765_b200 import _lib
 
 pytestmark = pytest.mark.gpu
 
+TILES = [128, 256]
+
 
 def _ptr(t):
     return t.data_ptr() if t is not None else None
 
 
-def _gemm(A, B, D, epi, R=None):
+def _gemm(A, B, D, epi, R=None, tile=0):
     s = torch.cuda.current_stream().cuda_stream
     M, K = A.shape
     N = B.shape[0]
-    _lib.check(_lib.lib().rdkv_gemm_bf16(
+    _lib.check(_lib.lib().rdkv_gemm_bf16_tiled(
         _ptr(A), A.stride(0), _ptr(B), B.stride(0), _ptr(D), D.stride(0),
-        _ptr(R), R.stride(0) if R is not None else 0, M, N, K, epi, s))
+        _ptr(R), R.stride(0) if R is not None else 0, M, N, K, epi, tile, s))
 
 
 def _inputs(M, N, K, seed=0):
@@ -32,41 +35,45 @@ SHAPES = [(128, 128, 64), (256, 384, 512), (200, 96, 128), (37, 4096, 2048), (20
           (1000, 3072, 2048), (64, 2048, 8192)]
 
 
+@pytest.mark.parametrize("tile", TILES)
 @pytest.mark.parametrize("M,N,K", SHAPES)
-def test_store_bf16(M, N, K):
+def test_store_bf16(M, N, K, tile):
     A, B = _inputs(M, N, K)
     D = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16)
-    _gemm(A, B, D, _lib.EPI_STORE)
+    _gemm(A, B, D, _lib.EPI_STORE, tile=tile)
     torch.cuda.synchronize()
     ref = A.float() @ B.float().T
     torch.testing.assert_close(D.float(), ref, atol=2e-2, rtol=1e-2)
 
 
+@pytest.mark.parametrize("tile", TILES)
 @pytest.mark.parametrize("M,N,K", [(33, 1024, 256), (128, 128256 // 4, 2048)])
-def test_store_f32(M, N, K):
+def test_store_f32(M, N, K, tile):
     A, B = _inputs(M, N, K, seed=1)
     D = torch.full((M, N), float("nan"), device="cuda", dtype=torch.float32)
-    _gemm(A, B, D, _lib.EPI_STORE_F32)
+    _gemm(A, B, D, _lib.EPI_STORE_F32, tile=tile)
     torch.cuda.synchronize()
     ref = A.float() @ B.float().T
     torch.testing.assert_close(D, ref, atol=1e-3, rtol=1e-3)
 
 
+@pytest.mark.parametrize("tile", TILES)
 @pytest.mark.parametrize("M,N,K", [(300, 512, 1024), (2048, 2048, 8192)])
-def test_residual_in_place(M, N, K):
+def test_residual_in_place(M, N, K, tile):
     A, B = _inputs(M, N, K, seed=2)
     X = torch.randn(M, N, device="cuda").to(torch.bfloat16)
     ref = X.float() + A.float() @ B.float().T
-    _gemm(A, B, X, _lib.EPI_RESID)
+    _gemm(A, B, X, _lib.EPI_RESID, tile=tile)
     torch.cuda.synchronize()
     torch.testing.assert_close(X.float(), ref, atol=3e-2, rtol=1e-2)
 
 
-@pytest.mark.parametrize("M,N,K", [(130, 256, 128), (640, 2 * 8192, 2048)])
-def test_swiglu(M, N, K):
+@pytest.mark.parametrize("tile", TILES)
+@pytest.mark.parametrize("M,N,K", [(130, 256, 128), (640, 2 * 8192, 2048), (64, 384, 512)])
+def test_swiglu(M, N, K, tile):
     A, B = _inputs(M, N, K, seed=3)
     D = torch.full((M, N // 2), float("nan"), device="cuda", dtype=torch.bfloat16)
-    _gemm(A, B, D, _lib.EPI_SWIGLU)
+    _gemm(A, B, D, _lib.EPI_SWIGLU, tile=tile)
     torch.cuda.synchronize()
     full = (A.float() @ B.float().T).view(M, N // 128, 2, 64)
     ref = (torch.nn.functional.silu(full[:, :, 0]) * full[:, :, 1]).reshape(M, N // 2)
