@@ -276,26 +276,28 @@ __global__ void __launch_bounds__(384, 1)
       const int lim0 = kmax - kbase;            // element e visible iff e <= lim0
       const bool need_mask = lim0 < 63;
       const uint32_t scol = tS + b * BKV + h * 64 + lane_off;
-      // pass 1: raw max of this half (scale > 0 commutes with max), 4 chains
-      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      // this half's 64 scores stay in registers for both passes
+      uint32_t va[32], vb[32];
+      tmem_ld32(scol, va);
+      tmem_ld32(scol + 32, vb);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[b]);  // S buffer may be overwritten now
+      if (need_mask) {
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t v[32];
-        tmem_ld32(scol + c * 32, v);
-        tmem_ld_wait();
-        if (!need_mask) {
-#pragma unroll
-          for (int i = 0; i < 32; i += 4)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) m4[u] = fmaxf(m4[u], __uint_as_float(v[i + u]));
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; i += 4)
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              m4[u] = fmaxf(m4[u], (c * 32 + i + u) <= lim0 ? __uint_as_float(v[i + u]) : -INFINITY);
+        for (int i = 0; i < 32; ++i) {
+          if (i > lim0) va[i] = __float_as_uint(-INFINITY);
+          if (32 + i > lim0) vb[i] = __float_as_uint(-INFINITY);
         }
       }
+      // pass 1: raw max (scale > 0 commutes with max), 4 chains
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int i = 0; i < 32; i += 4)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          m4[u] = fmaxf(m4[u], fmaxf(__uint_as_float(va[i + u]), __uint_as_float(vb[i + u])));
       const float mine = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
       red[((j & 1) * 2 + h) * ROWS + r] = mine;
       pair_sync();
@@ -306,21 +308,13 @@ __global__ void __launch_bounds__(384, 1)
       mbar_wait(&p_empty[b], ((j >> 1) & 1) ^ 1);
       float s4[4] = {0.f, 0.f, 0.f, 0.f};
       const uint32_t pbase = sb + C::OFF_P + b * C::PB + h * (ROWS * 128) + r * 128;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t v[32];
-        tmem_ld32(scol + c * 32, v);
-        tmem_ld_wait();
+      auto emit = [&](const uint32_t(&v)[32], const int c) {
         uint32_t w[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const int e = c * 32 + 2 * i;
-          float e0 = ex2_approx(fmaf(__uint_as_float(v[2 * i]), sl2, nmx));
-          float e1 = ex2_approx(fmaf(__uint_as_float(v[2 * i + 1]), sl2, nmx));
-          if (need_mask) {
-            e0 = e <= lim0 ? e0 : 0.f;
-            e1 = e + 1 <= lim0 ? e1 : 0.f;
-          }
+          // masked scores are -inf: ex2(-inf) = +0
+          const float e0 = ex2_approx(fmaf(__uint_as_float(v[2 * i]), sl2, nmx));
+          const float e1 = ex2_approx(fmaf(__uint_as_float(v[2 * i + 1]), sl2, nmx));
           s4[i & 3] += e0 + e1;
           w[i] = pack_bf16(e0, e1);
         }
@@ -329,14 +323,12 @@ __global__ void __launch_bounds__(384, 1)
           const int chunk = c * 4 + q;
           st_shared_v4(pbase + ((chunk ^ (r & 7)) << 4), w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
         }
-      }
-      tc_fence_before();
+      };
+      emit(va, 0);
+      emit(vb, 1);
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&s_empty[b]);
-        mbar_arrive(&p_full[b]);
-      }
+      if (lane == 0) mbar_arrive(&p_full[b]);
       l = l * ex2_approx(m_run - mx) + ((s4[0] + s4[1]) + (s4[2] + s4[3]));
       m_run = mx;
       if (j >= 1) consume(j - 1, m_pend);
