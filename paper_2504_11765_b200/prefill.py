@@ -44,10 +44,12 @@ class PrefillResult:
 
 
 def prefill_batch(engine: Engine, requests: Sequence[PrefillRequest], timed: bool = True,
-                  unpack_events: list | None = None) -> PrefillResult:
+                  unpack_events: list | None = None, use_graph: bool = True) -> PrefillResult:
     """Serve a batch of queries on one engine; kv_load / prefill are the
     device-measured durations of the whole batch's load and prefill phases.
-    ``unpack_events`` collects (start, end) CUDA events around the K3 launch."""
+    ``unpack_events`` collects (start, end) CUDA events around the K3 launch.
+    Untimed calls replay a per-shape CUDA graph (``Engine.graphs``); its output
+    tensors are reused by the next call of the same shape."""
     pool = engine.pool
     main = torch.cuda.current_stream(engine.device)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if timed else None
@@ -75,28 +77,35 @@ def prefill_batch(engine: Engine, requests: Sequence[PrefillRequest], timed: boo
         plan = BatchPlan(seqs, pool.block_size, engine.device)
         if staged:
             main.wait_stream(engine.copy_stream)
-        if jobs:
-            if unpack_events is not None:
-                ua, ub = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                ua.record(main)
-            kv_unpack(pool, [(d, n, i * plan.bt_stride) for d, n, i in jobs], _bt_view(plan),
-                      elem_width=2, stream=main)
-            if unpack_events is not None:
-                ub.record(main)
-                unpack_events.append((ua, ub))
-        if timed:
-            ev[1].record(main)
-        S = len(requests)
-        logits = torch.empty(S, engine.spec.vocab, dtype=torch.float32, device=engine.device)
-        nxt = torch.empty(S, dtype=torch.int32, device=engine.device)
-        engine.model.forward(plan, pool.data.data_ptr(), pool.slots, logits, nxt, stream=main)
-        if timed:
-            ev[2].record(main)
-            ev[2].synchronize()
-            kv_load = ev[0].elapsed_time(ev[1]) / 1e3
-            prefill = ev[1].elapsed_time(ev[2]) / 1e3
-        else:
+        ujobs = [(d, n, i * plan.bt_stride) for d, n, i in jobs]
+        graphed = None
+        if use_graph and not timed and unpack_events is None:
+            graphed = engine.graphs.run(plan, ujobs)  # [K3 unpack ->] forward as one CUDA-graph replay
+        if graphed is not None:
+            logits, nxt = graphed
             kv_load = prefill = 0.0
+        else:
+            if ujobs:
+                if unpack_events is not None:
+                    ua, ub = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    ua.record(main)
+                kv_unpack(pool, ujobs, _bt_view(plan), elem_width=2, stream=main)
+                if unpack_events is not None:
+                    ub.record(main)
+                    unpack_events.append((ua, ub))
+            if timed:
+                ev[1].record(main)
+            S = len(requests)
+            logits = torch.empty(S, engine.spec.vocab, dtype=torch.float32, device=engine.device)
+            nxt = torch.empty(S, dtype=torch.int32, device=engine.device)
+            engine.model.forward(plan, pool.data.data_ptr(), pool.slots, logits, nxt, stream=main)
+            if timed:
+                ev[2].record(main)
+                ev[2].synchronize()
+                kv_load = ev[0].elapsed_time(ev[1]) / 1e3
+                prefill = ev[1].elapsed_time(ev[2]) / 1e3
+            else:
+                kv_load = prefill = 0.0
         for d in staged:  # keep staging buffers alive until the stream has consumed them
             d.record_stream(main)
         bd = TtftBreakdown(kv_load, prefill)
