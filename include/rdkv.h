@@ -243,10 +243,13 @@ RDKV_API int rdkv_profile_enable(rdkv_model* model, int on);
  * collect; resets the counters.  Arrays hold RDKV_PROF_N entries. */
 RDKV_API int rdkv_profile_collect(rdkv_model* model, double* ms, int64_t* launches, double* flops);
 
-/* rdkv_gemm_bf16 with an explicit tile N (128 or 256; 0 = automatic). */
-RDKV_API int rdkv_gemm_bf16_tiled(const void* A, int64_t lda, const void* B, int64_t ldb, void* D,
-                                  int64_t ldd, const void* R, int64_t ldr, int M, int N, int K,
-                                  int epilogue, int tile_n, void* stream);
+/* rdkv_gemm_bf16 with an explicit tile N (128 or 256; 0 = automatic) and an
+ * optional fp32 scratch buffer enabling split-K for small-M shapes (the
+ * partial sums are reduced in a fixed order: results are deterministic). */
+RDKV_API int rdkv_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64_t ldb, void* D,
+                               int64_t ldd, const void* R, int64_t ldr, int M, int N, int K,
+                               int epilogue, int tile_n, void* scratch, size_t scratch_bytes,
+                               void* stream);
 
 #ifdef __cplusplus
 }

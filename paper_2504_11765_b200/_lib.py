@@ -69,7 +69,8 @@ SIGNATURES: dict[str, tuple] = {
                               C.POINTER(_sz), C.POINTER(_sz)]),
     "rdkv_drop_page_cache": (_i32, [_cp]),
     "rdkv_gemm_bf16": (_i32, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _i32, _i32, _vp]),
-    "rdkv_gemm_bf16_tiled": (_i32, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp]),
+    "rdkv_gemm_bf16_ex": (_i32, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _sz,
+                                 _vp]),
 }
 
 _lock = threading.Lock()

@@ -1,4 +1,11 @@
 // K1 implementation: see gemm_tc.cuh for the design summary.
+//
+// Work units: (output tile, K split).  With split = 1 (the normal case) the
+// epilogue applies the fused op straight from TMEM.  Small-M GEMMs (a single
+// query's 64 rows) have too few tiles to occupy 148 SMs and are weight-
+// bandwidth bound, so they split K: each unit writes an fp32 partial tile to
+// its own slab and `splitk_finalize` sums the slabs in a fixed order (bit-for-
+// bit deterministic, no atomics) and applies the same fused epilogue.
 #include <cudaTypedefs.h>
 #include <cstdio>
 #include <mutex>
@@ -14,7 +21,7 @@ constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
 
 template <int BN>
 struct GemmCfg {
-  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
   static constexpr uint32_t A_BYTES = BM * BK * 2;
   static constexpr uint32_t B_BYTES = BN * BK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
@@ -31,10 +38,40 @@ __device__ __forceinline__ void st_bf16x32(__nv_bfloat16* dst, const uint32_t (&
   for (int i = 0; i < 4; ++i) d[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
 }
 
+// ---------------------------------------------------------------- shared epilogue math
+// RoPE (rotate-half) on one head held in registers, then bf16 store to its destination.
+template <int DH>
+__device__ __forceinline__ void qkv_head_out(float (&v)[DH], int g, int row, int p, int sl, const GemmEpi& ep) {
+  if (g < ep.hq + ep.hkv) {
+    const float2* cs = reinterpret_cast<const float2*>(ep.rope) + (long long)p * (DH / 2);
+#pragma unroll
+    for (int i = 0; i < DH / 2; ++i) {
+      const float2 t = cs[i];
+      const float x1 = v[i], x2 = v[i + DH / 2];
+      v[i] = x1 * t.x - x2 * t.y;
+      v[i + DH / 2] = x2 * t.x + x1 * t.y;
+    }
+  }
+  __nv_bfloat16* dst;
+  if (g < ep.hq)
+    dst = ep.q + (long long)row * ep.ldq + (long long)g * DH;
+  else if (g < ep.hq + ep.hkv)
+    dst = ep.kplane + (long long)(g - ep.hq) * ep.head_stride + (long long)sl * DH;
+  else
+    dst = ep.vplane + (long long)(g - ep.hq - ep.hkv) * ep.head_stride + (long long)sl * DH;
+#pragma unroll
+  for (int c = 0; c < DH / 32; ++c) {
+    uint32_t w[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) w[i] = pack_bf16(v[c * 32 + 2 * i], v[c * 32 + 2 * i + 1]);
+    st_bf16x32(dst + c * 32, w);
+  }
+}
+
 template <int BN, int EPI, int DH>
 __global__ void __launch_bounds__(256, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                        int M, int N, int K, GemmEpi ep) {
+                        int M, int N, int K, int splits, GemmEpi ep) {
   using C = GemmCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -50,8 +87,18 @@ __global__ void __launch_bounds__(256, 1)
   const int lane = threadIdx.x & 31;
   const int m_tiles = (M + BM - 1) / BM;
   const int n_tiles = (N + BN - 1) / BN;
-  const int num_tiles = m_tiles * n_tiles;
+  const int units = m_tiles * n_tiles * splits;
   const int kblocks = K / BK;
+  const int kb_per = (kblocks + splits - 1) / splits;
+  // unit -> (tile, k-range); tiles are M-fastest so CTAs resident together share weight tiles
+  auto decode = [&](int u, int& mb, int& nb, int& kb0, int& kb1, int& sp) {
+    const int t = u / splits;
+    sp = u - t * splits;
+    mb = t % m_tiles;
+    nb = t / m_tiles;
+    kb0 = sp * kb_per;
+    kb1 = min(kb0 + kb_per, kblocks);
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -80,9 +127,10 @@ __global__ void __launch_bounds__(256, 1)
       const uint64_t pol_act = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int mb = t % m_tiles, nb = t / m_tiles;
-        for (int kb = 0; kb < kblocks; ++kb) {
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int mb, nb, kb0, kb1, sp;
+        decode(u, mb, nb, kb0, kb1, sp);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           tma_load_2d(&tmA, &full[stage], sA + stage * C::A_BYTES, kb * BK, mb * BM, pol_act);
@@ -102,18 +150,20 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int mb, nb, kb0, kb1, sp;
+        decode(u, mb, nb, kb0, kb1, sp);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t ad = sdesc_k_sw128(smem_u32(sA + stage * C::A_BYTES));
           const uint64_t bd = sdesc_k_sw128(smem_u32(sB + stage * C::B_BYTES));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+            umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           umma_commit(&empty[stage]);
           if (++stage == C::STAGES) {
             stage = 0;
@@ -130,15 +180,16 @@ __global__ void __launch_bounds__(256, 1)
     const int wq = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      const int mb = t % m_tiles, nb = t / m_tiles;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      int mb, nb, kb0, kb1, sp;
+      decode(u, mb, nb, kb0, kb1, sp);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = mb * BM + wq * 32 + lane;
       const bool row_ok = row < M;
       const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(wq * 32) << 16);
 
-      if constexpr (EPI == EPI_STORE || EPI == EPI_STORE_F32 || EPI == EPI_RESID) {
+      if constexpr (EPI == EPI_STORE || EPI == EPI_STORE_F32 || EPI == EPI_RESID || EPI == EPI_PARTIAL) {
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           uint32_t r[32];
@@ -146,8 +197,10 @@ __global__ void __launch_bounds__(256, 1)
           tmem_ld_wait();
           const int col = nb * BN + c * 32;
           if (row_ok && col < N) {
-            if constexpr (EPI == EPI_STORE_F32) {
-              float4* dst = reinterpret_cast<float4*>(static_cast<float*>(ep.out) + (long long)row * ep.ldo + col);
+            if constexpr (EPI == EPI_STORE_F32 || EPI == EPI_PARTIAL) {
+              float* base = static_cast<float*>(ep.out);
+              if constexpr (EPI == EPI_PARTIAL) base += (long long)sp * M * N;  // this split's slab
+              float4* dst = reinterpret_cast<float4*>(base + (long long)row * (EPI == EPI_PARTIAL ? N : ep.ldo) + col);
 #pragma unroll
               for (int i = 0; i < 8; ++i)
                 dst[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
@@ -158,8 +211,8 @@ __global__ void __launch_bounds__(256, 1)
                 const uint4* src = reinterpret_cast<const uint4*>(ep.resid + (long long)row * ep.ldr + col);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                  const uint4 u = src[i];
-                  const uint32_t uu[4] = {u.x, u.y, u.z, u.w};
+                  const uint4 q = src[i];
+                  const uint32_t uu[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
                   for (int j = 0; j < 4; ++j) {
                     const float2 f = unpack_bf16(uu[j]);
@@ -179,18 +232,18 @@ __global__ void __launch_bounds__(256, 1)
         // weights interleaved in 64-row blocks: tile column block 2i = gate, 2i+1 = up
 #pragma unroll 1
         for (int c = 0; c < BN / 64; ++c) {
-          const int pb = c >> 1, half = c & 1;  // pair of 64-blocks, 32-col half inside it
-          uint32_t g[32], u[32];
+          const int pb = c >> 1, half = c & 1;
+          uint32_t g[32], v[32];
           tmem_ld32(taddr + pb * 128 + half * 32, g);
-          tmem_ld32(taddr + pb * 128 + 64 + half * 32, u);
+          tmem_ld32(taddr + pb * 128 + 64 + half * 32, v);
           tmem_ld_wait();
           const int col = nb * (BN / 2) + pb * 64 + half * 32;  // output column
           if (row_ok && col < N / 2) {
             uint32_t w[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-              const float a0 = silu(__uint_as_float(g[2 * i])) * __uint_as_float(u[2 * i]);
-              const float a1 = silu(__uint_as_float(g[2 * i + 1])) * __uint_as_float(u[2 * i + 1]);
+              const float a0 = silu(__uint_as_float(g[2 * i])) * __uint_as_float(v[2 * i]);
+              const float a1 = silu(__uint_as_float(g[2 * i + 1])) * __uint_as_float(v[2 * i + 1]);
               w[i] = pack_bf16(a0, a1);
             }
             st_bf16x32(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + col, w);
@@ -213,31 +266,7 @@ __global__ void __launch_bounds__(256, 1)
           }
           const int g = (nb * BN + hh * DH) / DH;  // global head index in [q | k | v]
           if (!row_ok || g >= ep.hq + 2 * ep.hkv) continue;
-          if (g < ep.hq + ep.hkv) {
-            // rotate-half RoPE: pairs (i, i + DH/2)
-            const float2* cs = reinterpret_cast<const float2*>(ep.rope) + (long long)p * (DH / 2);
-#pragma unroll
-            for (int i = 0; i < DH / 2; ++i) {
-              const float2 t = cs[i];
-              const float x1 = v[i], x2 = v[i + DH / 2];
-              v[i] = x1 * t.x - x2 * t.y;
-              v[i + DH / 2] = x2 * t.x + x1 * t.y;
-            }
-          }
-          __nv_bfloat16* dst;
-          if (g < ep.hq)
-            dst = ep.q + (long long)row * ep.ldq + (long long)g * DH;
-          else if (g < ep.hq + ep.hkv)
-            dst = ep.kplane + (long long)(g - ep.hq) * ep.head_stride + (long long)sl * DH;
-          else
-            dst = ep.vplane + (long long)(g - ep.hq - ep.hkv) * ep.head_stride + (long long)sl * DH;
-#pragma unroll
-          for (int c = 0; c < DH / 32; ++c) {
-            uint32_t w[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) w[i] = pack_bf16(v[c * 32 + 2 * i], v[c * 32 + 2 * i + 1]);
-            st_bf16x32(dst + c * 32, w);
-          }
+          qkv_head_out<DH>(v, g, row, p, sl, ep);
         }
       }
       tc_fence_before();
@@ -254,8 +283,94 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// ---------------------------------------------------------------- split-K finalize
+// Sum the split slabs in a fixed order (deterministic) and apply the epilogue.
+// Grid: (rows, column chunks); 4 consecutive columns per thread (float4 loads).
+template <int EPI, int DH>
+__global__ void __launch_bounds__(256) splitk_finalize_kernel(const float* __restrict__ part, int splits, int M,
+                                                              int N, GemmEpi ep) {
+  const int row = blockIdx.x;
+  const long long slab = (long long)M * N;
+  const float* pr = part + (long long)row * N;
+  auto sum4 = [&](int col) {
+    float4 s = *reinterpret_cast<const float4*>(pr + col);
+    for (int k = 1; k < splits; ++k) {
+      const float4 t = *reinterpret_cast<const float4*>(pr + k * slab + col);
+      s.x += t.x;
+      s.y += t.y;
+      s.z += t.z;
+      s.w += t.w;
+    }
+    return s;
+  };
+  if constexpr (EPI == EPI_QKV) {
+    // one warp per head (8 heads per CTA); lane owns elements lane + 32k, so RoPE
+    // pairs (i, i + DH/2) stay in-lane
+    constexpr int PER = DH / 32;
+    const int g = blockIdx.y * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (g >= N / DH) return;
+    const int p = ep.pos[row], sl = ep.slot[row];
+    float v[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int col = g * DH + lane + 32 * k;
+      float t = pr[col];
+      for (int q = 1; q < splits; ++q) t += pr[q * slab + col];
+      v[k] = t;
+    }
+    if (g < ep.hq + ep.hkv) {
+      const float2* cs = reinterpret_cast<const float2*>(ep.rope) + (long long)p * (DH / 2);
+#pragma unroll
+      for (int k = 0; k < PER / 2; ++k) {
+        const float2 t = cs[lane + 32 * k];
+        const float x1 = v[k], x2 = v[k + PER / 2];
+        v[k] = x1 * t.x - x2 * t.y;
+        v[k + PER / 2] = x2 * t.x + x1 * t.y;
+      }
+    }
+    __nv_bfloat16* dst;
+    if (g < ep.hq)
+      dst = ep.q + (long long)row * ep.ldq + (long long)g * DH;
+    else if (g < ep.hq + ep.hkv)
+      dst = ep.kplane + (long long)(g - ep.hq) * ep.head_stride + (long long)sl * DH;
+    else
+      dst = ep.vplane + (long long)(g - ep.hq - ep.hkv) * ep.head_stride + (long long)sl * DH;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) dst[lane + 32 * k] = __float2bfloat16(v[k]);
+  } else if constexpr (EPI == EPI_SWIGLU) {
+    const int j = (blockIdx.y * 256 + threadIdx.x) * 4;  // 4 outputs inside one 64-block
+    if (j >= N / 2) return;
+    const int gc = (j / 64) * 128 + (j % 64);
+    const float4 g = sum4(gc), u = sum4(gc + 64);
+    uint2 w;
+    w.x = pack_bf16(silu(g.x) * u.x, silu(g.y) * u.y);
+    w.y = pack_bf16(silu(g.z) * u.z, silu(g.w) * u.w);
+    *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + j) = w;
+  } else {
+    const int j = (blockIdx.y * 256 + threadIdx.x) * 4;
+    if (j >= N) return;
+    float4 s = sum4(j);
+    if constexpr (EPI == EPI_STORE_F32) {
+      *reinterpret_cast<float4*>(static_cast<float*>(ep.out) + (long long)row * ep.ldo + j) = s;
+    } else {
+      if constexpr (EPI == EPI_RESID) {
+        const uint2 r = *reinterpret_cast<const uint2*>(ep.resid + (long long)row * ep.ldr + j);
+        const float2 a = unpack_bf16(r.x), b = unpack_bf16(r.y);
+        s.x += a.x;
+        s.y += a.y;
+        s.z += b.x;
+        s.w += b.y;
+      }
+      uint2 w;
+      w.x = pack_bf16(s.x, s.y);
+      w.y = pack_bf16(s.z, s.w);
+      *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + j) = w;
+    }
+  }
+}
+
 template <int BN, int EPI, int DH>
-int launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const GemmEpi& ep,
+int launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, int splits, const GemmEpi& ep,
                 cudaStream_t stream) {
   using C = GemmCfg<BN>;
   auto kern = gemm_bf16_tc_kernel<BN, EPI, DH>;
@@ -264,9 +379,20 @@ int launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int 
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     attr_set = true;
   }
-  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, 256, C::SMEM, stream>>>(ta, tb, M, N, K, ep);
+  const int units = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * splits;
+  const int grid = units < num_sms() ? units : num_sms();
+  kern<<<grid, 256, C::SMEM, stream>>>(ta, tb, M, N, K, splits, ep);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+template <int EPI, int DH>
+int launch_finalize(const float* part, int splits, int M, int N, const GemmEpi& ep, cudaStream_t stream) {
+  int gy;
+  if (EPI == EPI_QKV) gy = (N / (DH ? DH : 1) + 7) / 8;
+  else if (EPI == EPI_SWIGLU) gy = (N / 2 + 1023) / 1024;
+  else gy = (N + 1023) / 1024;
+  splitk_finalize_kernel<EPI, DH><<<dim3(M, gy), 256, 0, stream>>>(part, splits, M, N, ep);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -312,27 +438,84 @@ int pick_bn(int M, int N) {
   return cost(256, 1.0) <= cost(128, 1.15) ? 256 : 128;
 }
 
+// K splits for a GEMM whose tiles cannot fill the SMs (small M): enough units
+// for ~one wave, at least 4 k-blocks per split.
+int pick_splits(int M, int N, int K, int bn) {
+  const int tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn), sms = num_sms();
+  const int kblocks = K / BK;
+  if (tiles * 2 > sms || kblocks < 8) return 1;
+  int s = (sms + tiles - 1) / tiles;
+  s = s < kblocks / 4 ? s : kblocks / 4;
+  if (s < 2) return 1;
+  const int kb_per = (kblocks + s - 1) / s;  // make every split non-empty
+  return (kblocks + kb_per - 1) / kb_per;
+}
+
+// Automatic small-M plan: a single 128-row tile whose N tiles cannot fill half
+// the SMs is weight-bandwidth bound; split it into 64-wide N tiles x K splits
+// (about one wave, >= 4 k-blocks per split).  Narrow N tiles keep the fp32
+// partial traffic (splits x M x N x 4 B) well below the weight bytes.
+struct SplitPlan {
+  int bn, splits;
+};
+SplitPlan pick_split_plan(int M, int N, int K) {
+  const int sms = num_sms(), kblocks = K / BK;
+  if (M > BM || ((N + 127) / 128) * 2 > sms || kblocks < 8) return {0, 1};
+  const int tiles = (N + 63) / 64;
+  int s = sms / tiles;
+  s = s < kblocks / 4 ? s : kblocks / 4;
+  if (s < 2) return {0, 1};
+  const int kb_per = (kblocks + s - 1) / s;
+  return {64, (kblocks + kb_per - 1) / kb_per};
+}
+
+size_t splitk_scratch_bytes(int M, int N, int K) {
+  const SplitPlan sp = pick_split_plan(M, N, K);
+  return sp.splits > 1 ? (size_t)sp.splits * M * N * sizeof(float) : 0;
+}
+
 template <int BN>
 int dispatch(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long long ldb, int M, int N, int K,
-             int kind, int dh, const GemmEpi& ep, cudaStream_t stream) {
+             int kind, int dh, const GemmEpi& ep, cudaStream_t stream, int splits) {
   CUtensorMap ta, tb;
   RDKV_TRY(make_tmap(&ta, A, M, K, lda, BM));
   RDKV_TRY(make_tmap(&tb, B, N, K, ldb, BN));
+  if (splits > 1) {
+    GemmEpi pe = ep;
+    pe.out = ep.splitk_ws;
+    RDKV_TRY((launch_impl<BN, EPI_PARTIAL, 0>(ta, tb, M, N, K, splits, pe, stream)));
+    const float* part = static_cast<const float*>(ep.splitk_ws);
+    switch (kind) {
+      case EPI_STORE: return launch_finalize<EPI_STORE, 0>(part, splits, M, N, ep, stream);
+      case EPI_STORE_F32: return launch_finalize<EPI_STORE_F32, 0>(part, splits, M, N, ep, stream);
+      case EPI_RESID: return launch_finalize<EPI_RESID, 0>(part, splits, M, N, ep, stream);
+      case EPI_SWIGLU: return launch_finalize<EPI_SWIGLU, 0>(part, splits, M, N, ep, stream);
+      case EPI_QKV:
+        if (dh == 64) return launch_finalize<EPI_QKV, 64>(part, splits, M, N, ep, stream);
+        if (dh == 128) return launch_finalize<EPI_QKV, 128>(part, splits, M, N, ep, stream);
+        return set_error(RDKV_ERR_ARG, "qkv: head_dim %d unsupported (64 or 128)", dh);
+      default: return set_error(RDKV_ERR_ARG, "gemm: unknown epilogue %d", kind);
+    }
+  }
+  if constexpr (BN == 64) {
+    return set_error(RDKV_ERR_ARG, "gemm: 64-wide tiles are split-K only");
+  } else {
   switch (kind) {
-    case EPI_STORE: return launch_impl<BN, EPI_STORE, 0>(ta, tb, M, N, K, ep, stream);
-    case EPI_STORE_F32: return launch_impl<BN, EPI_STORE_F32, 0>(ta, tb, M, N, K, ep, stream);
-    case EPI_RESID: return launch_impl<BN, EPI_RESID, 0>(ta, tb, M, N, K, ep, stream);
-    case EPI_SWIGLU: return launch_impl<BN, EPI_SWIGLU, 0>(ta, tb, M, N, K, ep, stream);
+    case EPI_STORE: return launch_impl<BN, EPI_STORE, 0>(ta, tb, M, N, K, 1, ep, stream);
+    case EPI_STORE_F32: return launch_impl<BN, EPI_STORE_F32, 0>(ta, tb, M, N, K, 1, ep, stream);
+    case EPI_RESID: return launch_impl<BN, EPI_RESID, 0>(ta, tb, M, N, K, 1, ep, stream);
+    case EPI_SWIGLU: return launch_impl<BN, EPI_SWIGLU, 0>(ta, tb, M, N, K, 1, ep, stream);
     case EPI_QKV:
-      if (dh == 64) return launch_impl<BN, EPI_QKV, 64>(ta, tb, M, N, K, ep, stream);
-      if (dh == 128) return launch_impl<BN, EPI_QKV, 128>(ta, tb, M, N, K, ep, stream);
+      if (dh == 64) return launch_impl<BN, EPI_QKV, 64>(ta, tb, M, N, K, 1, ep, stream);
+      if (dh == 128) return launch_impl<BN, EPI_QKV, 128>(ta, tb, M, N, K, 1, ep, stream);
       return set_error(RDKV_ERR_ARG, "qkv: head_dim %d unsupported (64 or 128)", dh);
     default: return set_error(RDKV_ERR_ARG, "gemm: unknown epilogue %d", kind);
   }
+  }
 }
 
-int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long long ldb, int M, int N,
-                int K, int kind, int dh, const GemmEpi& ep, cudaStream_t stream, int bn) {
+int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long long ldb, int M, int N, int K,
+                int kind, int dh, const GemmEpi& ep, cudaStream_t stream, int bn) {
   if (M <= 0 || N <= 0) return 0;
   if (K <= 0 || K % BK != 0) return set_error(RDKV_ERR_ARG, "gemm: K=%d must be a positive multiple of 64", K);
   if (N % 32 != 0) return set_error(RDKV_ERR_ARG, "gemm: N=%d must be a multiple of 32", N);
@@ -341,10 +524,24 @@ int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, l
   if ((lda | ldb) & 7) return set_error(RDKV_ERR_ARG, "gemm: leading dims must be multiples of 8");
   if (bn != 0 && bn != 128 && bn != 256) return set_error(RDKV_ERR_ARG, "gemm: tile N %d must be 128 or 256", bn);
   if (kind == EPI_SWIGLU && N % 128 != 0) return set_error(RDKV_ERR_ARG, "swiglu: N must be a multiple of 128");
+  int splits = 1;
+  if (ep.splitk_ws) {
+    if (bn == 0) {
+      const SplitPlan sp = pick_split_plan(M, N, K);
+      if (sp.splits > 1 && (size_t)sp.splits * M * N * sizeof(float) <= ep.splitk_bytes) {
+        bn = sp.bn;
+        splits = sp.splits;
+      }
+    } else {  // explicit tile width (tests): split whenever it would help
+      splits = pick_splits(M, N, K, bn);
+      if ((size_t)splits * M * N * sizeof(float) > ep.splitk_bytes) splits = 1;
+    }
+  }
   if (bn == 0) bn = pick_bn(M, N);
   if (kind == EPI_SWIGLU && N % bn != 0) bn = 128;
-  if (bn == 128) return dispatch<128>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
-  return dispatch<256>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
+  if (bn == 64) return dispatch<64>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream, splits);
+  if (bn == 128) return dispatch<128>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream, splits);
+  return dispatch<256>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream, splits);
 }
 
 }  // namespace rdkv

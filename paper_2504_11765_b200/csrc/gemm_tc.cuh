@@ -21,7 +21,7 @@
 
 namespace rdkv {
 
-enum EpiKind : int { EPI_STORE = 0, EPI_STORE_F32 = 1, EPI_RESID = 2, EPI_SWIGLU = 3, EPI_QKV = 4 };
+enum EpiKind : int { EPI_STORE = 0, EPI_STORE_F32 = 1, EPI_RESID = 2, EPI_SWIGLU = 3, EPI_QKV = 4, EPI_PARTIAL = 5 };
 
 struct GemmEpi {
   void* out;                 // bf16 (or fp32 for STORE_F32)
@@ -38,7 +38,13 @@ struct GemmEpi {
   const int* pos;            // per row: RoPE position
   const float* rope;         // [max_pos][dh/2] x (cos, sin)
   int hq, hkv;
+  // split-K scratch (fp32 slabs); null disables split-K
+  void* splitk_ws;
+  size_t splitk_bytes;
 };
+
+// Scratch bytes split-K would use for this GEMM shape (0 if it would not split).
+size_t splitk_scratch_bytes(int M, int N, int K);
 
 // bn = tile N (128 or 256), 0 = choose by wave quantisation
 int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long long ldb, int M,

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <new>
+#include <algorithm>
 #include <vector>
 
 #include "attention.cuh"
@@ -78,6 +79,8 @@ inline size_t up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Ws {
   __nv_bfloat16 *x, *h, *q, *o, *a, *hl;
+  void* splitk;
+  size_t splitk_bytes;
 };
 
 size_t ws_layout(const rdkv_model_desc& d, int T, int S, Ws* ws, void* base) {
@@ -91,7 +94,17 @@ size_t ws_layout(const rdkv_model_desc& d, int T, int S, Ws* ws, void* base) {
   const size_t ox = take((size_t)T * d.hidden * 2), oh = take((size_t)T * d.hidden * 2);
   const size_t oq = take((size_t)T * qd * 2), oo = take((size_t)T * qd * 2);
   const size_t oa = take((size_t)T * d.ffn * 2), ol = take((size_t)(S > 0 ? S : 1) * d.hidden * 2);
+  // split-K scratch for small-M GEMMs (largest of the per-layer shapes and the LM head)
+  const int qkv_n = (d.n_heads + 2 * d.kv_heads) * d.head_dim;
+  size_t sk = splitk_scratch_bytes(T, qkv_n, d.hidden);
+  sk = std::max(sk, splitk_scratch_bytes(T, d.hidden, (int)qd));
+  sk = std::max(sk, splitk_scratch_bytes(T, 2 * d.ffn, d.hidden));
+  sk = std::max(sk, splitk_scratch_bytes(T, d.hidden, d.ffn));
+  sk = std::max(sk, splitk_scratch_bytes(S > 0 ? S : 1, d.vocab, d.hidden));
+  const size_t osk = take(sk);
   if (ws && base) {
+    ws->splitk = sk ? static_cast<uint8_t*>(base) + osk : nullptr;
+    ws->splitk_bytes = sk;
     auto* b = static_cast<uint8_t*>(base);
     ws->x = reinterpret_cast<__nv_bfloat16*>(b + ox);
     ws->h = reinterpret_cast<__nv_bfloat16*>(b + oh);
@@ -199,6 +212,8 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     // attention block
     LAUNCH(RDKV_PROF_MISC, 0.0, launch_rmsnorm(ws.x, d.hidden, nullptr, G(m, wb + 0), ws.h, d.hidden, T, d.hidden, d.norm_eps, st));
     GemmEpi eq{};
+    eq.splitk_ws = ws.splitk;
+    eq.splitk_bytes = ws.splitk_bytes;
     eq.q = ws.q;
     eq.ldq = qd;
     eq.kplane = kpl;
@@ -235,6 +250,8 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     else
       LAUNCH(RDKV_PROF_ATTN, 0.0, launch_attention(ap, dh, S, b->max_new, st));
     GemmEpi er{};
+    er.splitk_ws = ws.splitk;
+    er.splitk_bytes = ws.splitk_bytes;
     er.out = ws.x;
     er.ldo = d.hidden;
     er.resid = ws.x;
@@ -243,6 +260,8 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     // MLP block
     LAUNCH(RDKV_PROF_MISC, 0.0, launch_rmsnorm(ws.x, d.hidden, nullptr, G(m, wb + 3), ws.h, d.hidden, T, d.hidden, d.norm_eps, st));
     GemmEpi eg{};
+    eg.splitk_ws = ws.splitk;
+    eg.splitk_bytes = ws.splitk_bytes;
     eg.out = ws.a;
     eg.ldo = d.ffn;
     LAUNCH(RDKV_PROF_GEMM, 4.0 * T * d.ffn * d.hidden, launch_gemm(ws.h, d.hidden, W(m, wb + 4), d.hidden, T, 2 * d.ffn, d.hidden, EPI_SWIGLU, 0, eg, st));
@@ -253,6 +272,8 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     const int fn = 1 + RDKV_WEIGHTS_PER_LAYER * d.layers;
     LAUNCH(RDKV_PROF_HEAD, 0.0, launch_rmsnorm(ws.x, d.hidden, b->last_row, G(m, fn), ws.hl, d.hidden, S, d.hidden, d.norm_eps, st));
     GemmEpi el{};
+    el.splitk_ws = ws.splitk;
+    el.splitk_bytes = ws.splitk_bytes;
     el.out = b->logits;
     el.ldo = d.vocab;
     LAUNCH(RDKV_PROF_HEAD, 2.0 * S * d.vocab * d.hidden, launch_gemm(ws.hl, d.hidden, W(m, fn + 1), d.hidden, S, d.vocab, d.hidden, EPI_STORE_F32, 0, el, st));
