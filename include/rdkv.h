@@ -214,6 +214,8 @@ typedef struct rdkv_batch {
   int64_t kv_slots;
   float* logits;               /* dev [S][vocab] fp32                                */
   int32_t* next_token;         /* dev [S] argmax (first token), may be NULL          */
+  int32_t max_ctx;             /* max over sequences of n_cached + n_new (0: unknown;
+                                  enables split-KV attention for small batches)      */
 } rdkv_batch;
 
 /* Device workspace needed by rdkv_forward for n_tokens / n_seqs. */

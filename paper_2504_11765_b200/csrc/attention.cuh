@@ -21,7 +21,17 @@ struct AttnParams {
   int hq, hkv;
   float scale_log2;             // log2(e) / sqrt(dh)
   int contiguous;               // 1: each sequence's KV is one block (blob layout)
+  // split-KV (tensor-core kernel): scratch for per-split partials, chosen at launch
+  int kv_splits;
+  int n_tokens;                 // T (rows of q / o)
+  int max_ctx;                  // max over sequences of n_cached + n_new
+  float* split_o;               // [splits][T][hq][dh] fp32
+  float2* split_ml;             // [splits][T][hq] (max, sum)
+  size_t split_bytes;
 };
+
+// split-KV scratch bytes for T tokens (0 when T is too large to ever split)
+size_t attention_split_scratch_bytes(int T, int hq, int dh);
 
 // mma.sync kernel (any group size dividing 128, any block size)
 int launch_attention(const AttnParams& p, int head_dim, int n_seqs, int max_new, cudaStream_t st);

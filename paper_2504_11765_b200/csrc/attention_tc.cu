@@ -93,7 +93,8 @@ __global__ void __launch_bounds__(384, 1)
 
   const int G = p.hq / p.hkv;
   const int s = blockIdx.z, kvh = blockIdx.y;
-  const int qb = gridDim.x - 1 - blockIdx.x;  // longest causal rows first
+  const int xb = gridDim.x - 1 - blockIdx.x;  // longest causal rows first
+  const int qb = xb / p.kv_splits, ks = xb % p.kv_splits;  // query block, KV split
   const int n_new = p.seq_new[s];
   const int tok_per_cta = ROWS / G;
   const int tok0 = qb * tok_per_cta;
@@ -102,7 +103,11 @@ __global__ void __launch_bounds__(384, 1)
   const int nrows = ntok * G;
   const int pos0 = p.seq_cached[s] + tok0;
   const int kv_len = pos0 + ntok;
-  const int n_tiles = (kv_len + BKV - 1) / BKV;
+  // this CTA's share of the KV tiles (split-KV when the grid alone cannot fill the GPU)
+  const int n_all = (kv_len + BKV - 1) / BKV;
+  const int per_split = (n_all + p.kv_splits - 1) / p.kv_splits;
+  const int t_begin = ks * per_split;
+  const int n_tiles = max(0, min(n_all, t_begin + per_split) - t_begin);
   const int row_base = p.seq_start[s] + tok0;
   const int* bt = p.block_table + (long long)s * p.bt_stride;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -146,8 +151,8 @@ __global__ void __launch_bounds__(384, 1)
         int rows[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          int pos = j * BKV + h * HALF;
-          if (pos >= kv_len) pos = j * BKV;  // masked half: any valid, finite block
+          int pos = (t_begin + j) * BKV + h * HALF;
+          if (pos >= kv_len) pos = (t_begin + j) * BKV;  // masked half: any valid, finite block
           rows[h] = (int)(row0 + (long long)bt[pos / p.block_size] * p.block_size + pos % p.block_size);
         }
         mbar_arrive_expect_tx(&k_full[st], C::KB);
@@ -203,7 +208,7 @@ __global__ void __launch_bounds__(384, 1)
         umma_commit(&p_empty[b]);
         umma_commit(&kv_empty[st]);
       };
-      issue_qk(0);
+      if (n_tiles > 0) issue_qk(0);
       for (int j = 0; j < n_tiles; ++j) {
         if (j + 1 < n_tiles) issue_qk(j + 1);
         issue_pv(j);
@@ -272,7 +277,7 @@ __global__ void __launch_bounds__(384, 1)
       const int b = j & 1;
       mbar_wait(&s_full[b], (j >> 1) & 1);
       tc_fence_after();
-      const int kbase = j * BKV + h * 64;       // first key of this half
+      const int kbase = (t_begin + j) * BKV + h * 64;  // first key of this half
       const int lim0 = kmax - kbase;            // element e visible iff e <= lim0
       const bool need_mask = lim0 < 63;
       const uint32_t scol = tS + b * BKV + h * 64 + lane_off;
@@ -334,7 +339,7 @@ __global__ void __launch_bounds__(384, 1)
       if (j >= 1) consume(j - 1, m_pend);
       m_pend = mx;
     }
-    consume(n_tiles - 1, m_pend);
+    if (n_tiles > 0) consume(n_tiles - 1, m_pend);
     // total row sum = both halves; then normalise and store this half of the row
     // the parity slot the last tile did NOT use is free (its readers passed the last pair_sync)
     const int fs = n_tiles & 1;
@@ -342,15 +347,26 @@ __global__ void __launch_bounds__(384, 1)
     pair_sync();
     const float lt = l + red[(fs * 2 + (h ^ 1)) * ROWS + r];
     if (r < nrows) {
-      const float inv = 1.f / lt;
-      uint4* dst = reinterpret_cast<uint4*>(p.o + (long long)(row_base + r / G) * p.ldo +
-                                            (long long)(kvh * G + r % G) * DH + h * OD);
+      const long long trow = row_base + r / G;  // token row in [0, T)
+      const int head = kvh * G + r % G;
+      if (p.kv_splits > 1) {
+        // unnormalised partial at scale m_acc; combined by attn_split_combine_kernel
+        float* dst = p.split_o + (((long long)ks * p.n_tokens + trow) * p.hq + head) * DH + h * OD;
 #pragma unroll
-      for (int c = 0; c < OD / 8; ++c)
-        dst[c] = make_uint4(pack_bf16(o_acc[8 * c] * inv, o_acc[8 * c + 1] * inv),
-                            pack_bf16(o_acc[8 * c + 2] * inv, o_acc[8 * c + 3] * inv),
-                            pack_bf16(o_acc[8 * c + 4] * inv, o_acc[8 * c + 5] * inv),
-                            pack_bf16(o_acc[8 * c + 6] * inv, o_acc[8 * c + 7] * inv));
+        for (int c = 0; c < OD / 4; ++c)
+          reinterpret_cast<float4*>(dst)[c] =
+              make_float4(o_acc[4 * c], o_acc[4 * c + 1], o_acc[4 * c + 2], o_acc[4 * c + 3]);
+        if (h == 0) p.split_ml[((long long)ks * p.n_tokens + trow) * p.hq + head] = make_float2(m_acc, lt);
+      } else {
+        const float inv = 1.f / lt;
+        uint4* dst = reinterpret_cast<uint4*>(p.o + trow * p.ldo + (long long)head * DH + h * OD);
+#pragma unroll
+        for (int c = 0; c < OD / 8; ++c)
+          dst[c] = make_uint4(pack_bf16(o_acc[8 * c] * inv, o_acc[8 * c + 1] * inv),
+                              pack_bf16(o_acc[8 * c + 2] * inv, o_acc[8 * c + 3] * inv),
+                              pack_bf16(o_acc[8 * c + 4] * inv, o_acc[8 * c + 5] * inv),
+                              pack_bf16(o_acc[8 * c + 6] * inv, o_acc[8 * c + 7] * inv));
+      }
     }
   }
   __syncthreads();
@@ -358,6 +374,31 @@ __global__ void __launch_bounds__(384, 1)
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
+}
+
+// Merge the KV-split partials of every (token, head): O = sum_s o_s 2^(m_s-M) / sum_s l_s 2^(m_s-M).
+template <int DH>
+__global__ void __launch_bounds__(256) attn_split_combine_kernel(AttnParams p) {
+  const int t = blockIdx.x, head = blockIdx.y * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (head >= p.hq) return;
+  float M = -INFINITY;
+  for (int k = 0; k < p.kv_splits; ++k) M = fmaxf(M, p.split_ml[((long long)k * p.n_tokens + t) * p.hq + head].x);
+  constexpr int PER = DH / 32;
+  float acc[PER] = {};
+  float L = 0.f;
+  for (int k = 0; k < p.kv_splits; ++k) {
+    const float2 ml = p.split_ml[((long long)k * p.n_tokens + t) * p.hq + head];
+    if (ml.x == -INFINITY) continue;
+    const float w = ex2_approx(ml.x - M);
+    L += ml.y * w;
+    const float* src = p.split_o + (((long long)k * p.n_tokens + t) * p.hq + head) * DH;
+#pragma unroll
+    for (int e = 0; e < PER; ++e) acc[e] += src[lane + 32 * e] * w;
+  }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  __nv_bfloat16* dst = p.o + (long long)t * p.ldo + (long long)head * DH;
+#pragma unroll
+  for (int e = 0; e < PER; ++e) dst[lane + 32 * e] = __float2bfloat16(acc[e] * inv);
 }
 
 template <int DH>
@@ -374,9 +415,26 @@ int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
   RDKV_TRY(make_tmap(&tk, p.kplane, rows, DH, DH, HALF));
   RDKV_TRY(make_tmap(&tv, p.vplane, rows, DH, DH, HALF));
   const int tok_per_cta = ROWS / (p.hq / p.hkv);
-  dim3 grid((max_new + tok_per_cta - 1) / tok_per_cta, p.hkv, n_seqs);
-  attn_tc_kernel<DH><<<grid, 384, C::SMEM, st>>>(tk, tv, p);
+  const int qblocks = (max_new + tok_per_cta - 1) / tok_per_cta;
+  // split the KV range when the (query block x kv head x sequence) grid is too
+  // small for 148 SMs (single-query TTFT) and scratch is available
+  AttnParams q = p;
+  q.kv_splits = 1;
+  const int ctas = qblocks * p.hkv * n_seqs, sms = num_sms();
+  const int max_tiles = (p.max_ctx + BKV - 1) / BKV;
+  if (p.split_o && ctas * 2 <= sms && max_tiles >= 4) {
+    int k = sms / ctas;
+    k = k < max_tiles / 2 ? k : max_tiles / 2;
+    k = k < 16 ? k : 16;
+    if (k >= 2 && (size_t)k * p.n_tokens * p.hq * (DH * 4 + 8) <= p.split_bytes) q.kv_splits = k;
+  }
+  dim3 grid(qblocks * q.kv_splits, p.hkv, n_seqs);
+  attn_tc_kernel<DH><<<grid, 384, C::SMEM, st>>>(tk, tv, q);
   CUDA_TRY(cudaGetLastError());
+  if (q.kv_splits > 1) {
+    attn_split_combine_kernel<DH><<<dim3(p.n_tokens, (p.hq + 7) / 8), 256, 0, st>>>(q);
+    CUDA_TRY(cudaGetLastError());
+  }
   return 0;
 }
 
@@ -396,4 +454,11 @@ int launch_attention_tc(const AttnParams& p, int head_dim, int n_seqs, int max_n
   return launch_tc<128>(p, n_seqs, max_new, st);
 }
 
+}  // namespace rdkv
+
+namespace rdkv {
+size_t attention_split_scratch_bytes(int T, int hq, int dh) {
+  if (T <= 0 || T > 512) return 0;
+  return (size_t)16 * T * hq * (dh * 4 + 8);
+}
 }  // namespace rdkv

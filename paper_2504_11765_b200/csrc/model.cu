@@ -81,6 +81,8 @@ struct Ws {
   __nv_bfloat16 *x, *h, *q, *o, *a, *hl;
   void* splitk;
   size_t splitk_bytes;
+  void* attn_split;
+  size_t attn_split_bytes;
 };
 
 size_t ws_layout(const rdkv_model_desc& d, int T, int S, Ws* ws, void* base) {
@@ -102,7 +104,11 @@ size_t ws_layout(const rdkv_model_desc& d, int T, int S, Ws* ws, void* base) {
   sk = std::max(sk, splitk_scratch_bytes(T, d.hidden, d.ffn));
   sk = std::max(sk, splitk_scratch_bytes(S > 0 ? S : 1, d.vocab, d.hidden));
   const size_t osk = take(sk);
+  const size_t ask = attention_split_scratch_bytes(T, d.n_heads, d.head_dim);
+  const size_t oask = take(ask);
   if (ws && base) {
+    ws->attn_split = ask ? static_cast<uint8_t*>(base) + oask : nullptr;
+    ws->attn_split_bytes = ask;
     ws->splitk = sk ? static_cast<uint8_t*>(base) + osk : nullptr;
     ws->splitk_bytes = sk;
     auto* b = static_cast<uint8_t*>(base);
@@ -245,6 +251,15 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     ap.hkv = hkv;
     ap.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)dh));
     ap.contiguous = b->bt_stride == 1 ? 1 : 0;
+    ap.kv_splits = 1;
+    ap.n_tokens = T;
+    ap.max_ctx = b->max_ctx > 0 ? b->max_ctx : 0;
+    if (ws.attn_split && b->max_ctx > 0) {
+      const size_t o_bytes = (size_t)16 * T * hq * dh * 4;
+      ap.split_o = static_cast<float*>(ws.attn_split);
+      ap.split_ml = reinterpret_cast<float2*>(static_cast<uint8_t*>(ws.attn_split) + o_bytes);
+      ap.split_bytes = ws.attn_split_bytes;
+    }
     if (use_tc_attn && attention_tc_supported(ap, dh))
       LAUNCH(RDKV_PROF_ATTN, 0.0, launch_attention_tc(ap, dh, S, b->max_new, st));
     else

@@ -47,7 +47,7 @@ class RdkvBatch(C.Structure):
                 ("tokens", C.c_void_p), ("pos", C.c_void_p), ("slot", C.c_void_p), ("seq_start", C.c_void_p),
                 ("seq_new", C.c_void_p), ("seq_cached", C.c_void_p), ("block_table", C.c_void_p),
                 ("last_row", C.c_void_p), ("kv_base", C.c_void_p), ("kv_slots", C.c_int64),
-                ("logits", C.c_void_p), ("next_token", C.c_void_p)]
+                ("logits", C.c_void_p), ("next_token", C.c_void_p), ("max_ctx", C.c_int32)]
 
 
 class RdkvUnpackJob(C.Structure):
@@ -186,6 +186,7 @@ class BatchPlan:
         self.n_seqs, self.n_tokens, self.max_new = S, T, int(n_new.max())
         self.bt_stride, self.block_size = bt_stride, block_size
         self.n_new, self.n_cached = n_new, cached
+        self.max_ctx = int((n_new + cached).max())
         self.rebase(host.to(device, non_blocking=True))
 
     _FIELDS = ("tokens", "pos", "slot", "seq_start", "seq_new", "seq_cached", "block_table", "last_row")
@@ -197,7 +198,8 @@ class BatchPlan:
         self.ptr = {k: base + 4 * int(o) for k, o in zip(self._FIELDS, self._offs[:-1])}
 
     def signature(self) -> tuple:
-        return (self.n_seqs, self.n_tokens, self.max_new, self.bt_stride, self.block_size)
+        # max_ctx fixes the split-KV choice baked into a captured graph
+        return (self.n_seqs, self.n_tokens, self.max_new, self.bt_stride, self.block_size, self.max_ctx)
 
     def struct(self, kv_base: int, kv_slots: int, logits=None, next_token=None) -> RdkvBatch:
         p = self.ptr
@@ -208,7 +210,7 @@ class BatchPlan:
             seq_cached=p["seq_cached"], block_table=p["block_table"], last_row=p["last_row"],
             kv_base=kv_base, kv_slots=kv_slots,
             logits=logits.data_ptr() if logits is not None else None,
-            next_token=next_token.data_ptr() if next_token is not None else None)
+            next_token=next_token.data_ptr() if next_token is not None else None, max_ctx=self.max_ctx)
 
 
 # ----------------------------------------------------------------- the model handle

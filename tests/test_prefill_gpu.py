@@ -67,6 +67,19 @@ def test_cached_prefix_query_matches_full_prompt(setup):
     assert rel_err(logits[0], full_logits[0]) <= TOL
 
 
+def test_long_cached_prefix_split_kv(setup):
+    """A single query over a long cached prefix: the grid is tiny, so the
+    tensor-core attention splits the KV range across CTAs and merges partials."""
+    spec, eng, orc = setup
+    prefix = combo_tokens([21, 22, 23], [512, 512, 476], spec.vocab)    # 1500 cached tokens
+    new = query_tokens(9, 40, spec.vocab)
+    cached = eng.generate_doc_kv(prefix)
+    logits, nxt = eng.prefill([QueryRequest(new, cached, len(prefix))])
+    torch.cuda.synchronize()
+    _, ref = orc.forward(np.concatenate([prefix, new]))
+    _check_logits(logits[0], ref, nxt[0])
+
+
 def test_batched_ragged_equals_single(setup):
     spec, eng, orc = setup
     reqs, singles = [], []
