@@ -369,6 +369,63 @@ __global__ void __launch_bounds__(256) splitk_finalize_kernel(const float* __res
   }
 }
 
+// RESID finalize with the following RMSNorm fused in (one CTA per row, N <= 8192):
+// x = resid + sum(partials) -> bf16 -> out; h = x * rsqrt(mean(x^2) + eps) * gain -> norm_out.
+__global__ void __launch_bounds__(256) splitk_resid_norm_kernel(const float* __restrict__ part, int splits, int M,
+                                                                int N, GemmEpi ep) {
+  constexpr int MAXC = 8;
+  const int row = blockIdx.x;
+  const long long slab = (long long)M * N;
+  const float* pr = part + (long long)row * N;
+  float xs[MAXC][4];
+  float ss = 0.f;
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) {
+    const int j = (c * 256 + threadIdx.x) * 4;
+    if (j < N) {
+      float4 t = *reinterpret_cast<const float4*>(pr + j);
+      for (int k = 1; k < splits; ++k) {
+        const float4 u = *reinterpret_cast<const float4*>(pr + k * slab + j);
+        t.x += u.x;
+        t.y += u.y;
+        t.z += u.z;
+        t.w += u.w;
+      }
+      const uint2 r = *reinterpret_cast<const uint2*>(ep.resid + (long long)row * ep.ldr + j);
+      const float2 a = unpack_bf16(r.x), b = unpack_bf16(r.y);
+      uint2 w;
+      w.x = pack_bf16(t.x + a.x, t.y + a.y);
+      w.y = pack_bf16(t.z + b.x, t.w + b.y);
+      *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + j) = w;
+      const float2 p0 = unpack_bf16(w.x), p1 = unpack_bf16(w.y);  // normalise the rounded residual
+      xs[c][0] = p0.x;
+      xs[c][1] = p0.y;
+      xs[c][2] = p1.x;
+      xs[c][3] = p1.y;
+      ss += p0.x * p0.x + p0.y * p0.y + p1.x * p1.x + p1.y * p1.y;
+    }
+  }
+  __shared__ float red[8];
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) tot += red[w];
+  const float inv = rsqrtf(tot / (float)N + ep.norm_eps);
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) {
+    const int j = (c * 256 + threadIdx.x) * 4;
+    if (j < N) {
+      const float4 g = *reinterpret_cast<const float4*>(ep.norm_gain + j);
+      uint2 w;
+      w.x = pack_bf16(xs[c][0] * inv * g.x, xs[c][1] * inv * g.y);
+      w.y = pack_bf16(xs[c][2] * inv * g.z, xs[c][3] * inv * g.w);
+      *reinterpret_cast<uint2*>(ep.norm_out + (long long)row * N + j) = w;
+    }
+  }
+}
+
 template <int BN, int EPI, int DH>
 int launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, int splits, const GemmEpi& ep,
                 cudaStream_t stream) {
@@ -469,6 +526,11 @@ SplitPlan pick_split_plan(int M, int N, int K) {
   return {64, (kblocks + kb_per - 1) / kb_per};
 }
 
+bool gemm_splits(int M, int N, int K, size_t splitk_bytes) {
+  const SplitPlan sp = pick_split_plan(M, N, K);
+  return sp.splits > 1 && (size_t)sp.splits * M * N * sizeof(float) <= splitk_bytes;
+}
+
 size_t splitk_scratch_bytes(int M, int N, int K) {
   const SplitPlan sp = pick_split_plan(M, N, K);
   return sp.splits > 1 ? (size_t)sp.splits * M * N * sizeof(float) : 0;
@@ -488,7 +550,14 @@ int dispatch(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long
     switch (kind) {
       case EPI_STORE: return launch_finalize<EPI_STORE, 0>(part, splits, M, N, ep, stream);
       case EPI_STORE_F32: return launch_finalize<EPI_STORE_F32, 0>(part, splits, M, N, ep, stream);
-      case EPI_RESID: return launch_finalize<EPI_RESID, 0>(part, splits, M, N, ep, stream);
+      case EPI_RESID:
+        if (ep.norm_out) {
+          if (N > 8192 || N % 4) return set_error(RDKV_ERR_ARG, "resid+norm finalize: N must be <= 8192, %% 4");
+          splitk_resid_norm_kernel<<<M, 256, 0, stream>>>(part, splits, M, N, ep);
+          CUDA_TRY(cudaGetLastError());
+          return 0;
+        }
+        return launch_finalize<EPI_RESID, 0>(part, splits, M, N, ep, stream);
       case EPI_SWIGLU: return launch_finalize<EPI_SWIGLU, 0>(part, splits, M, N, ep, stream);
       case EPI_QKV:
         if (dh == 64) return launch_finalize<EPI_QKV, 64>(part, splits, M, N, ep, stream);

@@ -41,7 +41,14 @@ struct GemmEpi {
   // split-K scratch (fp32 slabs); null disables split-K
   void* splitk_ws;
   size_t splitk_bytes;
+  // optional RMSNorm fused into the split-K RESID finalize: norm_out = rmsnorm(out) * norm_gain
+  const float* norm_gain;
+  __nv_bfloat16* norm_out;
+  float norm_eps;
 };
+
+// True when launch_gemm will take the split-K path for this shape (small M).
+bool gemm_splits(int M, int N, int K, size_t splitk_bytes);
 
 // Scratch bytes split-K would use for this GEMM shape (0 if it would not split).
 size_t splitk_scratch_bytes(int M, int N, int K);

@@ -129,47 +129,54 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const __nv_bfloat16* __res
 }
 
 // ---------------------------------------------------------------- argmax
-__global__ void __launch_bounds__(1024) argmax_kernel(const float* __restrict__ logits, long long ld, int n,
-                                                      int* __restrict__ out) {
-  const float* row = logits + (long long)blockIdx.x * ld;
+// Two stages so a [rows x 128k] logit matrix spreads over many SMs:
+// (1) grid (rows, ARGMAX_CH): each CTA reduces a contiguous chunk -> (value, index);
+// (2) one warp per row reduces the chunk winners.  Ties resolve to the lowest
+// index (torch.argmax's first-occurrence rule) at every level.
+constexpr int ARGMAX_CH = 32;
+
+__device__ __forceinline__ void argmax_merge(float& best, int& idx, float vb, int ib) {
+  if (vb > best || (vb == best && ib < idx)) {
+    best = vb;
+    idx = ib;
+  }
+}
+
+__global__ void __launch_bounds__(256) argmax_chunk_kernel(const float* __restrict__ logits, long long ld, int n,
+                                                          float2* __restrict__ part) {
+  const int row = blockIdx.x, ch = blockIdx.y;
+  const int len = (n + ARGMAX_CH - 1) / ARGMAX_CH;
+  const int lo = ch * len, hi = min(n, lo + len);
+  const float* r = logits + (long long)row * ld;
   float best = -INFINITY;
   int idx = 0x7fffffff;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const float v = row[i];
-    if (v > best) {  // strided scan: first occurrence within this thread
-      best = v;
-      idx = i;
-    }
-  }
-  for (int o = 16; o; o >>= 1) {
-    const float vb = __shfl_xor_sync(0xffffffff, best, o);
-    const int ib = __shfl_xor_sync(0xffffffff, idx, o);
-    if (vb > best || (vb == best && ib < idx)) {
-      best = vb;
-      idx = ib;
-    }
-  }
-  __shared__ float sv[32];
-  __shared__ int si[32];
+  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) argmax_merge(best, idx, r[i], i);
+  for (int o = 16; o; o >>= 1)
+    argmax_merge(best, idx, __shfl_xor_sync(0xffffffff, best, o), __shfl_xor_sync(0xffffffff, idx, o));
+  __shared__ float sv[8];
+  __shared__ int si[8];
   if ((threadIdx.x & 31) == 0) {
     sv[threadIdx.x >> 5] = best;
     si[threadIdx.x >> 5] = idx;
   }
   __syncthreads();
   if (threadIdx.x < 32) {
-    const int nw = blockDim.x >> 5;
-    best = threadIdx.x < nw ? sv[threadIdx.x] : -INFINITY;
-    idx = threadIdx.x < nw ? si[threadIdx.x] : 0x7fffffff;
-    for (int o = 16; o; o >>= 1) {
-      const float vb = __shfl_xor_sync(0xffffffff, best, o);
-      const int ib = __shfl_xor_sync(0xffffffff, idx, o);
-      if (vb > best || (vb == best && ib < idx)) {
-        best = vb;
-        idx = ib;
-      }
-    }
-    if (threadIdx.x == 0) out[blockIdx.x] = idx;
+    best = threadIdx.x < 8 ? sv[threadIdx.x] : -INFINITY;
+    idx = threadIdx.x < 8 ? si[threadIdx.x] : 0x7fffffff;
+    for (int o = 16; o; o >>= 1)
+      argmax_merge(best, idx, __shfl_xor_sync(0xffffffff, best, o), __shfl_xor_sync(0xffffffff, idx, o));
+    if (threadIdx.x == 0) part[row * ARGMAX_CH + ch] = make_float2(best, __int_as_float(idx));
   }
+}
+
+__global__ void argmax_final_kernel(const float2* __restrict__ part, int* __restrict__ out) {
+  const int row = blockIdx.x, lane = threadIdx.x;
+  const float2 p = part[row * ARGMAX_CH + lane];
+  float best = p.x;
+  int idx = __float_as_int(p.y);
+  for (int o = 16; o; o >>= 1)
+    argmax_merge(best, idx, __shfl_xor_sync(0xffffffff, best, o), __shfl_xor_sync(0xffffffff, idx, o));
+  if (lane == 0) out[row] = idx;
 }
 
 }  // namespace
@@ -210,9 +217,15 @@ int launch_rmsnorm(const __nv_bfloat16* x, long long ldx, const int* rows, const
   return 0;
 }
 
-int launch_argmax(const float* logits, long long ld, int rows, int n, int* out, cudaStream_t st) {
+size_t argmax_scratch_bytes(int rows) { return (size_t)(rows > 0 ? rows : 1) * ARGMAX_CH * sizeof(float2); }
+
+int launch_argmax(const float* logits, long long ld, int rows, int n, int* out, void* scratch, cudaStream_t st) {
   if (rows <= 0) return 0;
-  argmax_kernel<<<rows, 1024, 0, st>>>(logits, ld, n, out);
+  static_assert(ARGMAX_CH == 32, "final stage is one warp");
+  auto* part = static_cast<float2*>(scratch);
+  argmax_chunk_kernel<<<dim3(rows, ARGMAX_CH), 256, 0, st>>>(logits, ld, n, part);
+  CUDA_TRY(cudaGetLastError());
+  argmax_final_kernel<<<rows, 32, 0, st>>>(part, out);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }

@@ -22,6 +22,7 @@ int launch_embed(const int* tok, const __nv_bfloat16* table, __nv_bfloat16* out,
                  cudaStream_t st);
 int launch_rmsnorm(const __nv_bfloat16* x, long long ldx, const int* rows, const float* gain, __nv_bfloat16* out,
                    long long ldo, int n_rows, int d, float eps, cudaStream_t st);
-int launch_argmax(const float* logits, long long ld, int rows, int n, int* out, cudaStream_t st);
+size_t argmax_scratch_bytes(int rows);
+int launch_argmax(const float* logits, long long ld, int rows, int n, int* out, void* scratch, cudaStream_t st);
 
 }  // namespace rdkv

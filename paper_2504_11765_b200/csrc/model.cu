@@ -83,6 +83,7 @@ struct Ws {
   size_t splitk_bytes;
   void* attn_split;
   size_t attn_split_bytes;
+  void* argmax;
 };
 
 size_t ws_layout(const rdkv_model_desc& d, int T, int S, Ws* ws, void* base) {
@@ -106,7 +107,9 @@ size_t ws_layout(const rdkv_model_desc& d, int T, int S, Ws* ws, void* base) {
   const size_t osk = take(sk);
   const size_t ask = attention_split_scratch_bytes(T, d.n_heads, d.head_dim);
   const size_t oask = take(ask);
+  const size_t oam = take(argmax_scratch_bytes(S));
   if (ws && base) {
+    ws->argmax = static_cast<uint8_t*>(base) + oam;
     ws->attn_split = ask ? static_cast<uint8_t*>(base) + oask : nullptr;
     ws->attn_split_bytes = ask;
     ws->splitk = sk ? static_cast<uint8_t*>(base) + osk : nullptr;
@@ -211,12 +214,18 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
   }();
 
   LAUNCH(RDKV_PROF_MISC, 0.0, launch_embed(b->tokens, W(m, 0), ws.x, T, d.hidden, d.vocab, st));
+  // small batches run the residual GEMMs split-K; their finalize also applies the
+  // following RMSNorm, saving a launch per norm
+  const bool o_fused = gemm_splits(T, d.hidden, (int)qd, ws.splitk_bytes);
+  const bool down_fused = gemm_splits(T, d.hidden, d.ffn, ws.splitk_bytes);
+  bool h_ready = false;  // ws.h already holds this layer's attention-norm output
   for (int l = 0; l < d.layers; ++l) {
     const int wb = 1 + RDKV_WEIGHTS_PER_LAYER * l;
     __nv_bfloat16* kpl = kv + (2LL * l) * plane;
     __nv_bfloat16* vpl = kv + (2LL * l + 1) * plane;
     // attention block
-    LAUNCH(RDKV_PROF_MISC, 0.0, launch_rmsnorm(ws.x, d.hidden, nullptr, G(m, wb + 0), ws.h, d.hidden, T, d.hidden, d.norm_eps, st));
+    if (!h_ready)
+      LAUNCH(RDKV_PROF_MISC, 0.0, launch_rmsnorm(ws.x, d.hidden, nullptr, G(m, wb + 0), ws.h, d.hidden, T, d.hidden, d.norm_eps, st));
     GemmEpi eq{};
     eq.splitk_ws = ws.splitk;
     eq.splitk_bytes = ws.splitk_bytes;
@@ -271,15 +280,24 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     er.ldo = d.hidden;
     er.resid = ws.x;
     er.ldr = d.hidden;
+    er.norm_eps = d.norm_eps;
+    if (o_fused) {
+      er.norm_gain = G(m, wb + 3);
+      er.norm_out = ws.h;
+    }
     LAUNCH(RDKV_PROF_GEMM, 2.0 * T * qd * d.hidden, launch_gemm(ws.o, qd, W(m, wb + 2), qd, T, d.hidden, (int)qd, EPI_RESID, 0, er, st));
     // MLP block
-    LAUNCH(RDKV_PROF_MISC, 0.0, launch_rmsnorm(ws.x, d.hidden, nullptr, G(m, wb + 3), ws.h, d.hidden, T, d.hidden, d.norm_eps, st));
+    if (!o_fused)
+      LAUNCH(RDKV_PROF_MISC, 0.0, launch_rmsnorm(ws.x, d.hidden, nullptr, G(m, wb + 3), ws.h, d.hidden, T, d.hidden, d.norm_eps, st));
     GemmEpi eg{};
     eg.splitk_ws = ws.splitk;
     eg.splitk_bytes = ws.splitk_bytes;
     eg.out = ws.a;
     eg.ldo = d.ffn;
     LAUNCH(RDKV_PROF_GEMM, 4.0 * T * d.ffn * d.hidden, launch_gemm(ws.h, d.hidden, W(m, wb + 4), d.hidden, T, 2 * d.ffn, d.hidden, EPI_SWIGLU, 0, eg, st));
+    h_ready = down_fused && l + 1 < d.layers;
+    er.norm_gain = h_ready ? G(m, wb + RDKV_WEIGHTS_PER_LAYER + 0) : nullptr;  // next layer's attention norm
+    er.norm_out = h_ready ? ws.h : nullptr;
     LAUNCH(RDKV_PROF_GEMM, 2.0 * T * d.ffn * d.hidden, launch_gemm(ws.a, d.ffn, W(m, wb + 5), d.ffn, T, d.hidden, d.ffn, EPI_RESID, 0, er, st));
   }
   if (b->want_logits) {
@@ -292,7 +310,7 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     el.out = b->logits;
     el.ldo = d.vocab;
     LAUNCH(RDKV_PROF_HEAD, 2.0 * S * d.vocab * d.hidden, launch_gemm(ws.hl, d.hidden, W(m, fn + 1), d.hidden, S, d.vocab, d.hidden, EPI_STORE_F32, 0, el, st));
-    if (b->next_token) LAUNCH(RDKV_PROF_HEAD, 0.0, launch_argmax(b->logits, d.vocab, S, d.vocab, b->next_token, st));
+    if (b->next_token) LAUNCH(RDKV_PROF_HEAD, 0.0, launch_argmax(b->logits, d.vocab, S, d.vocab, b->next_token, ws.argmax, st));
   }
   return 0;
 }

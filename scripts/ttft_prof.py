@@ -39,3 +39,9 @@ e0.record()
 for _ in range(20): prefill_batch(eng, [req], timed=False, use_graph=True)
 e1.record(); torch.cuda.synchronize()
 print("graph device+host pipelined ms/query", e0.elapsed_time(e1) / 20)
+# one profiled forward for ncu (--profile-from-start off)
+torch.cuda.synchronize()
+torch.cuda.cudart().cudaProfilerStart()
+prefill_batch(eng, [req], timed=False, use_graph=False)
+torch.cuda.synchronize()
+torch.cuda.cudart().cudaProfilerStop()
