@@ -1,10 +1,19 @@
 // C-ABI entry points for the device side of librdkv.
 #include <cuda_runtime.h>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "gemm_tc.cuh"
 
 namespace rdkv {
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("RDKV_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 int num_sms() {
   static int cached[64] = {0};

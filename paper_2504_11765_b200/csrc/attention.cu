@@ -21,6 +21,7 @@
 
 #include "attention.cuh"
 #include "common.cuh"
+#include "pdl.cuh"
 
 namespace rdkv {
 namespace {
@@ -69,6 +70,8 @@ __device__ __forceinline__ uint32_t swz(int row, int chunk) {
 
 template <int DH>
 __global__ void __launch_bounds__(THREADS, DH == 64 ? 2 : 1) attn_prefill_kernel(AttnParams p) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int CH = DH / 8;  // 16-B chunks per row
   constexpr uint32_t TILE = BN * DH * 2;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -262,7 +265,7 @@ int launch_dh(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
   const int G = p.hq / p.hkv;
   const int tok_per_cta = ROWS / G;
   dim3 grid((max_new + tok_per_cta - 1) / tok_per_cta, p.hkv, n_seqs);
-  attn_prefill_kernel<DH><<<grid, THREADS, smem, st>>>(p);
+  CUDA_TRY(launch_k(attn_prefill_kernel<DH>, grid, dim3(THREADS), smem, st, p));
   CUDA_TRY(cudaGetLastError());
   return 0;
 }

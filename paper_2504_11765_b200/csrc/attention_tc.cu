@@ -27,6 +27,7 @@
 
 #include "attention.cuh"
 #include "common.cuh"
+#include "pdl.cuh"
 #include "ptx.cuh"
 
 namespace rdkv {
@@ -138,6 +139,8 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();  // q / KV planes written by the predecessor are visible from here
   const uint32_t tS = tmem;             // S buffers at columns [0,128) and [128,256)
   const uint32_t tO = tmem + 2 * BKV;   // O_tile buffers at 256 and 256 + DH
 
@@ -379,6 +382,8 @@ __global__ void __launch_bounds__(384, 1)
 // Merge the KV-split partials of every (token, head): O = sum_s o_s 2^(m_s-M) / sum_s l_s 2^(m_s-M).
 template <int DH>
 __global__ void __launch_bounds__(256) attn_split_combine_kernel(AttnParams p) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x, head = blockIdx.y * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (head >= p.hq) return;
   float M = -INFINITY;
@@ -429,10 +434,10 @@ int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
     if (k >= 2 && (size_t)k * p.n_tokens * p.hq * (DH * 4 + 8) <= p.split_bytes) q.kv_splits = k;
   }
   dim3 grid(qblocks * q.kv_splits, p.hkv, n_seqs);
-  attn_tc_kernel<DH><<<grid, 384, C::SMEM, st>>>(tk, tv, q);
+  CUDA_TRY(launch_k(attn_tc_kernel<DH>, grid, dim3(384), C::SMEM, st, tk, tv, q));
   CUDA_TRY(cudaGetLastError());
   if (q.kv_splits > 1) {
-    attn_split_combine_kernel<DH><<<dim3(p.n_tokens, (p.hq + 7) / 8), 256, 0, st>>>(q);
+    CUDA_TRY(launch_k(attn_split_combine_kernel<DH>, dim3(p.n_tokens, (p.hq + 7) / 8), dim3(256), 0, st, q));
     CUDA_TRY(cudaGetLastError());
   }
   return 0;

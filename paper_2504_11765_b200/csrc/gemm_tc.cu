@@ -11,6 +11,7 @@
 #include <mutex>
 #include "common.cuh"
 #include "gemm_tc.cuh"
+#include "pdl.cuh"
 
 namespace rdkv {
 
@@ -120,6 +121,8 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();  // predecessor's outputs (activations, residual) are visible from here
 
   if (warp == 0) {
     // ---------------- TMA producer
@@ -289,6 +292,8 @@ __global__ void __launch_bounds__(256, 1)
 template <int EPI, int DH>
 __global__ void __launch_bounds__(256) splitk_finalize_kernel(const float* __restrict__ part, int splits, int M,
                                                               int N, GemmEpi ep) {
+  pdl_trigger();
+  pdl_wait();
   const int row = blockIdx.x;
   const long long slab = (long long)M * N;
   const float* pr = part + (long long)row * N;
@@ -374,6 +379,8 @@ __global__ void __launch_bounds__(256) splitk_finalize_kernel(const float* __res
 __global__ void __launch_bounds__(256) splitk_resid_norm_kernel(const float* __restrict__ part, int splits, int M,
                                                                 int N, GemmEpi ep) {
   constexpr int MAXC = 8;
+  pdl_trigger();
+  pdl_wait();
   const int row = blockIdx.x;
   const long long slab = (long long)M * N;
   const float* pr = part + (long long)row * N;
@@ -438,7 +445,7 @@ int launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int 
   }
   const int units = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * splits;
   const int grid = units < num_sms() ? units : num_sms();
-  kern<<<grid, 256, C::SMEM, stream>>>(ta, tb, M, N, K, splits, ep);
+  CUDA_TRY(launch_k(kern, dim3(grid), dim3(256), C::SMEM, stream, ta, tb, M, N, K, splits, ep));
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -449,7 +456,7 @@ int launch_finalize(const float* part, int splits, int M, int N, const GemmEpi& 
   if (EPI == EPI_QKV) gy = (N / (DH ? DH : 1) + 7) / 8;
   else if (EPI == EPI_SWIGLU) gy = (N / 2 + 1023) / 1024;
   else gy = (N + 1023) / 1024;
-  splitk_finalize_kernel<EPI, DH><<<dim3(M, gy), 256, 0, stream>>>(part, splits, M, N, ep);
+  CUDA_TRY(launch_k(splitk_finalize_kernel<EPI, DH>, dim3(M, gy), dim3(256), 0, stream, part, splits, M, N, ep));
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -553,7 +560,7 @@ int dispatch(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long
       case EPI_RESID:
         if (ep.norm_out) {
           if (N > 8192 || N % 4) return set_error(RDKV_ERR_ARG, "resid+norm finalize: N must be <= 8192, %% 4");
-          splitk_resid_norm_kernel<<<M, 256, 0, stream>>>(part, splits, M, N, ep);
+          CUDA_TRY(launch_k(splitk_resid_norm_kernel, dim3(M), dim3(256), 0, stream, part, splits, M, N, ep));
           CUDA_TRY(cudaGetLastError());
           return 0;
         }

@@ -8,6 +8,7 @@
 
 #include "common.cuh"
 #include "kernels_misc.cuh"
+#include "pdl.cuh"
 
 namespace rdkv {
 namespace {
@@ -28,6 +29,8 @@ template <int SRC_W>
 __global__ void __launch_bounds__(256) kv_unpack_kernel(const UnpackJob* __restrict__ jobs, const int* __restrict__ bt,
                                                         int block_size, __nv_bfloat16* __restrict__ pool, int layers,
                                                         int hkv, int dh, long long slots) {
+  pdl_trigger();
+  pdl_wait();
   const UnpackJob jb = jobs[blockIdx.y];
   const int nblk = (jb.n_tokens + block_size - 1) / block_size;
   const long long nseg = (long long)layers * 2 * hkv * nblk;
@@ -73,6 +76,8 @@ __global__ void __launch_bounds__(256) kv_unpack_kernel(const UnpackJob* __restr
 // ---------------------------------------------------------------- embed
 __global__ void embed_kernel(const int* __restrict__ tok, const __nv_bfloat16* __restrict__ table,
                              __nv_bfloat16* __restrict__ out, int d, int vocab) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   int id = tok[t];
   id = id < 0 ? 0 : (id >= vocab ? vocab - 1 : id);
@@ -87,6 +92,8 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const __nv_bfloat16* __res
                                                       const int* __restrict__ rows, const float* __restrict__ gain,
                                                       __nv_bfloat16* __restrict__ out, long long ldo, int d,
                                                       float eps) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const int src_row = rows ? rows[r] : r;
   const __nv_bfloat16* xr = x + (long long)src_row * ldx;
@@ -144,6 +151,8 @@ __device__ __forceinline__ void argmax_merge(float& best, int& idx, float vb, in
 
 __global__ void __launch_bounds__(256) argmax_chunk_kernel(const float* __restrict__ logits, long long ld, int n,
                                                           float2* __restrict__ part) {
+  pdl_trigger();
+  pdl_wait();
   const int row = blockIdx.x, ch = blockIdx.y;
   const int len = (n + ARGMAX_CH - 1) / ARGMAX_CH;
   const int lo = ch * len, hi = min(n, lo + len);
@@ -170,6 +179,8 @@ __global__ void __launch_bounds__(256) argmax_chunk_kernel(const float* __restri
 }
 
 __global__ void argmax_final_kernel(const float2* __restrict__ part, int* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int row = blockIdx.x, lane = threadIdx.x;
   const float2 p = part[row * ARGMAX_CH + lane];
   float best = p.x;
@@ -193,9 +204,9 @@ int launch_kv_unpack(const UnpackJob* jobs_dev, int n_jobs, int max_tokens, cons
   dim3 grid((unsigned)gx, (unsigned)n_jobs);
   auto* dst = static_cast<__nv_bfloat16*>(pool);
   if (elem_width == 2)
-    kv_unpack_kernel<2><<<grid, 256, 0, st>>>(jobs_dev, bt, block_size, dst, layers, hkv, dh, slots);
+    CUDA_TRY(launch_k(kv_unpack_kernel<2>, grid, dim3(256), 0, st, jobs_dev, bt, block_size, dst, layers, hkv, dh, slots));
   else
-    kv_unpack_kernel<4><<<grid, 256, 0, st>>>(jobs_dev, bt, block_size, dst, layers, hkv, dh, slots);
+    CUDA_TRY(launch_k(kv_unpack_kernel<4>, grid, dim3(256), 0, st, jobs_dev, bt, block_size, dst, layers, hkv, dh, slots));
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -203,7 +214,7 @@ int launch_kv_unpack(const UnpackJob* jobs_dev, int n_jobs, int max_tokens, cons
 int launch_embed(const int* tok, const __nv_bfloat16* table, __nv_bfloat16* out, int n, int d, int vocab,
                  cudaStream_t st) {
   if (n <= 0) return 0;
-  embed_kernel<<<n, 128, 0, st>>>(tok, table, out, d, vocab);
+  CUDA_TRY(launch_k(embed_kernel, dim3(n), dim3(128), 0, st, tok, table, out, d, vocab));
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -212,7 +223,7 @@ int launch_rmsnorm(const __nv_bfloat16* x, long long ldx, const int* rows, const
                    long long ldo, int n_rows, int d, float eps, cudaStream_t st) {
   if (n_rows <= 0) return 0;
   if (d % 8 != 0) return set_error(RDKV_ERR_ARG, "rmsnorm: d must be a multiple of 8");
-  rmsnorm_kernel<<<n_rows, 256, 0, st>>>(x, ldx, rows, gain, out, ldo, d, eps);
+  CUDA_TRY(launch_k(rmsnorm_kernel, dim3(n_rows), dim3(256), 0, st, x, ldx, rows, gain, out, ldo, d, eps));
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -223,9 +234,9 @@ int launch_argmax(const float* logits, long long ld, int rows, int n, int* out, 
   if (rows <= 0) return 0;
   static_assert(ARGMAX_CH == 32, "final stage is one warp");
   auto* part = static_cast<float2*>(scratch);
-  argmax_chunk_kernel<<<dim3(rows, ARGMAX_CH), 256, 0, st>>>(logits, ld, n, part);
+  CUDA_TRY(launch_k(argmax_chunk_kernel, dim3(rows, ARGMAX_CH), dim3(256), 0, st, logits, ld, n, part));
   CUDA_TRY(cudaGetLastError());
-  argmax_final_kernel<<<rows, 32, 0, st>>>(part, out);
+  CUDA_TRY(launch_k(argmax_final_kernel, dim3(rows), dim3(32), 0, st, part, out));
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
