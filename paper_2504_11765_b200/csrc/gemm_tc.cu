@@ -22,7 +22,7 @@ constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
 
 template <int BN>
 struct GemmCfg {
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
   static constexpr uint32_t A_BYTES = BM * BK * 2;
   static constexpr uint32_t B_BYTES = BN * BK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
@@ -286,6 +286,157 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// ---------------------------------------------------------------- small-M swap-AB
+// D^T = W . X^T for M <= 128 tokens: the weights are the 128-row A operand
+// (every weight byte crosses L2->SM once), the NT-row token tile is UMMA N.  Each
+// unit (128 weight rows, K split) writes fp32 partial rows part[split][m][n]
+// (thread = weight row n, so a warp writes 32 consecutive n per token: coalesced);
+// splitk_finalize applies the fused epilogue.
+template <int NT>
+__global__ void __launch_bounds__(256, 1)
+    gemm_swapab_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, int M, int N,
+                       int K, int splits, float* __restrict__ part) {
+  constexpr int STAGES = NT >= 128 ? 6 : 8;
+  constexpr uint32_t W_BYTES = 128 * BK * 2, X_BYTES = NT * BK * 2, STAGE = W_BYTES + X_BYTES;
+  constexpr uint32_t ACC = NT < 32 ? 32 : NT;  // accumulator column stride (tcgen05.ld reads 32 columns)
+  constexpr uint32_t TMEM_COLS = 2 * ACC;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sW = smem;
+  uint8_t* sX = smem + STAGES * W_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w_tiles = (N + 127) / 128;
+  const int units = w_tiles * splits;
+  const int kblocks = K / BK, kb_per = (kblocks + splits - 1) / splits;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmW);
+    tma_prefetch_desc(&tmX);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_act = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int wt = u / splits, sp = u % splits;
+        const int kb0 = sp * kb_per, kb1 = min(kb0 + kb_per, kblocks);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], STAGE);
+          tma_load_2d_nohint(&tmW, &full[stage], sW + stage * W_BYTES, kb * BK, wt * 128);
+          tma_load_2d(&tmX, &full[stage], sX + stage * X_BYTES, kb * BK, 0, pol_act);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(128, NT);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int sp = u % splits;
+        const int kb0 = sp * kb_per, kb1 = min(kb0 + kb_per, kblocks);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * ACC;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ad = sdesc_k_sw128(smem_u32(sW + stage * W_BYTES));
+          const uint64_t bd = sdesc_k_sw128(smem_u32(sX + stage * X_BYTES));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    const int wq = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int wt = u / splits, sp = u % splits;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int n = wt * 128 + wq * 32 + lane;  // weight row == output column
+      const uint32_t taddr = tmem_base + acc * ACC + ((uint32_t)(wq * 32) << 16);
+      float* dst = part + (long long)sp * M * N + n;
+#pragma unroll
+      for (int c = 0; c < (NT + 31) / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(taddr + c * 32, r);
+        tmem_ld_wait();
+        if (n < N) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c * 32 + i < M) dst[(long long)(c * 32 + i) * N] = __uint_as_float(r[i]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+template <int NT>
+int launch_swapab(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K, int splits, float* part,
+                  cudaStream_t stream) {
+  constexpr size_t SMEM = 1024 + (NT >= 128 ? 6 : 8) * ((size_t)128 * BK * 2 + (size_t)NT * BK * 2) + 256;
+  static bool attr_set = false;
+  if (!attr_set) {
+    CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    attr_set = true;
+  }
+  const int units = ((N + 127) / 128) * splits;
+  const int grid = units < num_sms() ? units : num_sms();
+  CUDA_TRY(launch_k(gemm_swapab_kernel<NT>, dim3(grid), dim3(256), SMEM, stream, tw, tx, M, N, K, splits, part));
+  return 0;
+}
+
 // ---------------------------------------------------------------- split-K finalize
 // Sum the split slabs in a fixed order (deterministic) and apply the epilogue.
 // Grid: (rows, column chunks); 4 consecutive columns per thread (float4 loads).
@@ -515,33 +666,73 @@ int pick_splits(int M, int N, int K, int bn) {
   return (kblocks + kb_per - 1) / kb_per;
 }
 
-// Automatic small-M plan: a single 128-row tile whose N tiles cannot fill half
-// the SMs is weight-bandwidth bound; split it into 64-wide N tiles x K splits
-// (about one wave, >= 4 k-blocks per split).  Narrow N tiles keep the fp32
-// partial traffic (splits x M x N x 4 B) well below the weight bytes.
+// Small-M plan: <= 128 tokens make every layer GEMM weight-bandwidth bound.  Run
+// it swap-AB (weights = 128-row A operand, tokens = UMMA N) with enough K splits
+// for about one wave; fp32 partials are reduced by splitk_finalize, which also
+// applies the fused epilogue.
 struct SplitPlan {
-  int bn, splits;
+  int nt, splits;  // token tile (0 = not small-M) and K splits
 };
 SplitPlan pick_split_plan(int M, int N, int K) {
-  const int sms = num_sms(), kblocks = K / BK;
-  if (M > BM || ((N + 127) / 128) * 2 > sms || kblocks < 8) return {0, 1};
-  const int tiles = (N + 63) / 64;
-  int s = sms / tiles;
+  if (M > 128 || K % BK) return {0, 1};
+  const int nt = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : 128;
+  const int sms = num_sms(), kblocks = K / BK, w_tiles = (N + 127) / 128;
+  int s = w_tiles >= sms ? 1 : sms / w_tiles;
   s = s < kblocks / 4 ? s : kblocks / 4;
-  if (s < 2) return {0, 1};
+  if (s < 1) s = 1;
   const int kb_per = (kblocks + s - 1) / s;
-  return {64, (kblocks + kb_per - 1) / kb_per};
+  return {nt, (kblocks + kb_per - 1) / kb_per};
 }
 
 bool gemm_splits(int M, int N, int K, size_t splitk_bytes) {
   const SplitPlan sp = pick_split_plan(M, N, K);
-  return sp.splits > 1 && (size_t)sp.splits * M * N * sizeof(float) <= splitk_bytes;
+  return sp.nt > 0 && (size_t)sp.splits * M * N * sizeof(float) <= splitk_bytes;
 }
 
 size_t splitk_scratch_bytes(int M, int N, int K) {
   const SplitPlan sp = pick_split_plan(M, N, K);
-  return sp.splits > 1 ? (size_t)sp.splits * M * N * sizeof(float) : 0;
+  return sp.nt > 0 ? (size_t)sp.splits * M * N * sizeof(float) : 0;
 }
+
+namespace {
+
+// Sum `splits` fp32 partial slabs and apply the requested epilogue.
+int finalize(int kind, int dh, const float* part, int splits, int M, int N, const GemmEpi& ep, cudaStream_t stream) {
+  switch (kind) {
+    case EPI_STORE: return launch_finalize<EPI_STORE, 0>(part, splits, M, N, ep, stream);
+    case EPI_STORE_F32: return launch_finalize<EPI_STORE_F32, 0>(part, splits, M, N, ep, stream);
+    case EPI_RESID:
+      if (ep.norm_out) {
+        if (N > 8192 || N % 4) return set_error(RDKV_ERR_ARG, "resid+norm finalize: N must be <= 8192, %% 4");
+        CUDA_TRY(launch_k(splitk_resid_norm_kernel, dim3(M), dim3(256), 0, stream, part, splits, M, N, ep));
+        return 0;
+      }
+      return launch_finalize<EPI_RESID, 0>(part, splits, M, N, ep, stream);
+    case EPI_SWIGLU: return launch_finalize<EPI_SWIGLU, 0>(part, splits, M, N, ep, stream);
+    case EPI_QKV:
+      if (dh == 64) return launch_finalize<EPI_QKV, 64>(part, splits, M, N, ep, stream);
+      if (dh == 128) return launch_finalize<EPI_QKV, 128>(part, splits, M, N, ep, stream);
+      return set_error(RDKV_ERR_ARG, "qkv: head_dim %d unsupported (64 or 128)", dh);
+    default: return set_error(RDKV_ERR_ARG, "gemm: unknown epilogue %d", kind);
+  }
+}
+
+int launch_small_m(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long long ldb, int M, int N, int K,
+                   int kind, int dh, const GemmEpi& ep, cudaStream_t stream, SplitPlan sp) {
+  CUtensorMap tw, tx;
+  RDKV_TRY(make_tmap(&tw, B, N, K, ldb, 128));
+  RDKV_TRY(make_tmap(&tx, A, M, K, lda, sp.nt));
+  auto* part = static_cast<float*>(ep.splitk_ws);
+  switch (sp.nt) {
+    case 16: RDKV_TRY(launch_swapab<16>(tw, tx, M, N, K, sp.splits, part, stream)); break;
+    case 32: RDKV_TRY(launch_swapab<32>(tw, tx, M, N, K, sp.splits, part, stream)); break;
+    case 64: RDKV_TRY(launch_swapab<64>(tw, tx, M, N, K, sp.splits, part, stream)); break;
+    default: RDKV_TRY(launch_swapab<128>(tw, tx, M, N, K, sp.splits, part, stream)); break;
+  }
+  return finalize(kind, dh, part, sp.splits, M, N, ep, stream);
+}
+
+}  // namespace
 
 template <int BN>
 int dispatch(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long long ldb, int M, int N, int K,
@@ -553,29 +744,8 @@ int dispatch(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long
     GemmEpi pe = ep;
     pe.out = ep.splitk_ws;
     RDKV_TRY((launch_impl<BN, EPI_PARTIAL, 0>(ta, tb, M, N, K, splits, pe, stream)));
-    const float* part = static_cast<const float*>(ep.splitk_ws);
-    switch (kind) {
-      case EPI_STORE: return launch_finalize<EPI_STORE, 0>(part, splits, M, N, ep, stream);
-      case EPI_STORE_F32: return launch_finalize<EPI_STORE_F32, 0>(part, splits, M, N, ep, stream);
-      case EPI_RESID:
-        if (ep.norm_out) {
-          if (N > 8192 || N % 4) return set_error(RDKV_ERR_ARG, "resid+norm finalize: N must be <= 8192, %% 4");
-          CUDA_TRY(launch_k(splitk_resid_norm_kernel, dim3(M), dim3(256), 0, stream, part, splits, M, N, ep));
-          CUDA_TRY(cudaGetLastError());
-          return 0;
-        }
-        return launch_finalize<EPI_RESID, 0>(part, splits, M, N, ep, stream);
-      case EPI_SWIGLU: return launch_finalize<EPI_SWIGLU, 0>(part, splits, M, N, ep, stream);
-      case EPI_QKV:
-        if (dh == 64) return launch_finalize<EPI_QKV, 64>(part, splits, M, N, ep, stream);
-        if (dh == 128) return launch_finalize<EPI_QKV, 128>(part, splits, M, N, ep, stream);
-        return set_error(RDKV_ERR_ARG, "qkv: head_dim %d unsupported (64 or 128)", dh);
-      default: return set_error(RDKV_ERR_ARG, "gemm: unknown epilogue %d", kind);
-    }
+    return finalize(kind, dh, static_cast<const float*>(ep.splitk_ws), splits, M, N, ep, stream);
   }
-  if constexpr (BN == 64) {
-    return set_error(RDKV_ERR_ARG, "gemm: 64-wide tiles are split-K only");
-  } else {
   switch (kind) {
     case EPI_STORE: return launch_impl<BN, EPI_STORE, 0>(ta, tb, M, N, K, 1, ep, stream);
     case EPI_STORE_F32: return launch_impl<BN, EPI_STORE_F32, 0>(ta, tb, M, N, K, 1, ep, stream);
@@ -586,7 +756,6 @@ int dispatch(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long
       if (dh == 128) return launch_impl<BN, EPI_QKV, 128>(ta, tb, M, N, K, 1, ep, stream);
       return set_error(RDKV_ERR_ARG, "qkv: head_dim %d unsupported (64 or 128)", dh);
     default: return set_error(RDKV_ERR_ARG, "gemm: unknown epilogue %d", kind);
-  }
   }
 }
 
@@ -604,18 +773,15 @@ int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, l
   if (ep.splitk_ws) {
     if (bn == 0) {
       const SplitPlan sp = pick_split_plan(M, N, K);
-      if (sp.splits > 1 && (size_t)sp.splits * M * N * sizeof(float) <= ep.splitk_bytes) {
-        bn = sp.bn;
-        splits = sp.splits;
-      }
-    } else {  // explicit tile width (tests): split whenever it would help
+      if (sp.nt > 0 && (size_t)sp.splits * M * N * sizeof(float) <= ep.splitk_bytes)
+        return launch_small_m(A, lda, B, ldb, M, N, K, kind, dh, ep, stream, sp);
+    } else {  // explicit tile width (tests): split-K with that tile when it would help
       splits = pick_splits(M, N, K, bn);
       if ((size_t)splits * M * N * sizeof(float) > ep.splitk_bytes) splits = 1;
     }
   }
   if (bn == 0) bn = pick_bn(M, N);
   if (kind == EPI_SWIGLU && N % bn != 0) bn = 128;
-  if (bn == 64) return dispatch<64>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream, splits);
   if (bn == 128) return dispatch<128>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream, splits);
   return dispatch<256>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream, splits);
 }
