@@ -147,13 +147,14 @@ typedef struct rdkv_unpack_job {
 /* Unpack n_jobs blob payloads into the paged KV pool
  *   pool: [L][2][Hkv][pool_slots][dh] bf16, token t of job j at slot
  *         block_table[first_block + t / block_size] * block_size + t % block_size.
- * Converts fp32 payloads (elem_width 4) to bf16.  HBM-bound: 2 x payload bytes
- * per call.  Replaces the payload materialisation of codec.decode
+ * Converts fp32 payloads (elem_width 4) to bf16.  Only layers [layer_begin,
+ * layer_end) are moved, so a caller can stream layer by layer on a side stream
+ * while the forward consumes earlier layers.  HBM-bound: 2 x payload bytes.  Replaces the payload materialisation of codec.decode
  * (codec.py:292) and the modeled load_time (costs.py:102-108). */
 RDKV_API int rdkv_kv_unpack(const rdkv_unpack_job* jobs_dev, int n_jobs, int max_tokens,
                             const int32_t* block_table_dev, int block_size, void* pool_base,
                             int layers, int kv_heads, int head_dim, int64_t pool_slots,
-                            int elem_width, void* stream);
+                            int elem_width, int layer_begin, int layer_end, void* stream);
 
 /* ------------------------------------------ model: document / query prefill */
 
@@ -216,6 +217,8 @@ typedef struct rdkv_batch {
   int32_t* next_token;         /* dev [S] argmax (first token), may be NULL          */
   int32_t max_ctx;             /* max over sequences of n_cached + n_new (0: unknown;
                                   enables split-KV attention for small batches)      */
+  void* const* layer_ready;     /* optional [layers] cudaEvent_t: layer l's attention
+                                  waits for event l (layer-wise KV streaming)        */
 } rdkv_batch;
 
 /* Device workspace needed by rdkv_forward for n_tokens / n_seqs. */

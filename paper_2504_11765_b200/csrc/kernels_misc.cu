@@ -27,8 +27,8 @@ __device__ __forceinline__ uint4 ld_stream(const void* p) {
 // 16-byte loads, UNROLL of them in flight per lane.
 template <int SRC_W>
 __global__ void __launch_bounds__(256) kv_unpack_kernel(const UnpackJob* __restrict__ jobs, const int* __restrict__ bt,
-                                                        int block_size, __nv_bfloat16* __restrict__ pool, int layers,
-                                                        int hkv, int dh, long long slots) {
+                                                        int block_size, __nv_bfloat16* __restrict__ pool, int layer0,
+                                                        int layers, int hkv, int dh, long long slots) {
   pdl_trigger();
   pdl_wait();
   const UnpackJob jb = jobs[blockIdx.y];
@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(256) kv_unpack_kernel(const UnpackJob* __restr
   constexpr int UNROLL = 4;
   for (long long seg = (long long)blockIdx.x * 8 + warp; seg < nseg; seg += (long long)gridDim.x * 8) {
     const int b = (int)(seg % nblk);
-    const long long plane = seg / nblk;  // (l*2 + kv)*hkv + h
+    const long long plane = (long long)layer0 * 2 * hkv + seg / nblk;  // (l*2 + kv)*hkv + h
     const int t0 = b * block_size;
     const int ntok = min(block_size, jb.n_tokens - t0);
     const long long n_el = (long long)ntok * dh;
@@ -193,8 +193,10 @@ __global__ void argmax_final_kernel(const float2* __restrict__ part, int* __rest
 }  // namespace
 
 int launch_kv_unpack(const UnpackJob* jobs_dev, int n_jobs, int max_tokens, const int* bt, int block_size,
-                     void* pool, int layers, int hkv, int dh, long long slots, int elem_width, cudaStream_t st) {
-  if (n_jobs <= 0 || max_tokens <= 0) return 0;
+                     void* pool, int layer_begin, int layer_end, int hkv, int dh, long long slots, int elem_width,
+                     cudaStream_t st) {
+  const int layers = layer_end - layer_begin;
+  if (n_jobs <= 0 || max_tokens <= 0 || layers <= 0) return 0;
   if (dh % 8 != 0) return set_error(RDKV_ERR_ARG, "unpack: head_dim must be a multiple of 8");
   if (elem_width != 2 && elem_width != 4) return set_error(RDKV_ERR_ARG, "unpack: elem_width must be 2 or 4");
   const long long segs = (long long)layers * 2 * hkv * ((max_tokens + block_size - 1) / block_size);
@@ -204,9 +206,9 @@ int launch_kv_unpack(const UnpackJob* jobs_dev, int n_jobs, int max_tokens, cons
   dim3 grid((unsigned)gx, (unsigned)n_jobs);
   auto* dst = static_cast<__nv_bfloat16*>(pool);
   if (elem_width == 2)
-    CUDA_TRY(launch_k(kv_unpack_kernel<2>, grid, dim3(256), 0, st, jobs_dev, bt, block_size, dst, layers, hkv, dh, slots));
+    CUDA_TRY(launch_k(kv_unpack_kernel<2>, grid, dim3(256), 0, st, jobs_dev, bt, block_size, dst, layer_begin, layers, hkv, dh, slots));
   else
-    CUDA_TRY(launch_k(kv_unpack_kernel<4>, grid, dim3(256), 0, st, jobs_dev, bt, block_size, dst, layers, hkv, dh, slots));
+    CUDA_TRY(launch_k(kv_unpack_kernel<4>, grid, dim3(256), 0, st, jobs_dev, bt, block_size, dst, layer_begin, layers, hkv, dh, slots));
   CUDA_TRY(cudaGetLastError());
   return 0;
 }

@@ -269,6 +269,8 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
       ap.split_ml = reinterpret_cast<float2*>(static_cast<uint8_t*>(ws.attn_split) + o_bytes);
       ap.split_bytes = ws.attn_split_bytes;
     }
+    if (b->layer_ready && b->layer_ready[l])  // layer-wise streaming: this layer's cached KV has landed
+      CUDA_TRY(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(b->layer_ready[l]), 0));
     if (use_tc_attn && attention_tc_supported(ap, dh))
       LAUNCH(RDKV_PROF_ATTN, 0.0, launch_attention_tc(ap, dh, S, b->max_new, st));
     else
@@ -345,10 +347,12 @@ int rdkv_profile_collect(rdkv_model* m, double* ms, int64_t* launches, double* f
 
 int rdkv_kv_unpack(const rdkv_unpack_job* jobs_dev, int n_jobs, int max_tokens, const int32_t* block_table_dev,
                    int block_size, void* pool_base, int layers, int kv_heads, int head_dim, int64_t pool_slots,
-                   int elem_width, void* stream) {
+                   int elem_width, int layer_begin, int layer_end, void* stream) {
   if (block_size <= 0 || !pool_base || !jobs_dev) return set_error(RDKV_ERR_ARG, "kv_unpack: bad arguments");
-  return launch_kv_unpack(jobs_dev, n_jobs, max_tokens, block_table_dev, block_size, pool_base, layers, kv_heads,
-                          head_dim, pool_slots, elem_width, static_cast<cudaStream_t>(stream));
+  if (layer_begin < 0 || layer_end > layers || layer_begin > layer_end)
+    return set_error(RDKV_ERR_ARG, "kv_unpack: bad layer range [%d, %d) of %d", layer_begin, layer_end, layers);
+  return launch_kv_unpack(jobs_dev, n_jobs, max_tokens, block_table_dev, block_size, pool_base, layer_begin,
+                          layer_end, kv_heads, head_dim, pool_slots, elem_width, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

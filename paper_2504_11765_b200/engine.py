@@ -47,7 +47,8 @@ class RdkvBatch(C.Structure):
                 ("tokens", C.c_void_p), ("pos", C.c_void_p), ("slot", C.c_void_p), ("seq_start", C.c_void_p),
                 ("seq_new", C.c_void_p), ("seq_cached", C.c_void_p), ("block_table", C.c_void_p),
                 ("last_row", C.c_void_p), ("kv_base", C.c_void_p), ("kv_slots", C.c_int64),
-                ("logits", C.c_void_p), ("next_token", C.c_void_p), ("max_ctx", C.c_int32)]
+                ("logits", C.c_void_p), ("next_token", C.c_void_p), ("max_ctx", C.c_int32),
+                ("layer_ready", C.c_void_p)]
 
 
 class RdkvUnpackJob(C.Structure):
@@ -63,7 +64,7 @@ _N_SIG = {
     "rdkv_workspace_bytes": (C.c_size_t, [C.c_void_p, C.c_int, C.c_int]),
     "rdkv_forward": (C.c_int, [C.c_void_p, C.POINTER(RdkvBatch), C.c_void_p, C.c_size_t, C.c_void_p]),
     "rdkv_kv_unpack": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int,
-                                 C.c_int, C.c_int64, C.c_int, C.c_void_p]),
+                                 C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_void_p]),
     "rdkv_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
     "rdkv_profile_collect": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                        C.POINTER(C.c_double)]),
@@ -201,7 +202,7 @@ class BatchPlan:
         # max_ctx fixes the split-KV choice baked into a captured graph
         return (self.n_seqs, self.n_tokens, self.max_new, self.bt_stride, self.block_size, self.max_ctx)
 
-    def struct(self, kv_base: int, kv_slots: int, logits=None, next_token=None) -> RdkvBatch:
+    def struct(self, kv_base: int, kv_slots: int, logits=None, next_token=None, layer_ready=None) -> RdkvBatch:
         p = self.ptr
         return RdkvBatch(
             n_seqs=self.n_seqs, n_tokens=self.n_tokens, max_new=self.max_new, block_size=self.block_size,
@@ -210,7 +211,8 @@ class BatchPlan:
             seq_cached=p["seq_cached"], block_table=p["block_table"], last_row=p["last_row"],
             kv_base=kv_base, kv_slots=kv_slots,
             logits=logits.data_ptr() if logits is not None else None,
-            next_token=next_token.data_ptr() if next_token is not None else None, max_ctx=self.max_ctx)
+            next_token=next_token.data_ptr() if next_token is not None else None, max_ctx=self.max_ctx,
+            layer_ready=C.cast(layer_ready, C.c_void_p).value if layer_ready is not None else None)
 
 
 # ----------------------------------------------------------------- the model handle
@@ -261,32 +263,64 @@ class DeviceModel:
         return {k: {"ms": ms[i], "launches": int(n[i]), "flops": fl[i]} for i, k in enumerate(PROF_CLASSES)}
 
     def forward(self, plan: BatchPlan, kv_base: int, kv_slots: int, logits=None, next_token=None,
-                stream: torch.cuda.Stream | None = None) -> None:
+                stream: torch.cuda.Stream | None = None, layer_ready=None) -> None:
         ws = self.workspace(plan.n_tokens, plan.n_seqs)
-        b = plan.struct(kv_base, kv_slots, logits, next_token)
+        b = plan.struct(kv_base, kv_slots, logits, next_token, layer_ready)
         _lib.check(_L().rdkv_forward(self._h, C.byref(b), ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
 
 
 def kv_unpack(pool: KvPool, jobs: Sequence[tuple[torch.Tensor, int, int]], block_table: torch.Tensor,
-              elem_width: int = 2, stream: torch.cuda.Stream | None = None) -> None:
+              elem_width: int = 2, stream: torch.cuda.Stream | None = None, layers: tuple[int, int] | None = None,
+              jobs_dev: torch.Tensor | None = None) -> None:
     """K3: unpack device-resident blob payloads into the pool.
 
     ``jobs`` = (payload device tensor, n_tokens, first_block index into the flat
     ``block_table`` int32 device tensor)."""
     if not jobs:
         return
-    arr = np.zeros(len(jobs), dtype=_UNPACK_DTYPE)
-    for i, (src, n, fb) in enumerate(jobs):
-        arr[i] = (src.data_ptr(), n, fb, 0)
-    host = torch.from_numpy(arr.view(np.uint8).copy())
-    if torch.cuda.is_available():
-        host = host.pin_memory()
-    dev = host.to(pool.data.device, non_blocking=True)
+    if jobs_dev is None:
+        jobs_dev = pack_unpack_jobs(jobs).to(pool.data.device, non_blocking=True)
     s = pool.spec
-    _lib.check(_L().rdkv_kv_unpack(dev.data_ptr(), len(jobs), max(n for _, n, _ in jobs), block_table.data_ptr(),
+    l0, l1 = layers if layers is not None else (0, s.layers)
+    _lib.check(_L().rdkv_kv_unpack(jobs_dev.data_ptr(), len(jobs), max(n for _, n, _ in jobs), block_table.data_ptr(),
                                    pool.block_size, pool.data.data_ptr(), s.layers, s.kv_heads, s.head_dim,
-                                   pool.slots, elem_width, _stream_ptr(stream)))
-    pool._last_jobs = dev  # keep alive until the stream consumes it
+                                   pool.slots, elem_width, l0, l1, _stream_ptr(stream)))
+    pool._last_jobs = jobs_dev  # keep alive until the stream consumes it
+
+
+class LayerStreamer:
+    """Layer-wise KV streaming: layer l's unpack runs on a side stream and
+    records event l; the forward waits on event l only before layer l's
+    attention, so the HBM-bound unpack overlaps the compute-bound GEMMs of the
+    layers before it."""
+
+    def __init__(self, engine: "Engine") -> None:
+        L = engine.spec.layers
+        self.eng = engine
+        self.stream = torch.cuda.Stream(device=engine.device)
+        self.events = [torch.cuda.Event() for _ in range(L)]
+        self.handles = (C.c_void_p * L)()
+
+    def launch(self, pool: KvPool, jobs, block_table: torch.Tensor, jobs_dev: torch.Tensor, main: torch.cuda.Stream,
+               first_event=None, last_event=None):
+        """Enqueue the per-layer unpacks; returns the event-handle array for rdkv_forward."""
+        self.stream.wait_stream(main)
+        # buffers allocated on `main` but read here must not be recycled early
+        jobs_dev.record_stream(self.stream)
+        block_table.record_stream(self.stream)
+        for src, _, _ in jobs:
+            src.record_stream(self.stream)
+        with torch.cuda.stream(self.stream):
+            if first_event is not None:
+                first_event.record(self.stream)
+            for l, ev in enumerate(self.events):
+                kv_unpack(pool, jobs, block_table, stream=self.stream, layers=(l, l + 1), jobs_dev=jobs_dev)
+                ev.record(self.stream)
+            if last_event is not None:
+                last_event.record(self.stream)
+        for l, ev in enumerate(self.events):
+            self.handles[l] = ev.cuda_event
+        return self.handles
 
 
 def pack_unpack_jobs(jobs: Sequence[tuple[torch.Tensor, int, int]]) -> torch.Tensor:
@@ -353,14 +387,15 @@ class GraphRunner:
         max_tok = max((n for _, n, _ in jobs), default=0)
         bt_ptr = plan.ptr["block_table"]
 
+        bt_view = plan.meta[(bt_ptr - plan.meta.data_ptr()) // 4:]
+
         def body():
-            st = torch.cuda.current_stream().cuda_stream
+            main = torch.cuda.current_stream()
+            handles = None
             if n_jobs:
-                _lib.check(_L().rdkv_kv_unpack(e.jobs.data_ptr(), n_jobs, max_tok, bt_ptr, pool.block_size,
-                                               pool.data.data_ptr(), s.layers, s.kv_heads, s.head_dim, pool.slots,
-                                               2, st))
-            b = plan.struct(pool.data.data_ptr(), pool.slots, e.logits, e.nxt)
-            _lib.check(_L().rdkv_forward(eng.model._h, C.byref(b), e.ws.data_ptr(), e.ws.numel(), st))
+                handles = eng.streamer.launch(pool, jobs, bt_view, e.jobs, main)
+            b = plan.struct(pool.data.data_ptr(), pool.slots, e.logits, e.nxt, handles)
+            _lib.check(_L().rdkv_forward(eng.model._h, C.byref(b), e.ws.data_ptr(), e.ws.numel(), main.cuda_stream))
 
         body()  # eager warm-up (first launches set kernel attributes) and this call's result
         torch.cuda.current_stream().synchronize()
@@ -436,6 +471,7 @@ class Engine:
         self.copy_stream = torch.cuda.Stream(device=self.device)
         self.device_cache = DeviceKvCache(device_cache_bytes)
         self.graphs = GraphRunner(self)
+        self.streamer = LayerStreamer(self)
 
     def stage(self, payload: torch.Tensor, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
         """Async H2D copy of a pinned host payload; returns the device bf16 view."""

@@ -23,7 +23,7 @@ import numpy as np
 import torch
 
 from .costs import TtftBreakdown
-from .engine import BatchPlan, Engine, SeqPlan, _bt_view, kv_unpack
+from .engine import BatchPlan, Engine, SeqPlan, _bt_view, kv_unpack, pack_unpack_jobs
 from .store import KvKey, LookupResult, Outcome
 
 
@@ -44,7 +44,8 @@ class PrefillResult:
 
 
 def prefill_batch(engine: Engine, requests: Sequence[PrefillRequest], timed: bool = True,
-                  unpack_events: list | None = None, use_graph: bool = True) -> PrefillResult:
+                  unpack_events: list | None = None, use_graph: bool = True,
+                  stream_layers: bool = True) -> PrefillResult:
     """Serve a batch of queries on one engine; kv_load / prefill are the
     device-measured durations of the whole batch's load and prefill phases.
     ``unpack_events`` collects (start, end) CUDA events around the K3 launch.
@@ -85,7 +86,16 @@ def prefill_batch(engine: Engine, requests: Sequence[PrefillRequest], timed: boo
             logits, nxt = graphed
             kv_load = prefill = 0.0
         else:
-            if ujobs:
+            handles = None
+            if ujobs and stream_layers and not timed:
+                # layer-wise streaming: per-layer unpacks on a side stream overlap the forward
+                ua = ub = None
+                if unpack_events is not None:
+                    ua, ub = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    unpack_events.append((ua, ub))
+                jobs_dev = pack_unpack_jobs(ujobs).to(engine.device, non_blocking=True)
+                handles = engine.streamer.launch(pool, ujobs, _bt_view(plan), jobs_dev, main, ua, ub)
+            elif ujobs:
                 if unpack_events is not None:
                     ua, ub = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     ua.record(main)
@@ -98,7 +108,8 @@ def prefill_batch(engine: Engine, requests: Sequence[PrefillRequest], timed: boo
             S = len(requests)
             logits = torch.empty(S, engine.spec.vocab, dtype=torch.float32, device=engine.device)
             nxt = torch.empty(S, dtype=torch.int32, device=engine.device)
-            engine.model.forward(plan, pool.data.data_ptr(), pool.slots, logits, nxt, stream=main)
+            engine.model.forward(plan, pool.data.data_ptr(), pool.slots, logits, nxt, stream=main,
+                                 layer_ready=handles)
             if timed:
                 ev[2].record(main)
                 ev[2].synchronize()

@@ -22,8 +22,8 @@ def test_measured_policy_run(tmp_path):
     svc = SharedCacheService(KvStore(tmp_path, memory_capacity_bytes=0))
     devs = (DeviceProfile("gpu0", DeviceKind.INFERENCE_GPU, 1.0), DeviceProfile("gen", DeviceKind.GENERATOR_GPU, 1.0))
     cfg = SimConfig(configuration=Configuration.SHARED_GPU_N, devices=devs,
-                    cost=CostParams(model=spec.profile(), network_delay=0.0), arrival=ArrivalSpec(rate=2000.0),
-                    k=3, tries=2, seed=1, threshold=0.0005, memory_capacity_bytes=0)
+                    cost=CostParams(model=spec.profile(), network_delay=0.0), arrival=ArrivalSpec(rate=1.0e6),
+                    k=3, tries=2, seed=1, threshold=0.0, memory_capacity_bytes=0)
     items = zipf_stream(30, 1.0, 40, seed=3, k=3, q_tokens=16, doc_tokens=64)
     ex = MeasuredExecutor(eng, svc)
     report, records = run(cfg, items, ex)
