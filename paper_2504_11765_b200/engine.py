@@ -289,35 +289,55 @@ def kv_unpack(pool: KvPool, jobs: Sequence[tuple[torch.Tensor, int, int]], block
 
 
 class LayerStreamer:
-    """Layer-wise KV streaming: layer l's unpack runs on a side stream and
-    records event l; the forward waits on event l only before layer l's
-    attention, so the HBM-bound unpack overlaps the compute-bound GEMMs of the
-    layers before it."""
+    """Layer-wise KV streaming.
+
+    The payload layout puts the layer outermost, so layer l of every cached
+    blob is one contiguous slice.  Per layer: (1) the host-tier slices are
+    copied H2D on a copy stream, (2) K3 unpacks that layer on an unpack stream
+    once its copy has landed and records event l, (3) the forward waits on
+    event l only before layer l's attention.  PCIe transfer, the HBM-bound
+    unpack and the compute-bound GEMMs of earlier layers all overlap."""
 
     def __init__(self, engine: "Engine") -> None:
         L = engine.spec.layers
         self.eng = engine
-        self.stream = torch.cuda.Stream(device=engine.device)
+        self.stream = torch.cuda.Stream(device=engine.device)       # unpack
+        self.h2d = torch.cuda.Stream(device=engine.device)          # host -> HBM copies
         self.events = [torch.cuda.Event() for _ in range(L)]
+        self.copied = [torch.cuda.Event() for _ in range(L)]
         self.handles = (C.c_void_p * L)()
 
     def launch(self, pool: KvPool, jobs, block_table: torch.Tensor, jobs_dev: torch.Tensor, main: torch.cuda.Stream,
-               first_event=None, last_event=None):
-        """Enqueue the per-layer unpacks; returns the event-handle array for rdkv_forward."""
+               first_event=None, last_event=None, h2d: Sequence[tuple[torch.Tensor, torch.Tensor]] = ()):
+        """Enqueue per-layer [H2D ->] unpack; returns the event-handle array for rdkv_forward.
+        ``h2d`` = (pinned host payload, device staging buffer) pairs still to be copied."""
+        L = len(self.events)
         self.stream.wait_stream(main)
         # buffers allocated on `main` but read here must not be recycled early
         jobs_dev.record_stream(self.stream)
         block_table.record_stream(self.stream)
         for src, _, _ in jobs:
             src.record_stream(self.stream)
-        with torch.cuda.stream(self.stream):
-            if first_event is not None:
-                first_event.record(self.stream)
-            for l, ev in enumerate(self.events):
+        if h2d:
+            self.h2d.wait_stream(main)
+            for _, dev in h2d:
+                dev.record_stream(self.h2d)
+        for l in range(L):
+            if h2d:
+                with torch.cuda.stream(self.h2d):
+                    for host, dev in h2d:
+                        per = host.numel() // L
+                        dev[l * per:(l + 1) * per].copy_(host[l * per:(l + 1) * per], non_blocking=True)
+                    self.copied[l].record(self.h2d)
+            with torch.cuda.stream(self.stream):
+                if l == 0 and first_event is not None:
+                    first_event.record(self.stream)
+                if h2d:
+                    self.stream.wait_event(self.copied[l])
                 kv_unpack(pool, jobs, block_table, stream=self.stream, layers=(l, l + 1), jobs_dev=jobs_dev)
-                ev.record(self.stream)
-            if last_event is not None:
-                last_event.record(self.stream)
+                self.events[l].record(self.stream)
+        if last_event is not None:
+            last_event.record(self.stream)
         for l, ev in enumerate(self.events):
             self.handles[l] = ev.cuda_event
         return self.handles

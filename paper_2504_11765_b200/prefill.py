@@ -56,7 +56,7 @@ def prefill_batch(engine: Engine, requests: Sequence[PrefillRequest], timed: boo
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if timed else None
     if timed:
         ev[0].record(main)
-    seqs, owned, jobs, staged = [], [], [], []
+    seqs, owned, jobs, staged, pending_h2d = [], [], [], [], []
     # staging buffers are allocated on `main`; the copy stream must not write
     # them before main's earlier users of that memory are done
     engine.copy_stream.wait_stream(main)
@@ -72,7 +72,12 @@ def prefill_batch(engine: Engine, requests: Sequence[PrefillRequest], timed: boo
             if hit:
                 dev = engine.device_cache.get(r.key) if r.key is not None else None
                 if dev is None:
-                    dev = engine.stage(r.lookup.blob.payload_tensor(), stream=engine.copy_stream)
+                    host = r.lookup.blob.payload_tensor()
+                    if stream_layers and not timed:  # copied layer by layer by the streamer
+                        dev = torch.empty(host.numel(), dtype=torch.uint8, device=engine.device).view(torch.bfloat16)
+                        pending_h2d.append((host, dev.view(torch.uint8)))
+                    else:
+                        dev = engine.stage(host, stream=engine.copy_stream)
                     staged.append(dev)
                 jobs.append((dev, n_cached, i))
         plan = BatchPlan(seqs, pool.block_size, engine.device)
@@ -80,7 +85,7 @@ def prefill_batch(engine: Engine, requests: Sequence[PrefillRequest], timed: boo
             main.wait_stream(engine.copy_stream)
         ujobs = [(d, n, i * plan.bt_stride) for d, n, i in jobs]
         graphed = None
-        if use_graph and not timed and unpack_events is None:
+        if use_graph and not timed and unpack_events is None and not pending_h2d:
             graphed = engine.graphs.run(plan, ujobs)  # [K3 unpack ->] forward as one CUDA-graph replay
         if graphed is not None:
             logits, nxt = graphed
@@ -94,7 +99,7 @@ def prefill_batch(engine: Engine, requests: Sequence[PrefillRequest], timed: boo
                     ua, ub = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     unpack_events.append((ua, ub))
                 jobs_dev = pack_unpack_jobs(ujobs).to(engine.device, non_blocking=True)
-                handles = engine.streamer.launch(pool, ujobs, _bt_view(plan), jobs_dev, main, ua, ub)
+                handles = engine.streamer.launch(pool, ujobs, _bt_view(plan), jobs_dev, main, ua, ub, h2d=pending_h2d)
             elif ujobs:
                 if unpack_events is not None:
                     ua, ub = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
