@@ -8,6 +8,7 @@
 // bit deterministic, no atomics) and applies the same fused epilogue.
 #include <cudaTypedefs.h>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include "common.cuh"
 #include "gemm_tc.cuh"
@@ -30,7 +31,7 @@ struct GemmCfg {
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
 };
 
-__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+__device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 
 // Store 32 consecutive bf16 values (packed in 16 words) with 16-byte stores.
 __device__ __forceinline__ void st_bf16x32(__nv_bfloat16* dst, const uint32_t (&w)[16]) {
@@ -66,6 +67,95 @@ __device__ __forceinline__ void qkv_head_out(float (&v)[DH], int g, int row, int
 #pragma unroll
     for (int i = 0; i < 16; ++i) w[i] = pack_bf16(v[c * 32 + 2 * i], v[c * 32 + 2 * i + 1]);
     st_bf16x32(dst + c * 32, w);
+  }
+}
+
+// One accumulator tile -> fused epilogue -> global.  `row` is this thread's output row
+// (its TMEM lane), `taddr` the tile's TMEM address for this warp's lane quadrant.
+template <int BN, int EPI, int DH>
+__device__ __forceinline__ void epilogue_rows(uint32_t taddr, int row, int nb, int sp, int M, int N,
+                                              const GemmEpi& ep) {
+  const bool row_ok = row < M;
+
+  if constexpr (EPI == EPI_STORE || EPI == EPI_STORE_F32 || EPI == EPI_RESID || EPI == EPI_PARTIAL) {
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      uint32_t r[32];
+      tmem_ld32(taddr + c * 32, r);
+      tmem_ld_wait();
+      const int col = nb * BN + c * 32;
+      if (row_ok && col < N) {
+        if constexpr (EPI == EPI_STORE_F32 || EPI == EPI_PARTIAL) {
+          float* base = static_cast<float*>(ep.out);
+          if constexpr (EPI == EPI_PARTIAL) base += (long long)sp * M * N;  // this split's slab
+          float4* dst = reinterpret_cast<float4*>(base + (long long)row * (EPI == EPI_PARTIAL ? N : ep.ldo) + col);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            dst[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                                 __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+        } else {
+          uint32_t w[16];
+          if constexpr (EPI == EPI_RESID) {
+            const uint4* src = reinterpret_cast<const uint4*>(ep.resid + (long long)row * ep.ldr + col);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const uint4 q = src[i];
+              const uint32_t uu[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float2 f = unpack_bf16(uu[j]);
+                const int e = 8 * i + 2 * j;
+                w[4 * i + j] = pack_bf16(f.x + __uint_as_float(r[e]), f.y + __uint_as_float(r[e + 1]));
+              }
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) w[i] = pack_bf16(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+          }
+          st_bf16x32(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + col, w);
+        }
+      }
+    }
+  } else if constexpr (EPI == EPI_SWIGLU) {
+    // weights interleaved in 64-row blocks: tile column block 2i = gate, 2i+1 = up
+#pragma unroll 1
+    for (int c = 0; c < BN / 64; ++c) {
+      const int pb = c >> 1, half = c & 1;
+      uint32_t g[32], v[32];
+      tmem_ld32(taddr + pb * 128 + half * 32, g);
+      tmem_ld32(taddr + pb * 128 + 64 + half * 32, v);
+      tmem_ld_wait();
+      const int col = nb * (BN / 2) + pb * 64 + half * 32;  // output column
+      if (row_ok && col < N / 2) {
+        uint32_t w[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float a0 = silu(__uint_as_float(g[2 * i])) * __uint_as_float(v[2 * i]);
+          const float a1 = silu(__uint_as_float(g[2 * i + 1])) * __uint_as_float(v[2 * i + 1]);
+          w[i] = pack_bf16(a0, a1);
+        }
+        st_bf16x32(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + col, w);
+      }
+    }
+  } else if constexpr (EPI == EPI_QKV) {
+    static_assert(BN % DH == 0, "tile must hold whole heads");
+    const int p = row_ok ? ep.pos[row] : 0;
+    const int sl = row_ok ? ep.slot[row] : 0;
+#pragma unroll 1
+    for (int hh = 0; hh < BN / DH; ++hh) {
+      float v[DH];
+#pragma unroll
+      for (int c = 0; c < DH / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(taddr + hh * DH + c * 32, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[c * 32 + i] = __uint_as_float(r[i]);
+      }
+      const int g = (nb * BN + hh * DH) / DH;  // global head index in [q | k | v]
+      if (!row_ok || g >= ep.hq + 2 * ep.hkv) continue;
+      qkv_head_out<DH>(v, g, row, p, sl, ep);
+    }
   }
 }
 
@@ -189,89 +279,8 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = mb * BM + wq * 32 + lane;
-      const bool row_ok = row < M;
       const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(wq * 32) << 16);
-
-      if constexpr (EPI == EPI_STORE || EPI == EPI_STORE_F32 || EPI == EPI_RESID || EPI == EPI_PARTIAL) {
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(taddr + c * 32, r);
-          tmem_ld_wait();
-          const int col = nb * BN + c * 32;
-          if (row_ok && col < N) {
-            if constexpr (EPI == EPI_STORE_F32 || EPI == EPI_PARTIAL) {
-              float* base = static_cast<float*>(ep.out);
-              if constexpr (EPI == EPI_PARTIAL) base += (long long)sp * M * N;  // this split's slab
-              float4* dst = reinterpret_cast<float4*>(base + (long long)row * (EPI == EPI_PARTIAL ? N : ep.ldo) + col);
-#pragma unroll
-              for (int i = 0; i < 8; ++i)
-                dst[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
-                                     __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
-            } else {
-              uint32_t w[16];
-              if constexpr (EPI == EPI_RESID) {
-                const uint4* src = reinterpret_cast<const uint4*>(ep.resid + (long long)row * ep.ldr + col);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  const uint4 q = src[i];
-                  const uint32_t uu[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-                  for (int j = 0; j < 4; ++j) {
-                    const float2 f = unpack_bf16(uu[j]);
-                    const int e = 8 * i + 2 * j;
-                    w[4 * i + j] = pack_bf16(f.x + __uint_as_float(r[e]), f.y + __uint_as_float(r[e + 1]));
-                  }
-                }
-              } else {
-#pragma unroll
-                for (int i = 0; i < 16; ++i) w[i] = pack_bf16(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
-              }
-              st_bf16x32(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + col, w);
-            }
-          }
-        }
-      } else if constexpr (EPI == EPI_SWIGLU) {
-        // weights interleaved in 64-row blocks: tile column block 2i = gate, 2i+1 = up
-#pragma unroll 1
-        for (int c = 0; c < BN / 64; ++c) {
-          const int pb = c >> 1, half = c & 1;
-          uint32_t g[32], v[32];
-          tmem_ld32(taddr + pb * 128 + half * 32, g);
-          tmem_ld32(taddr + pb * 128 + 64 + half * 32, v);
-          tmem_ld_wait();
-          const int col = nb * (BN / 2) + pb * 64 + half * 32;  // output column
-          if (row_ok && col < N / 2) {
-            uint32_t w[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const float a0 = silu(__uint_as_float(g[2 * i])) * __uint_as_float(v[2 * i]);
-              const float a1 = silu(__uint_as_float(g[2 * i + 1])) * __uint_as_float(v[2 * i + 1]);
-              w[i] = pack_bf16(a0, a1);
-            }
-            st_bf16x32(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + col, w);
-          }
-        }
-      } else if constexpr (EPI == EPI_QKV) {
-        static_assert(BN % DH == 0, "tile must hold whole heads");
-        const int p = row_ok ? ep.pos[row] : 0;
-        const int sl = row_ok ? ep.slot[row] : 0;
-#pragma unroll 1
-        for (int hh = 0; hh < BN / DH; ++hh) {
-          float v[DH];
-#pragma unroll
-          for (int c = 0; c < DH / 32; ++c) {
-            uint32_t r[32];
-            tmem_ld32(taddr + hh * DH + c * 32, r);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[c * 32 + i] = __uint_as_float(r[i]);
-          }
-          const int g = (nb * BN + hh * DH) / DH;  // global head index in [q | k | v]
-          if (!row_ok || g >= ep.hq + 2 * ep.hkv) continue;
-          qkv_head_out<DH>(v, g, row, p, sl, ep);
-        }
-      }
+      epilogue_rows<BN, EPI, DH>(taddr, row, nb, sp, M, N, ep);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -284,6 +293,173 @@ __global__ void __launch_bounds__(256, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
+}
+
+// ---------------------------------------------------------------- CTA-pair GEMM
+// cta_group::2 variant for large M: a cluster of 2 CTAs (one SM pair) owns a
+// 256 x 256 output tile.  Each CTA stages its 128 rows of A and its 128 of the
+// 256 B rows (TMA completes on the leader's barrier); the leader issues M=256
+// MMAs that read both CTAs' smem and write each CTA's 128 accumulator rows to
+// its own TMEM.  Operand bytes per FLOP halve vs the 128 x 256 single-CTA tile,
+// which is what lifts the L2 -> SM traffic ceiling (~12 TB/s on B200).
+template <int BN>
+struct PairCfg {
+  static constexpr int STAGES = BN == 256 ? 6 : 8;
+  static constexpr uint32_t A_BYTES = 128 * BK * 2, B_BYTES = (BN / 2) * BK * 2, STAGE = A_BYTES + B_BYTES;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE + 256;
+};
+
+template <int BN, int EPI, int DH>
+__global__ void __launch_bounds__(256, 1)
+    gemm_bf16_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
+                         int N, int K, GemmEpi ep) {
+  using C = PairCfg<BN>;
+  constexpr int STAGES = C::STAGES;
+  constexpr uint32_t A_BYTES = C::A_BYTES, B_BYTES = C::B_BYTES, STAGE = C::STAGE;
+  constexpr uint32_t TMEM_COLS = 2 * BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = (int)cluster_id_x(), npairs = (int)nclusters_x();
+  const int m_tiles = (M + 255) / 256, n_tiles = (N + BN - 1) / BN;
+  const int units = m_tiles * n_tiles, kblocks = K / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // 4 epilogue warps in each CTA of the pair
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_2sm(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // peer barriers initialised before any remote arrive / complete_tx
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_act = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = pair; u < units; u += npairs) {
+        const int mb = u % m_tiles, nb = u / m_tiles;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * STAGE);
+          const uint32_t bar = mapa_shared(smem_u32(&full[stage]), 0);
+          tma_load_2d_2sm(&tmA, bar, sA + stage * A_BYTES, kb * BK, mb * 256 + (int)rank * 128, pol_act);
+          tma_load_2d_2sm(&tmB, bar, sB + stage * B_BYTES, kb * BK, nb * BN + (int)rank * (BN / 2), pol_act);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(256, BN);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int u = pair; u < units; u += npairs) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ad = sdesc_k_sw128(smem_u32(sA + stage * A_BYTES));
+          const uint64_t bd = sdesc_k_sw128(smem_u32(sB + stage * B_BYTES));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) umma_bf16_2sm(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+          umma_commit_2sm(&empty[stage], 0x3);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_2sm(&tfull[acc], 0x3);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    const int wq = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 0), tempty1 = mapa_shared(smem_u32(&tempty[1]), 0);
+    for (int u = pair; u < units; u += npairs) {
+      const int mb = u % m_tiles, nb = u / m_tiles;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * 256 + (int)rank * 128 + wq * 32 + lane;
+      const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(wq * 32) << 16);
+      epilogue_rows<BN, EPI, DH>(taddr, row, nb, 0, M, N, ep);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(acc ? tempty1 : tempty0);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  __syncthreads();
+  cluster_sync();  // the leader's MMAs into this CTA's TMEM / smem are complete
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_2sm(tmem_base, TMEM_COLS);
+  }
+}
+
+template <int BN, int EPI, int DH>
+int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const GemmEpi& ep,
+                cudaStream_t stream) {
+  constexpr size_t SMEM = PairCfg<BN>::SMEM;
+  auto kern = gemm_bf16_tc2_kernel<BN, EPI, DH>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    attr_set = true;
+  }
+  const int units = ((M + 255) / 256) * ((N + BN - 1) / BN);
+  const int max_pairs = num_sms() / 2;
+  const int pairs = units < max_pairs ? units : max_pairs;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, ep));
+  return 0;
 }
 
 // ---------------------------------------------------------------- small-M swap-AB
@@ -759,6 +935,62 @@ int dispatch(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long
   }
 }
 
+template <int BN>
+int dispatch_pair(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long long ldb, int M, int N, int K,
+                  int kind, int dh, const GemmEpi& ep, cudaStream_t stream) {
+  CUtensorMap ta, tb;
+  RDKV_TRY(make_tmap(&ta, A, M, K, lda, 128));
+  RDKV_TRY(make_tmap(&tb, B, N, K, ldb, BN / 2));
+  switch (kind) {
+    case EPI_STORE: return launch_pair<BN, EPI_STORE, 0>(ta, tb, M, N, K, ep, stream);
+    case EPI_STORE_F32: return launch_pair<BN, EPI_STORE_F32, 0>(ta, tb, M, N, K, ep, stream);
+    case EPI_RESID: return launch_pair<BN, EPI_RESID, 0>(ta, tb, M, N, K, ep, stream);
+    case EPI_SWIGLU: return launch_pair<BN, EPI_SWIGLU, 0>(ta, tb, M, N, K, ep, stream);
+    case EPI_QKV:
+      if (dh == 64) return launch_pair<BN, EPI_QKV, 64>(ta, tb, M, N, K, ep, stream);
+      if (dh == 128) return launch_pair<BN, EPI_QKV, 128>(ta, tb, M, N, K, ep, stream);
+      return set_error(RDKV_ERR_ARG, "qkv: head_dim %d unsupported (64 or 128)", dh);
+    default: return set_error(RDKV_ERR_ARG, "gemm: unknown epilogue %d", kind);
+  }
+}
+
+// Tile plan for the unsplit path: {1-CTA 128x128, 1-CTA 128x256, pair 256x128,
+// pair 256x256}, cost = waves x per-SM tile work / efficiency.  Efficiencies are
+// the measured tensor-pipe ceilings set by L2->SM operand traffic per FLOP.
+struct TilePlan {
+  bool pair;
+  int bn;
+};
+bool pairs_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("RDKV_GEMM_PAIRS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+TilePlan pick_tiles(int M, int N) {
+  const int sms = num_sms();
+  struct Cand {
+    bool pair;
+    int bn;
+    double eff;
+  } cands[4] = {{false, 128, 0.60}, {false, 256, 0.75}, {true, 128, 0.75}, {true, 256, 0.90}};
+  double best = 1e30;
+  TilePlan plan{false, 256};
+  for (const Cand& c : cands) {
+    if (c.pair && (M < 256 || !pairs_enabled())) continue;
+    const int rows = c.pair ? 256 : 128;
+    const long long units = (long long)((M + rows - 1) / rows) * ((N + c.bn - 1) / c.bn);
+    const int slots = c.pair ? sms / 2 : sms;
+    const double t = (double)((units + slots - 1) / slots) * 128.0 * c.bn / c.eff;
+    if (t < best - 1e-9) {
+      best = t;
+      plan = {c.pair, c.bn};
+    }
+  }
+  return plan;
+}
+
 int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long long ldb, int M, int N, int K,
                 int kind, int dh, const GemmEpi& ep, cudaStream_t stream, int bn) {
   if (M <= 0 || N <= 0) return 0;
@@ -767,7 +999,8 @@ int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, l
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15)
     return set_error(RDKV_ERR_ARG, "gemm: operands must be 16-byte aligned");
   if ((lda | ldb) & 7) return set_error(RDKV_ERR_ARG, "gemm: leading dims must be multiples of 8");
-  if (bn != 0 && bn != 128 && bn != 256) return set_error(RDKV_ERR_ARG, "gemm: tile N %d must be 128 or 256", bn);
+  if (bn != 0 && bn != 128 && bn != 256 && bn != 384 && bn != 512)
+    return set_error(RDKV_ERR_ARG, "gemm: tile N %d must be 128, 256 (or 384/512 for CTA pairs)", bn);
   if (kind == EPI_SWIGLU && N % 128 != 0) return set_error(RDKV_ERR_ARG, "swiglu: N must be a multiple of 128");
   int splits = 1;
   if (ep.splitk_ws) {
@@ -779,6 +1012,19 @@ int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, l
       splits = pick_splits(M, N, K, bn);
       if ((size_t)splits * M * N * sizeof(float) > ep.splitk_bytes) splits = 1;
     }
+  }
+  if (bn == 0 && splits == 1) {
+    const TilePlan tp = pick_tiles(M, N);
+    if (tp.pair && !(kind == EPI_SWIGLU && N % tp.bn != 0)) {
+      if (tp.bn == 128) return dispatch_pair<128>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
+      return dispatch_pair<256>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
+    }
+    bn = tp.bn;
+  }
+  if (bn == 512 || bn == 384) {  // explicit CTA-pair request (tests): 512 -> 256 x 256, 384 -> 256 x 128
+    if (M < 256) return set_error(RDKV_ERR_ARG, "gemm: CTA-pair tiles need M >= 256");
+    if (bn == 384) return dispatch_pair<128>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
+    return dispatch_pair<256>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
   }
   if (bn == 0) bn = pick_bn(M, N);
   if (kind == EPI_SWIGLU && N % bn != 0) bn = 128;

@@ -87,44 +87,46 @@ __global__ void embed_kernel(const int* __restrict__ tok, const __nv_bfloat16* _
 }
 
 // ---------------------------------------------------------------- rmsnorm
-// out[r] = x[src_row(r)] * rsqrt(mean(x^2) + eps) * gain ; one CTA per row.
-__global__ void __launch_bounds__(256) rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, long long ldx,
-                                                      const int* __restrict__ rows, const float* __restrict__ gain,
-                                                      __nv_bfloat16* __restrict__ out, long long ldo, int d,
-                                                      float eps) {
+// out[r] = x[src_row(r)] * rsqrt(mean(x^2) + eps) * gain.
+// Warp per row, the row held in registers (CH 16-byte chunks per lane, d <=
+// 256*CH), so x is read once: one HBM pass in, one out.
+template <int CH>
+__global__ void __launch_bounds__(256) rmsnorm_warp_kernel(const __nv_bfloat16* __restrict__ x, long long ldx,
+                                                           const int* __restrict__ rows,
+                                                           const float* __restrict__ gain,
+                                                           __nv_bfloat16* __restrict__ out, long long ldo, int n_rows,
+                                                           int d, float eps) {
   pdl_trigger();
   pdl_wait();
-  const int r = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * 8 + warp;
+  if (r >= n_rows) return;
   const int src_row = rows ? rows[r] : r;
   const __nv_bfloat16* xr = x + (long long)src_row * ldx;
+  uint4 v[CH];
   float ss = 0.f;
-  for (int i = threadIdx.x * 8; i < d; i += blockDim.x * 8) {
-    const uint4 u = *reinterpret_cast<const uint4*>(xr + i);
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int i = (c * 32 + lane) * 8;
+    v[c] = i < d ? ld_stream(xr + i) : make_uint4(0, 0, 0, 0);
+    const uint32_t w[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const float2 f = unpack_bf16_f(w[j]);
       ss += f.x * f.x + f.y * f.y;
     }
   }
-  __shared__ float red[32];
   for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
-    if (threadIdx.x == 0) red[0] = v;
-  }
-  __syncthreads();
-  const float inv = rsqrtf(red[0] / (float)d + eps);
+  const float inv = rsqrtf(ss / (float)d + eps);
   __nv_bfloat16* orow = out + (long long)r * ldo;
-  for (int i = threadIdx.x * 8; i < d; i += blockDim.x * 8) {
-    const uint4 u = *reinterpret_cast<const uint4*>(xr + i);
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int i = (c * 32 + lane) * 8;
+    if (i >= d) break;
     const float4 g0 = *reinterpret_cast<const float4*>(gain + i);
     const float4 g1 = *reinterpret_cast<const float4*>(gain + i + 4);
     const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    const uint32_t w[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
     uint32_t o[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -224,9 +226,14 @@ int launch_embed(const int* tok, const __nv_bfloat16* table, __nv_bfloat16* out,
 int launch_rmsnorm(const __nv_bfloat16* x, long long ldx, const int* rows, const float* gain, __nv_bfloat16* out,
                    long long ldo, int n_rows, int d, float eps, cudaStream_t st) {
   if (n_rows <= 0) return 0;
-  if (d % 8 != 0) return set_error(RDKV_ERR_ARG, "rmsnorm: d must be a multiple of 8");
-  CUDA_TRY(launch_k(rmsnorm_kernel, dim3(n_rows), dim3(256), 0, st, x, ldx, rows, gain, out, ldo, d, eps));
-  CUDA_TRY(cudaGetLastError());
+  if (d % 8 != 0 || d > 8192) return set_error(RDKV_ERR_ARG, "rmsnorm: d must be a multiple of 8 and <= 8192");
+  const dim3 grid((n_rows + 7) / 8), block(256);
+  if (d <= 2048)
+    CUDA_TRY(launch_k(rmsnorm_warp_kernel<8>, grid, block, 0, st, x, ldx, rows, gain, out, ldo, n_rows, d, eps));
+  else if (d <= 4096)
+    CUDA_TRY(launch_k(rmsnorm_warp_kernel<16>, grid, block, 0, st, x, ldx, rows, gain, out, ldo, n_rows, d, eps));
+  else
+    CUDA_TRY(launch_k(rmsnorm_warp_kernel<32>, grid, block, 0, st, x, ldx, rows, gain, out, ldo, n_rows, d, eps));
   return 0;
 }
 

@@ -9,7 +9,7 @@ from paper_2504_11765_b200 import _lib
 
 pytestmark = pytest.mark.gpu
 
-TILES = [0, 128, 256]  # 0 = automatic (small M with scratch -> 64-wide tiles x K splits)
+TILES = [0, 128, 256, 384, 512]  # 0 automatic; 384 / 512 = CTA-pair (cta_group::2) 256x128 / 256x256 tiles
 
 
 def _ptr(t):
@@ -19,6 +19,8 @@ def _ptr(t):
 def _gemm(A, B, D, epi, R=None, tile=0, scratch=None):
     s = torch.cuda.current_stream().cuda_stream
     M, K = A.shape
+    if tile in (384, 512) and M < 256:
+        pytest.skip("CTA-pair tiles need M >= 256")
     N = B.shape[0]
     _lib.check(_lib.lib().rdkv_gemm_bf16_ex(
         _ptr(A), A.stride(0), _ptr(B), B.stride(0), _ptr(D), D.stride(0),
