@@ -84,9 +84,13 @@ def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("RDKV_SHARE_GPU") == "1":  # plumbing test: every rank on GPU 0
+        local = 0
     if ws > 1:
         import torch.distributed as dist
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        backend = os.environ.get("RDKV_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
+        if backend == "nccl":
+            torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)
     return ws, rank, local
 
@@ -101,6 +105,8 @@ def _max_over_ranks(x: float, ws: int, device) -> float:
     if ws == 1:
         return x
     import torch.distributed as dist
+    if dist.get_backend() != "nccl":
+        device = "cpu"
     t = torch.tensor([x], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
