@@ -233,11 +233,14 @@ RDKV_API int rdkv_forward(rdkv_model* model, const rdkv_batch* batch, void* work
 /* ------------------------------------------------------------ measurement */
 
 /* Kernel classes of rdkv_forward for per-class device timing. */
-#define RDKV_PROF_GEMM 0 /* K1 layer GEMMs: QKV, O, gate/up, down           */
+#define RDKV_PROF_QKV 0  /* K1 QKV GEMM (+ RoPE / KV-layout epilogue)        */
 #define RDKV_PROF_ATTN 1 /* K2/K4 attention                                  */
 #define RDKV_PROF_MISC 2 /* embedding gather, RMSNorm                         */
 #define RDKV_PROF_HEAD 3 /* K5 LM-head GEMM + argmax                          */
-#define RDKV_PROF_N 4
+#define RDKV_PROF_O 4    /* K1 attention-output GEMM (+ residual)            */
+#define RDKV_PROF_GU 5   /* K1 gate/up GEMM (+ SwiGLU)                       */
+#define RDKV_PROF_DOWN 6 /* K1 down GEMM (+ residual)                        */
+#define RDKV_PROF_N 7
 
 /* With on != 0, every kernel rdkv_forward launches is bracketed by CUDA events
  * on its stream.  Launch and algorithmic-FLOP counters run regardless. */

@@ -31,8 +31,8 @@ struct rdkv_model {
   };
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> spare;
-  int64_t launches[RDKV_PROF_N] = {0, 0, 0, 0};
-  double flops[RDKV_PROF_N] = {0, 0, 0, 0};
+  int64_t launches[RDKV_PROF_N] = {};
+  double flops[RDKV_PROF_N] = {};
 
   cudaEvent_t event() {
     if (!spare.empty()) {
@@ -239,7 +239,7 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     eq.rope = m->rope;
     eq.hq = hq;
     eq.hkv = hkv;
-    LAUNCH(RDKV_PROF_GEMM, 2.0 * T * (hq + 2 * hkv) * dh * d.hidden,
+    LAUNCH(RDKV_PROF_QKV, 2.0 * T * (hq + 2 * hkv) * dh * d.hidden,
            launch_gemm(ws.h, d.hidden, W(m, wb + 1), d.hidden, T, (int)((hq + 2 * hkv) * dh), d.hidden, EPI_QKV, dh,
                          eq, st));
     AttnParams ap{};
@@ -287,7 +287,7 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
       er.norm_gain = G(m, wb + 3);
       er.norm_out = ws.h;
     }
-    LAUNCH(RDKV_PROF_GEMM, 2.0 * T * qd * d.hidden, launch_gemm(ws.o, qd, W(m, wb + 2), qd, T, d.hidden, (int)qd, EPI_RESID, 0, er, st));
+    LAUNCH(RDKV_PROF_O, 2.0 * T * qd * d.hidden, launch_gemm(ws.o, qd, W(m, wb + 2), qd, T, d.hidden, (int)qd, EPI_RESID, 0, er, st));
     // MLP block
     if (!o_fused)
       LAUNCH(RDKV_PROF_MISC, 0.0, launch_rmsnorm(ws.x, d.hidden, nullptr, G(m, wb + 3), ws.h, d.hidden, T, d.hidden, d.norm_eps, st));
@@ -296,11 +296,11 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     eg.splitk_bytes = ws.splitk_bytes;
     eg.out = ws.a;
     eg.ldo = d.ffn;
-    LAUNCH(RDKV_PROF_GEMM, 4.0 * T * d.ffn * d.hidden, launch_gemm(ws.h, d.hidden, W(m, wb + 4), d.hidden, T, 2 * d.ffn, d.hidden, EPI_SWIGLU, 0, eg, st));
+    LAUNCH(RDKV_PROF_GU, 4.0 * T * d.ffn * d.hidden, launch_gemm(ws.h, d.hidden, W(m, wb + 4), d.hidden, T, 2 * d.ffn, d.hidden, EPI_SWIGLU, 0, eg, st));
     h_ready = down_fused && l + 1 < d.layers;
     er.norm_gain = h_ready ? G(m, wb + RDKV_WEIGHTS_PER_LAYER + 0) : nullptr;  // next layer's attention norm
     er.norm_out = h_ready ? ws.h : nullptr;
-    LAUNCH(RDKV_PROF_GEMM, 2.0 * T * d.ffn * d.hidden, launch_gemm(ws.a, d.ffn, W(m, wb + 5), d.ffn, T, d.hidden, d.ffn, EPI_RESID, 0, er, st));
+    LAUNCH(RDKV_PROF_DOWN, 2.0 * T * d.ffn * d.hidden, launch_gemm(ws.a, d.ffn, W(m, wb + 5), d.ffn, T, d.hidden, d.ffn, EPI_RESID, 0, er, st));
   }
   if (b->want_logits) {
     if (!b->logits || !b->last_row) return set_error(RDKV_ERR_ARG, "forward: logits requested without buffers");
@@ -325,7 +325,7 @@ int rdkv_profile_enable(rdkv_model* m, int on) {
 
 int rdkv_profile_collect(rdkv_model* m, double* ms, int64_t* launches, double* flops) {
   if (!m) return set_error(RDKV_ERR_ARG, "profile_collect: null model");
-  double acc[RDKV_PROF_N] = {0, 0, 0, 0};
+  double acc[RDKV_PROF_N] = {};
   for (auto& r : m->recs) {
     CUDA_TRY(cudaEventSynchronize(r.b));
     float t = 0.f;

@@ -70,7 +70,7 @@ _N_SIG = {
                                        C.POINTER(C.c_double)]),
 }
 
-PROF_CLASSES = ("gemm", "attention", "norm_embed", "lm_head")
+PROF_CLASSES = ("gemm_qkv", "attention", "norm_embed", "lm_head", "gemm_o", "gemm_gate_up", "gemm_down")
 
 
 def _L():
@@ -258,7 +258,8 @@ class DeviceModel:
 
     def collect(self) -> dict[str, dict]:
         """Per kernel class since the last collect: device ms, launches, GEMM FLOPs."""
-        ms, n, fl = (C.c_double * 4)(), (C.c_int64 * 4)(), (C.c_double * 4)()
+        k = len(PROF_CLASSES)
+        ms, n, fl = (C.c_double * k)(), (C.c_int64 * k)(), (C.c_double * k)()
         _lib.check(_L().rdkv_profile_collect(self._h, ms, n, fl))
         return {k: {"ms": ms[i], "launches": int(n[i]), "flops": fl[i]} for i, k in enumerate(PROF_CLASSES)}
 
