@@ -156,6 +156,27 @@ RDKV_API int rdkv_kv_unpack(const rdkv_unpack_job* jobs_dev, int n_jobs, int max
                             int layers, int kv_heads, int head_dim, int64_t pool_slots,
                             int elem_width, int layer_begin, int layer_end, void* stream);
 
+/* ------------------------------------------------ K2/K4: prefill attention */
+
+/* Causal GQA attention of n_tokens new query rows over each sequence's cached
+ * prefix plus its own new tokens (cached_prefill_work semantics, costs.py:89-99:
+ * the token at position n_cached + i sees every position <= its own).
+ *   q, o      [n_tokens][n_heads * head_dim] bf16 (q post-RoPE)
+ *   kplane/vplane  one layer's K / V plane [kv_heads][kv_slots][head_dim] bf16,
+ *             position p of sequence s at slot block_table[s*bt_stride + p/block_size]
+ *             * block_size + p % block_size
+ * impl 0 = tcgen05 kernel (block_size % 64 == 0 or bt_stride == 1), 1 = mma.sync
+ * kernel (any block size).  `scratch` (rdkv_attention_scratch_bytes) enables
+ * split-KV for grids too small to fill the GPU.  The building block rdkv_forward
+ * calls per layer; exposed for tests. */
+RDKV_API int rdkv_attention(const void* q, int64_t ldq, void* o, int64_t ldo, const void* kplane,
+                            const void* vplane, int64_t kv_slots, const int32_t* seq_start,
+                            const int32_t* seq_new, const int32_t* seq_cached, const int32_t* block_table,
+                            int bt_stride, int block_size, int n_seqs, int n_tokens, int max_new,
+                            int max_ctx, int n_heads, int kv_heads, int head_dim, int impl, void* scratch,
+                            size_t scratch_bytes, void* stream);
+RDKV_API size_t rdkv_attention_scratch_bytes(int n_tokens, int n_heads, int head_dim);
+
 /* ------------------------------------------ model: document / query prefill */
 
 /* Llama-shaped decoder (RMSNorm, RoPE rotate-half, GQA, SwiGLU). */

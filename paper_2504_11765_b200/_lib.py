@@ -11,7 +11,10 @@ import ctypes as C
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "librdkv.so"
+import os
+
+# RDKV_LIB points at an alternative build (A/B measurements of kernel variants)
+LIB_PATH = Path(os.environ.get("RDKV_LIB") or Path(__file__).resolve().parent / "librdkv.so")
 
 RDKV_OK = 0
 RDKV_ERR_BAD_MAGIC = -1
@@ -69,6 +72,9 @@ SIGNATURES: dict[str, tuple] = {
                               C.POINTER(_sz), C.POINTER(_sz)]),
     "rdkv_drop_page_cache": (_i32, [_cp]),
     "rdkv_gemm_bf16": (_i32, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _i32, _i32, _vp]),
+    "rdkv_attention": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32,
+                              _i32, _i32, _i32, _i32, _i32, _vp, _sz, _vp]),
+    "rdkv_attention_scratch_bytes": (_sz, [_i32, _i32, _i32]),
     "rdkv_gemm_bf16_ex": (_i32, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _sz,
                                  _vp]),
 }

@@ -3,23 +3,30 @@
 //
 // Semantics are those of attention.cu (reference: cached_prefill_work,
 // costs.py:89-99 — new tokens at positions [n_cached, n_cached+n_new) attend
-// over every position <= their own).  A CTA owns 128 query rows of ONE kv
+// over every position <= their own).  A Q tile is 128 query rows of ONE kv
 // head, row r = (token t0 + r / G, q-head kvh*G + r % G), so the G query heads
-// sharing a K/V head read each K/V tile once.
+// sharing a K/V head read each K/V tile once.  A CTA owns TWO consecutive Q
+// tiles (for G = 4: 64 query tokens = a whole C2 query) that share every K/V
+// tile the TMA brings in.
 //
-// Warp roles (256 threads, one CTA per SM):
-//   warp 0      TMA producer: K and V tiles of 128 positions (two 64-row boxes
-//               each, one per KV block of the paged pool / blob) into a
-//               STAGES-deep smem ring, 128-byte swizzle
-//   warp 1      MMA issuer (one thread): S[b] = Q.K^T  (M=128, N=128, K=dh) into
-//               TMEM, then O_tile[b] = P.V (M=128, N=dh, K=128; V is the
-//               MN-major B operand) into TMEM; order QK0, QK1, PV0, QK2, PV1, ...
-//   warp 2      TMEM allocator (512 columns: S x2, O_tile x2)
-//   warps 4..7  softmax (one query row per thread = one TMEM lane): load Q,
-//               then per tile: tcgen05.ld S, mask, online max / exp2 / sum,
-//               write P (bf16, swizzled K-major) to smem; fold the previous
-//               tile's O_tile into a register accumulator with the running
-//               rescale; finally normalise and store O.
+// Warp roles (320 threads, one CTA per SM):
+//   warps 0-3   softmax of Q tile 0, warps 4-7 softmax of Q tile 1: one query
+//               row per thread (= one TMEM lane).  Per KV tile: tcgen05.ld the
+//               128 scores, mask, row max (FMNMX3), P = 2^(s*scale - m) with
+//               packed FFMA2 + MUFU ex2, tcgen05.st of P (bf16 pairs) into TMEM.
+//               The row max is moved lazily (only when it grows by > 2^8), and
+//               only then is the O row in TMEM rescaled.  The two warpgroups
+//               run independently, so one's exp2 overlaps the other's loads.
+//   warp 8      TMA producer: K and V tiles of 128 positions (two 64-row boxes
+//               each, one per KV block of the paged pool / blob), STAGES-deep
+//               smem ring, 128-byte swizzle.
+//   warps 9,10  MMA issuers, one thread per Q tile (warp 9 also allocates
+//               TMEM): S_i = Q_i.K^T (M=128, N=128, K=dh, smem operands) and
+//               O_i += P_i.V with P_i read from TMEM (tcgen05.mma A-from-TMEM,
+//               V as the MN-major B).  Separate issuers keep the two Q tiles'
+//               pipelines independent.
+// TMEM (512 columns): S_0 S_1 (128 each), O_0 O_1 (dh each), P_0 P_1 (64 each,
+// dh=64) or P_i over S_i (dh=128, after S_i is in registers).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
@@ -42,19 +49,30 @@ constexpr int HALF = 64;  // rows per TMA box (= one KV block of the pool)
 
 template <int DH>
 struct TcCfg {
-  static constexpr int STAGES = DH == 64 ? 3 : 2;
-  static constexpr uint32_t QB = ROWS * DH * 2;    // Q tile bytes
+  // dh=128 fills TMEM with S0,S1,O0,O1 (4 x 128 columns), so P_i is written over
+  // S_i (already in registers); dh=64 has room for separate P buffers
+  static constexpr bool ALIAS = DH == 128;
+  static constexpr int STAGES = DH == 64 ? 5 : 2;
+  static constexpr uint32_t QB = ROWS * DH * 2;    // one Q tile
   static constexpr uint32_t KB = BKV * DH * 2;     // one K (or V) tile
-  static constexpr uint32_t PB = ROWS * BKV * 2;   // one P tile
-  static constexpr uint32_t OFF_Q = 0;
-  static constexpr uint32_t OFF_K = OFF_Q + QB;
+  static constexpr uint32_t OFF_Q = 0;             // [2 Q tiles]
+  static constexpr uint32_t OFF_K = OFF_Q + 2 * QB;
   static constexpr uint32_t OFF_V = OFF_K + STAGES * KB;
-  static constexpr uint32_t OFF_P = OFF_V + STAGES * KB;
-  static constexpr uint32_t OFF_RED = OFF_P + 2 * PB;  // [2 parity][2 half][128] fp32 row-max / row-sum exchange
-  static constexpr uint32_t OFF_BAR = OFF_RED + 4 * ROWS * 4;
-  // no alignment slack: DH=128 uses all but ~0.6 KB of the 227 KB; the base is checked at run time
-  static constexpr size_t SMEM = OFF_BAR + 8 * (1 + 3 * STAGES + 12) + 16;
+  static constexpr uint32_t OFF_BAR = OFF_V + STAGES * KB;
+  static constexpr size_t SMEM = OFF_BAR + 8 * (1 + 3 * STAGES + 8) + 16;
+  // TMEM columns
+  static constexpr uint32_t COL_S = 0;                          // S_i at 128 i
+  static constexpr uint32_t COL_O = 2 * BKV;                    // O_i at 256 + DH i
+  static constexpr uint32_t COL_P = ALIAS ? 0 : 2 * BKV + 2 * DH;  // P_i at COL_P + (ALIAS ? 128 : 64) i
+  static constexpr uint32_t P_STRIDE = ALIAS ? BKV : BKV / 2;
 };
+
+constexpr int THREADS = 384;  // warps 0-3 / 4-7: softmax of Q tile 0 / 1; 8: TMA; 9 / 10: MMA of tile 0 / 1; 11 idle
+constexpr float RESCALE_LOG2 = 8.f;   // lazy O rescale: keep a stale row max until it is 2^8 too small
+#ifndef RDKV_ATTN_EMU
+#define RDKV_ATTN_EMU 3
+#endif
+constexpr int EMU_OF_8 = RDKV_ATTN_EMU;  // exp2 of this many of every 8 score groups runs as a polynomial
 
 // K-major SW128 operand (rows of 128 B, 8-row atoms 1024 B apart)
 __device__ __forceinline__ uint64_t desc_k(uint32_t saddr) { return sdesc_k_sw128(saddr); }
@@ -71,7 +89,7 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
 }
 
 template <int DH>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnParams p) {
   using C = TcCfg<DH>;
   constexpr int ST = C::STAGES;
@@ -84,24 +102,22 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* k_full = bars + 1;             // [ST]
   uint64_t* v_full = k_full + ST;          // [ST]
   uint64_t* kv_empty = v_full + ST;        // [ST]
-  uint64_t* s_full = kv_empty + ST;        // [2]
-  uint64_t* s_empty = s_full + 2;          // [2]
-  uint64_t* p_full = s_empty + 2;          // [2]
-  uint64_t* p_empty = p_full + 2;          // [2]
-  uint64_t* o_full = p_empty + 2;          // [2]
-  uint64_t* o_empty = o_full + 2;          // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
+  uint64_t* s_full = kv_empty + ST;        // [2] per Q tile: S_i = Q_i.K^T landed
+  uint64_t* s_empty = s_full + 2;          // [2] S_i read into registers
+  uint64_t* p_full = s_empty + 2;          // [2] P_i written (and O_i rescaled)
+  uint64_t* o_done = p_full + 2;           // [2] O_i += P_i.V retired (P_i free)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
   const int G = p.hq / p.hkv;
+  const int TPT = ROWS / G;                 // tokens per Q tile
   const int s = blockIdx.z, kvh = blockIdx.y;
   const int xb = gridDim.x - 1 - blockIdx.x;  // longest causal rows first
-  const int qb = xb / p.kv_splits, ks = xb % p.kv_splits;  // query block, KV split
+  const int qb = xb / p.kv_splits, ks = xb % p.kv_splits;  // query-tile pair, KV split
   const int n_new = p.seq_new[s];
-  const int tok_per_cta = ROWS / G;
-  const int tok0 = qb * tok_per_cta;
+  const int tok0 = qb * 2 * TPT;
   if (tok0 >= n_new) return;
-  const int ntok = min(tok_per_cta, n_new - tok0);
-  const int nrows = ntok * G;
+  const int ntok = min(2 * TPT, n_new - tok0);
+  const int n_q = ntok > TPT ? 2 : 1;       // active Q tiles
   const int pos0 = p.seq_cached[s] + tok0;
   const int kv_len = pos0 + ntok;
   // this CTA's share of the KV tiles (split-KV when the grid alone cannot fill the GPU)
@@ -113,38 +129,35 @@ __global__ void __launch_bounds__(384, 1)
   const int* bt = p.block_table + (long long)s * p.bt_stride;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 8 && lane == 0) {
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
-  }
-  if (warp == 1 && lane == 0) {
     mbar_init(q_full, 8);
     for (int i = 0; i < ST; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&v_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
+      mbar_init(&kv_empty[i], n_q);  // released by both Q tiles' P.V
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 8);
-      mbar_init(&p_full[i], 8);
-      mbar_init(&p_empty[i], 1);
-      mbar_init(&o_full[i], 1);
-      mbar_init(&o_empty[i], 8);
+      mbar_init(&s_empty[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&o_done[i], 1);
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();
   pdl_wait();  // q / KV planes written by the predecessor are visible from here
-  const uint32_t tS = tmem;             // S buffers at columns [0,128) and [128,256)
-  const uint32_t tO = tmem + 2 * BKV;   // O_tile buffers at 256 and 256 + DH
 
-  if (warp == 0) {
+  // register budget: the softmax warpgroups hold a 128-score row per thread,
+  // the TMA / MMA warpgroup gives its registers up
+  if (warp >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
+  if (warp == 8) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       const long long row0 = (long long)kvh * (p.head_stride / DH);  // first row of this head in the plane view
@@ -174,206 +187,216 @@ __global__ void __launch_bounds__(384, 1)
                                c * 64, rows[h]);
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+  } else if (warp == 9 || warp == 10) {
+    // ------------------------------------------------------------ MMA issuers
+    // one issuing thread per Q tile, so neither softmax warpgroup ever waits on
+    // the other's progress (their exp2 phases drift apart and overlap)
+    const int i = warp - 9;
+    if (lane == 0 && n_tiles > 0 && i < n_q) {
       constexpr uint32_t idesc_qk = idesc_bf16_f32(ROWS, BKV);
       constexpr uint32_t idesc_pv = idesc_bf16_f32(ROWS, DH) | (1u << 16);  // B (V) is MN-major
-      mbar_wait_sleep(q_full, 0);
-      tc_fence_after();
-      auto issue_qk = [&](int j) {
-        const int st = j % ST, b = j & 1;
-        mbar_wait_sleep(&k_full[st], (j / ST) & 1);
-        mbar_wait_sleep(&s_empty[b], ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t qa = sb + C::OFF_Q, ka = sb + C::OFF_K + st * C::KB;
+      const uint32_t qa = sb + C::OFF_Q + i * C::QB;
+      const uint32_t tS = tmem + C::COL_S + i * BKV, tO = tmem + C::COL_O + i * DH;
+      const uint32_t tP = tmem + C::COL_P + i * C::P_STRIDE;
+      auto issue_qk = [&](int j) {  // S_i = Q_i . K(j)^T
+        const uint32_t ka = sb + C::OFF_K + (j % ST) * C::KB;
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
-          const uint32_t blk = (kk >> 2) * (ROWS * 128), sub = (kk & 3) * 32;
-          umma_bf16(tS + b * BKV, desc_k(qa + blk + sub), desc_k(ka + (kk >> 2) * (BKV * 128) + sub), idesc_qk,
-                    kk > 0 ? 1u : 0u);
+          const uint32_t sub = (kk & 3) * 32;
+          umma_bf16(tS, desc_k(qa + (kk >> 2) * (ROWS * 128) + sub), desc_k(ka + (kk >> 2) * (BKV * 128) + sub),
+                    idesc_qk, kk > 0 ? 1u : 0u);
         }
-        umma_commit(&s_full[b]);
+        umma_commit(&s_full[i]);
       };
-      auto issue_pv = [&](int j) {
-        const int st = j % ST, b = j & 1;
-        mbar_wait_sleep(&v_full[st], (j / ST) & 1);
-        mbar_wait_sleep(&p_full[b], (j >> 1) & 1);
-        mbar_wait_sleep(&o_empty[b], ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t pa = sb + C::OFF_P + b * C::PB, va = sb + C::OFF_V + st * C::KB;
-#pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk) {
-          const uint32_t a_off = (kk >> 2) * (ROWS * 128) + (kk & 3) * 32;
-          umma_bf16(tO + b * DH, desc_k(pa + a_off), desc_mn(va + kk * 2048, BKV * 128), idesc_pv, kk > 0 ? 1u : 0u);
-        }
-        umma_commit(&o_full[b]);
-        umma_commit(&p_empty[b]);
-        umma_commit(&kv_empty[st]);
-      };
-      if (n_tiles > 0) issue_qk(0);
+      mbar_wait_sleep(q_full, 0);
+      mbar_wait_sleep(&k_full[0], 0);
+      tc_fence_after();
+      issue_qk(0);
       for (int j = 0; j < n_tiles; ++j) {
-        if (j + 1 < n_tiles) issue_qk(j + 1);
-        issue_pv(j);
+        const int st = j % ST;
+        const bool more = j + 1 < n_tiles;
+        if (!C::ALIAS && more) {  // next S_i while the softmax still works on this tile
+          mbar_wait_sleep(&k_full[(j + 1) % ST], ((j + 1) / ST) & 1);
+          mbar_wait_sleep(&s_empty[i], j & 1);
+          tc_fence_after();
+          issue_qk(j + 1);
+        }
+        mbar_wait_sleep(&v_full[st], (j / ST) & 1);
+        mbar_wait_sleep(&p_full[i], j & 1);
+        tc_fence_after();
+        const uint32_t va = sb + C::OFF_V + st * C::KB;
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk)  // O_i (+)= P_i . V(j), P_i from TMEM
+          umma_bf16_ts(tO, tP + kk * 8, desc_mn(va + kk * 2048, BKV * 128), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&o_done[i]);
+        umma_commit(&kv_empty[st]);
+        if (C::ALIAS && more) {  // S_i overwrites P_i only after the P.V above (issue order)
+          mbar_wait_sleep(&k_full[(j + 1) % ST], ((j + 1) / ST) & 1);
+          tc_fence_after();
+          issue_qk(j + 1);
+        }
       }
     }
-  } else if (warp >= 4) {
-    // ------------------------------------------------------------ softmax warps
-    // 8 warps: warp 4+q and warp 8+q both own TMEM lanes [32q, 32q+32) (query
-    // rows); half h = (warp-4)/4 takes S columns [64h, 64h+64) and O columns
-    // [h*DH/2, (h+1)*DH/2).  The pair exchanges the row max per tile.
-    const int quad = (warp - 4) & 3, h = (warp - 4) >> 2;
-    const int r = quad * 32 + lane;  // query row == TMEM lane
+  } else if (warp < 8) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
+    // ------------------------------------------------------------ softmax warpgroups
+    // warp w < 8: Q tile i = w / 4, TMEM lanes [32 (w % 4), +32) = query rows;
+    // each thread owns one full row of S (128 keys) and of O.
+    const int i = warp >> 2, quad = warp & 3;
+    const int r = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    float* red = reinterpret_cast<float*>(smem + C::OFF_RED);  // [2 parity][2 half][128 rows]
-    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory"); };
-    // Q row half -> smem (K-major SW128, DH/64 column blocks of [128 rows][128 B])
+    const int nrows = max(0, min(TPT, ntok - i * TPT)) * G;
+    // Q row -> smem (K-major SW128, DH/64 column blocks of [128 rows][128 B])
     {
       const bool ok = r < nrows;
       const int rr = ok ? r : 0;
-      const uint4* src = reinterpret_cast<const uint4*>(p.q + (long long)(row_base + rr / G) * p.ldq +
-                                                        (long long)(kvh * G + rr % G) * DH);
+      const uint4* src = reinterpret_cast<const uint4*>(
+          p.q + (long long)(row_base + i * TPT + rr / G) * p.ldq + (long long)(kvh * G + rr % G) * DH);
 #pragma unroll
-      for (int cc = 0; cc < DH / 16; ++cc) {
-        const int c = h * (DH / 16) + cc;
+      for (int c = 0; c < DH / 8; ++c) {
         const uint4 v = ok ? src[c] : make_uint4(0, 0, 0, 0);
-        const uint32_t a = sb + C::OFF_Q + (c >> 3) * (ROWS * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4);
+        const uint32_t a = sb + C::OFF_Q + i * C::QB + (c >> 3) * (ROWS * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4);
         st_shared_v4(a, v.x, v.y, v.z, v.w);
       }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(q_full);
     }
-    // padded rows pretend to be the last valid position so no row is fully masked
-    const int qpos = (r < nrows) ? pos0 + r / G : kv_len - 1;
-    const int kmax = min(qpos, kv_len - 1);  // last visible key position of this row
-    const float sl2 = p.scale_log2;
-    constexpr int OD = DH / 2;  // O columns owned by this half
-    float o_acc[OD];
+    if (i < n_q && n_tiles > 0) {
+      // padded rows pretend to be the last valid position so no row is fully masked
+      const int qpos = (r < nrows) ? pos0 + i * TPT + r / G : kv_len - 1;
+      const float sl2 = p.scale_log2;
+      const uint32_t tS = tmem + C::COL_S + i * BKV + lane_off;
+      const uint32_t tO = tmem + C::COL_O + i * DH + lane_off;
+      const uint32_t tP = tmem + C::COL_P + i * C::P_STRIDE + lane_off;
+      float m_used = -INFINITY;  // row max the P values and O are scaled to (log2 domain)
+      float l = 0.f;             // row sum at scale m_used
+      for (int j = 0; j < n_tiles; ++j) {
+        mbar_wait(&s_full[i], j & 1);
+        tc_fence_after();
+        uint32_t sv[BKV];
 #pragma unroll
-    for (int i = 0; i < OD; ++i) o_acc[i] = 0.f;
-    float m_run = -INFINITY;   // max used for the newest P
-    float m_acc = -INFINITY;   // scale of o_acc
-    float m_pend = -INFINITY;  // max of the tile whose O_tile is pending
-    float l = 0.f;             // this half's share of the row sum (same scale as o_acc after the last fold)
-
-    auto consume = [&](int t, float m_t) {
-      const int b = t & 1;
-      mbar_wait(&o_full[b], (t >> 1) & 1);
-      tc_fence_after();
-      const float f = ex2_approx(m_acc - m_t);
-#pragma unroll
-      for (int c = 0; c < OD / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tO + b * DH + h * OD + c * 32 + lane_off, v);
+        for (int c = 0; c < BKV / 32; ++c) tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[c * 32]));
         tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[i]);
+        const int lim = qpos - (t_begin + j) * BKV;  // key e of the tile visible iff e <= lim
+        if (lim < BKV - 1) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) o_acc[c * 32 + i] = fmaf(o_acc[c * 32 + i], f, __uint_as_float(v[i]));
+          for (int e = 0; e < BKV; ++e)
+            if (e > lim) sv[e] = __float_as_uint(-INFINITY);
+        }
+        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int e = 0; e < BKV; e += 8)
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            mx4[u] = fmax3(mx4[u], __uint_as_float(sv[e + 2 * u]), __uint_as_float(sv[e + 2 * u + 1]));
+        const float mt = fmax3(fmaxf(mx4[0], mx4[1]), mx4[2], mx4[3]) * sl2;
+        // lazy rescale: move the reference max only when it grew by more than 2^8
+        const bool need = mt > m_used + RESCALE_LOG2;
+        const bool rescale = __any_sync(0xffffffffu, need) && j > 0;
+        float f = 1.f;
+        if (need) {
+          f = ex2_approx(m_used - mt);  // 0 when m_used = -inf
+          l *= f;
+          m_used = mt;
+        }
+        // P = 2^(S*scale - m_used) as bf16 pairs (registers), row sum in fp32; this
+        // overlaps P_i.V(j-1), which still reads the P_i buffer
+        const float nb = m_used == -INFINITY ? 0.f : -m_used;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        uint32_t pk[BKV / 2];
+#pragma unroll
+        for (int k = 0; k < BKV; k += 4) {
+          float x0, x1, x2, x3;
+          ffma2(x0, x1, __uint_as_float(sv[k]), __uint_as_float(sv[k + 1]), sl2, sl2, nb, nb);
+          ffma2(x2, x3, __uint_as_float(sv[k + 2]), __uint_as_float(sv[k + 3]), sl2, sl2, nb, nb);
+          if (((k / 4) * 3) % 8 < EMU_OF_8) {  // this group of 4 on the FMA pipe
+            exp2_emu2(x0, x1, x0, x1);
+            exp2_emu2(x2, x3, x2, x3);
+          } else {  // on the MUFU
+            x0 = ex2_approx(x0);
+            x1 = ex2_approx(x1);
+            x2 = ex2_approx(x2);
+            x3 = ex2_approx(x3);
+          }
+          fadd2(s0, s1, s0, s1, x0, x1);
+          fadd2(s2, s3, s2, s3, x2, x3);
+          pk[k / 2] = pack_bf16(x0, x1);
+          pk[k / 2 + 1] = pack_bf16(x2, x3);
+        }
+        // P_i (and O_i) are free once P_i.V(j-1) has retired (implied by s_full when P aliases S)
+        if (j > 0) {
+          mbar_wait(&o_done[i], (j - 1) & 1);
+          tc_fence_after();
+        }
+#pragma unroll
+        for (int c = 0; c < BKV / 64; ++c) tmem_st32(tP + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[c * 32]));
+        l += (s0 + s1) + (s2 + s3);
+        if (rescale) {  // O_i row *= f before P_i.V(j) accumulates into it
+#pragma unroll
+          for (int c = 0; c < DH / 32; ++c) {
+            uint32_t ov[32];
+            tmem_ld32(tO + c * 32, ov);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+              float a0, a1;
+              fmul2(a0, a1, __uint_as_float(ov[e]), __uint_as_float(ov[e + 1]), f, f);
+              ov[e] = __float_as_uint(a0);
+              ov[e + 1] = __float_as_uint(a1);
+            }
+            tmem_st32(tO + c * 32, ov);
+          }
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[i]);
       }
-      m_acc = m_t;
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&o_empty[b]);
-    };
-
-    for (int j = 0; j < n_tiles; ++j) {
-      const int b = j & 1;
-      mbar_wait(&s_full[b], (j >> 1) & 1);
+      // final O row: wait for the last P.V, normalise, store
+      mbar_wait(&o_done[i], (n_tiles - 1) & 1);
       tc_fence_after();
-      const int kbase = (t_begin + j) * BKV + h * 64;  // first key of this half
-      const int lim0 = kmax - kbase;            // element e visible iff e <= lim0
-      const bool need_mask = lim0 < 63;
-      const uint32_t scol = tS + b * BKV + h * 64 + lane_off;
-      // this half's 64 scores stay in registers for both passes
-      uint32_t va[32], vb[32];
-      tmem_ld32(scol, va);
-      tmem_ld32(scol + 32, vb);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[b]);  // S buffer may be overwritten now
-      if (need_mask) {
+      const bool ok = r < nrows;  // every lane joins the .sync.aligned TMEM loads; valid rows store
+      const long long trow = row_base + i * TPT + (ok ? r : 0) / G;  // token row in [0, T)
+      const int head = kvh * G + (ok ? r : 0) % G;
+      const float inv = l > 0.f ? 1.f / l : 0.f;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          if (i > lim0) va[i] = __float_as_uint(-INFINITY);
-          if (32 + i > lim0) vb[i] = __float_as_uint(-INFINITY);
+      for (int c = 0; c < DH / 32; ++c) {
+        uint32_t ov[32];
+        tmem_ld32(tO + c * 32, ov);
+        tmem_ld_wait();
+        if (!ok) continue;
+        if (p.kv_splits > 1) {
+          // unnormalised partial at scale m_used; combined by attn_split_combine_kernel
+          float4* dst =
+              reinterpret_cast<float4*>(p.split_o + (((long long)ks * p.n_tokens + trow) * p.hq + head) * DH + c * 32);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            dst[e] = make_float4(__uint_as_float(ov[4 * e]), __uint_as_float(ov[4 * e + 1]),
+                                 __uint_as_float(ov[4 * e + 2]), __uint_as_float(ov[4 * e + 3]));
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(p.o + trow * p.ldo + (long long)head * DH + c * 32);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            dst[e] = make_uint4(pack_bf16(__uint_as_float(ov[8 * e]) * inv, __uint_as_float(ov[8 * e + 1]) * inv),
+                                pack_bf16(__uint_as_float(ov[8 * e + 2]) * inv, __uint_as_float(ov[8 * e + 3]) * inv),
+                                pack_bf16(__uint_as_float(ov[8 * e + 4]) * inv, __uint_as_float(ov[8 * e + 5]) * inv),
+                                pack_bf16(__uint_as_float(ov[8 * e + 6]) * inv, __uint_as_float(ov[8 * e + 7]) * inv));
         }
       }
-      // pass 1: raw max (scale > 0 commutes with max), 4 chains
-      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-      for (int i = 0; i < 32; i += 4)
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          m4[u] = fmaxf(m4[u], fmaxf(__uint_as_float(va[i + u]), __uint_as_float(vb[i + u])));
-      const float mine = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-      red[((j & 1) * 2 + h) * ROWS + r] = mine;
-      pair_sync();
-      const float other = red[((j & 1) * 2 + (h ^ 1)) * ROWS + r];
-      const float mx = fmaxf(m_run, fmaxf(mine, other) * sl2);
-      const float nmx = -mx;
-      // pass 2: P = exp2(S*scale - max) -> smem (bf16, swizzled K-major), partial row sum
-      mbar_wait(&p_empty[b], ((j >> 1) & 1) ^ 1);
-      float s4[4] = {0.f, 0.f, 0.f, 0.f};
-      const uint32_t pbase = sb + C::OFF_P + b * C::PB + h * (ROWS * 128) + r * 128;
-      auto emit = [&](const uint32_t(&v)[32], const int c) {
-        uint32_t w[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          // masked scores are -inf: ex2(-inf) = +0
-          const float e0 = ex2_approx(fmaf(__uint_as_float(v[2 * i]), sl2, nmx));
-          const float e1 = ex2_approx(fmaf(__uint_as_float(v[2 * i + 1]), sl2, nmx));
-          s4[i & 3] += e0 + e1;
-          w[i] = pack_bf16(e0, e1);
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int chunk = c * 4 + q;
-          st_shared_v4(pbase + ((chunk ^ (r & 7)) << 4), w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
-        }
-      };
-      emit(va, 0);
-      emit(vb, 1);
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[b]);
-      l = l * ex2_approx(m_run - mx) + ((s4[0] + s4[1]) + (s4[2] + s4[3]));
-      m_run = mx;
-      if (j >= 1) consume(j - 1, m_pend);
-      m_pend = mx;
-    }
-    if (n_tiles > 0) consume(n_tiles - 1, m_pend);
-    // total row sum = both halves; then normalise and store this half of the row
-    // the parity slot the last tile did NOT use is free (its readers passed the last pair_sync)
-    const int fs = n_tiles & 1;
-    red[(fs * 2 + h) * ROWS + r] = l;
-    pair_sync();
-    const float lt = l + red[(fs * 2 + (h ^ 1)) * ROWS + r];
-    if (r < nrows) {
-      const long long trow = row_base + r / G;  // token row in [0, T)
-      const int head = kvh * G + r % G;
-      if (p.kv_splits > 1) {
-        // unnormalised partial at scale m_acc; combined by attn_split_combine_kernel
-        float* dst = p.split_o + (((long long)ks * p.n_tokens + trow) * p.hq + head) * DH + h * OD;
-#pragma unroll
-        for (int c = 0; c < OD / 4; ++c)
-          reinterpret_cast<float4*>(dst)[c] =
-              make_float4(o_acc[4 * c], o_acc[4 * c + 1], o_acc[4 * c + 2], o_acc[4 * c + 3]);
-        if (h == 0) p.split_ml[((long long)ks * p.n_tokens + trow) * p.hq + head] = make_float2(m_acc, lt);
-      } else {
-        const float inv = 1.f / lt;
-        uint4* dst = reinterpret_cast<uint4*>(p.o + trow * p.ldo + (long long)head * DH + h * OD);
-#pragma unroll
-        for (int c = 0; c < OD / 8; ++c)
-          dst[c] = make_uint4(pack_bf16(o_acc[8 * c] * inv, o_acc[8 * c + 1] * inv),
-                              pack_bf16(o_acc[8 * c + 2] * inv, o_acc[8 * c + 3] * inv),
-                              pack_bf16(o_acc[8 * c + 4] * inv, o_acc[8 * c + 5] * inv),
-                              pack_bf16(o_acc[8 * c + 6] * inv, o_acc[8 * c + 7] * inv));
-      }
+      if (ok && p.kv_splits > 1) p.split_ml[((long long)ks * p.n_tokens + trow) * p.hq + head] = make_float2(m_used, l);
+    } else if (p.kv_splits > 1 && n_tiles == 0 && r < nrows) {
+      // empty split: mark the partial as absent
+      const long long trow = row_base + i * TPT + r / G;
+      p.split_ml[((long long)ks * p.n_tokens + trow) * p.hq + kvh * G + r % G] = make_float2(-INFINITY, 0.f);
     }
   }
+  tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 9) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
@@ -419,7 +442,7 @@ int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
   CUtensorMap tk, tv;
   RDKV_TRY(make_tmap(&tk, p.kplane, rows, DH, DH, HALF));
   RDKV_TRY(make_tmap(&tv, p.vplane, rows, DH, DH, HALF));
-  const int tok_per_cta = ROWS / (p.hq / p.hkv);
+  const int tok_per_cta = 2 * ROWS / (p.hq / p.hkv);  // two Q tiles per CTA
   const int qblocks = (max_new + tok_per_cta - 1) / tok_per_cta;
   // split the KV range when the (query block x kv head x sequence) grid is too
   // small for 148 SMs (single-query TTFT) and scratch is available
@@ -434,7 +457,7 @@ int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
     if (k >= 2 && (size_t)k * p.n_tokens * p.hq * (DH * 4 + 8) <= p.split_bytes) q.kv_splits = k;
   }
   dim3 grid(qblocks * q.kv_splits, p.hkv, n_seqs);
-  CUDA_TRY(launch_k(attn_tc_kernel<DH>, grid, dim3(384), C::SMEM, st, tk, tv, q));
+  CUDA_TRY(launch_k(attn_tc_kernel<DH>, grid, dim3(THREADS), C::SMEM, st, tk, tv, q));
   CUDA_TRY(cudaGetLastError());
   if (q.kv_splits > 1) {
     CUDA_TRY(launch_k(attn_split_combine_kernel<DH>, dim3(p.n_tokens, (p.hq + 7) / 8), dim3(256), 0, st, q));
