@@ -156,6 +156,13 @@ RDKV_API int rdkv_kv_unpack(const rdkv_unpack_job* jobs_dev, int n_jobs, int max
                             int layers, int kv_heads, int head_dim, int64_t pool_slots,
                             int elem_width, int layer_begin, int layer_end, void* stream);
 
+/* Copy the first n_tokens slots of pool block src_block into dst_block, in every
+ * (layer, K|V, head) plane: one strided DMA (cudaMemcpy2DAsync, L*2*Hkv rows).
+ * Copy-on-write of a resident prefix's partial last block, so a query can append
+ * its new tokens without touching the shared HBM-tier entry. */
+RDKV_API int rdkv_kv_copy_block(void* pool_base, int layers, int kv_heads, int head_dim, int64_t pool_slots,
+                                int block_size, int src_block, int dst_block, int n_tokens, void* stream);
+
 /* ------------------------------------------------ K2/K4: prefill attention */
 
 /* Causal GQA attention of n_tokens new query rows over each sequence's cached

@@ -345,6 +345,20 @@ int rdkv_profile_collect(rdkv_model* m, double* ms, int64_t* launches, double* f
   return 0;
 }
 
+int rdkv_kv_copy_block(void* pool_base, int layers, int kv_heads, int head_dim, int64_t pool_slots, int block_size,
+                       int src_block, int dst_block, int n_tokens, void* stream) {
+  if (!pool_base || block_size <= 0 || n_tokens < 0 || n_tokens > block_size || src_block < 0 || dst_block < 0 ||
+      (int64_t)(src_block + 1) * block_size > pool_slots || (int64_t)(dst_block + 1) * block_size > pool_slots)
+    return set_error(RDKV_ERR_ARG, "kv_copy_block: bad arguments");
+  if (n_tokens == 0) return 0;
+  const size_t row = (size_t)head_dim * 2, pitch = (size_t)pool_slots * row;
+  auto* base = static_cast<uint8_t*>(pool_base);
+  CUDA_TRY(cudaMemcpy2DAsync(base + (size_t)dst_block * block_size * row, pitch,
+                             base + (size_t)src_block * block_size * row, pitch, (size_t)n_tokens * row,
+                             (size_t)layers * 2 * kv_heads, cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
 int rdkv_kv_unpack(const rdkv_unpack_job* jobs_dev, int n_jobs, int max_tokens, const int32_t* block_table_dev,
                    int block_size, void* pool_base, int layers, int kv_heads, int head_dim, int64_t pool_slots,
                    int elem_width, int layer_begin, int layer_end, void* stream) {

@@ -65,6 +65,8 @@ _N_SIG = {
     "rdkv_forward": (C.c_int, [C.c_void_p, C.POINTER(RdkvBatch), C.c_void_p, C.c_size_t, C.c_void_p]),
     "rdkv_kv_unpack": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int,
                                  C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_void_p]),
+    "rdkv_kv_copy_block": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int,
+                                     C.c_int, C.c_void_p]),
     "rdkv_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
     "rdkv_profile_collect": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                        C.POINTER(C.c_double)]),
@@ -118,7 +120,9 @@ class KvPool:
         return (n_tokens + self.block_size - 1) // self.block_size
 
     def alloc(self, n_tokens: int) -> list[int]:
-        n = self.blocks_for(n_tokens)
+        return self.alloc_blocks(self.blocks_for(n_tokens))
+
+    def alloc_blocks(self, n: int) -> list[int]:
         if n > len(self._free):
             raise MemoryError(f"KV pool exhausted: need {n} blocks, {len(self._free)} free")
         return [self._free.popleft() for _ in range(n)]
@@ -442,41 +446,83 @@ class QueryRequest:
     n_cached: int = 0
 
 
-class DeviceKvCache:
-    """HBM placement cache: KvKey -> device payload, byte-bounded LRU.
+@dataclass
+class ResidentEntry:
+    blocks: list[int]       # pool blocks holding positions [0, n_tokens)
+    n_tokens: int
+    pins: int = 0           # batches currently reading the blocks
+
+
+class ResidentKvTier:
+    """HBM tier: KvKey -> cached prefix KV living *in the paged pool* (block-LRU).
+
+    A hit costs nothing to load: the query's block table starts with the
+    entry's blocks and only its new tokens get fresh blocks (a partial last
+    block is copied on write).  Entries are filled once, by one K3 unpack of
+    the blob payload, when a composite is generated or first streamed in.
 
     Purely a *placement* layer under the store: the logical outcome of every
     access (MEMORY_HIT / DISK_HIT / MISS and its accounting) is still decided
-    by the KvStore; this only changes where the bytes are copied from
-    (SURVEY §8e invariant)."""
+    by the KvStore; this only changes where the bytes come from (SURVEY §8e
+    invariant).  Eviction returns blocks to the pool free list, which is
+    stream-ordered: later writers are enqueued after earlier readers."""
 
-    def __init__(self, capacity_bytes: int) -> None:
-        self.capacity = capacity_bytes
+    def __init__(self, pool: "KvPool", capacity_blocks: int) -> None:
+        self.pool = pool
+        self.capacity = capacity_blocks
         self.used = 0
-        self._d: "OrderedDict" = OrderedDict()
+        self._d: "OrderedDict[object, ResidentEntry]" = OrderedDict()
         self._lock = threading.Lock()
-
-    def get(self, key) -> torch.Tensor | None:
-        with self._lock:
-            t = self._d.get(key)
-            if t is not None:
-                self._d.move_to_end(key)
-            return t
-
-    def put(self, key, t: torch.Tensor) -> None:
-        n = t.numel() * t.element_size()
-        with self._lock:
-            if key in self._d or n > self.capacity:
-                return
-            while self._d and self.used + n > self.capacity:
-                _, old = self._d.popitem(last=False)
-                self.used -= old.numel() * old.element_size()
-            self._d[key] = t
-            self.used += n
 
     def __contains__(self, key) -> bool:
         with self._lock:
             return key in self._d
+
+    def __len__(self) -> int:
+        return len(self._d)
+
+    def acquire(self, key) -> ResidentEntry | None:
+        """Pin and return the entry (MRU), or None."""
+        with self._lock:
+            e = self._d.get(key)
+            if e is not None:
+                self._d.move_to_end(key)
+                e.pins += 1
+            return e
+
+    def unpin(self, key) -> None:
+        with self._lock:
+            e = self._d.get(key)
+            if e is not None and e.pins > 0:
+                e.pins -= 1
+
+    def reserve(self, n_tokens: int) -> list[int] | None:
+        """Blocks for a new entry, evicting unpinned LRU entries; None if it cannot fit."""
+        need = self.pool.blocks_for(n_tokens)
+        with self._lock:
+            if need > self.capacity:
+                return None
+            for k in list(self._d):
+                if self.used + need <= self.capacity:
+                    break
+                e = self._d[k]
+                if e.pins:
+                    continue
+                del self._d[k]
+                self.used -= len(e.blocks)
+                self.pool.release(e.blocks)
+            if self.used + need > self.capacity or need > self.pool.free_blocks:
+                return None
+            self.used += need
+            return self.pool.alloc(n_tokens)
+
+    def commit(self, key, blocks: list[int], n_tokens: int) -> None:
+        with self._lock:
+            old = self._d.pop(key, None)
+            if old is not None:  # lost a race: keep the newer copy
+                self.used -= len(old.blocks)
+                self.pool.release(old.blocks)
+            self._d[key] = ResidentEntry(list(blocks), n_tokens)
 
 
 class Engine:
@@ -484,13 +530,18 @@ class Engine:
 
     def __init__(self, spec: ModelSpec, weights: ModelWeights | None = None, seed: int = 0, device="cuda",
                  pool_tokens: int = 1 << 16, block_size: int = 64, device_cache_bytes: int = 0) -> None:
+        """``pool_tokens`` = working KV slots for in-flight queries; ``device_cache_bytes``
+        = extra pool capacity reserved for the HBM-resident tier of cached prefixes."""
         self.device = torch.device(device)
         self.spec = spec
         self.weights = weights if weights is not None else init_weights(spec, seed, self.device)
         self.model = DeviceModel(self.weights)
-        self.pool = KvPool(spec, (pool_tokens + block_size - 1) // block_size, block_size, self.device)
+        work_blocks = (pool_tokens + block_size - 1) // block_size
+        block_bytes = spec.kv_bytes_per_token() * block_size
+        tier_blocks = device_cache_bytes // block_bytes
+        self.pool = KvPool(spec, work_blocks + tier_blocks, block_size, self.device)
         self.copy_stream = torch.cuda.Stream(device=self.device)
-        self.device_cache = DeviceKvCache(device_cache_bytes)
+        self.resident = ResidentKvTier(self.pool, tier_blocks)
         self.graphs = GraphRunner(self)
         self.streamer = LayerStreamer(self)
 
@@ -500,6 +551,30 @@ class Engine:
         with torch.cuda.stream(stream) if stream is not None else _nullctx():
             dev.copy_(payload, non_blocking=True)
         return dev.view(torch.bfloat16)
+
+    def make_resident(self, key, payload: torch.Tensor, n_tokens: int,
+                      stream: torch.cuda.Stream | None = None) -> bool:
+        """Place a device blob payload [L][2][Hkv][n][dh] into the HBM tier (one K3
+        unpack into freshly reserved pool blocks).  False if it does not fit."""
+        if key in self.resident:
+            return True
+        blocks = self.resident.reserve(n_tokens)
+        if blocks is None:
+            return False
+        bt = torch.tensor(blocks, dtype=torch.int32).pin_memory().to(self.device, non_blocking=True)
+        kv_unpack(self.pool, [(payload, n_tokens, 0)], bt, stream=stream)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        payload.record_stream(s)
+        bt.record_stream(s)
+        self.resident.commit(key, blocks, n_tokens)
+        return True
+
+    def copy_block(self, src_block: int, dst_block: int, n_tokens: int,
+                   stream: torch.cuda.Stream | None = None) -> None:
+        s = self.spec
+        _lib.check(_L().rdkv_kv_copy_block(self.pool.data.data_ptr(), s.layers, s.kv_heads, s.head_dim,
+                                           self.pool.slots, self.pool.block_size, src_block, dst_block, n_tokens,
+                                           _stream_ptr(stream)))
 
     # -------------------------------------------------------------- generation
     def generate_doc_kv(self, tokens: np.ndarray, out: torch.Tensor | None = None,

@@ -10,8 +10,8 @@ A call runs the document prefill over the ordered combination's concatenated
 tokens (positions 0..n-1, prefetch.py:6-8) on the engine's GPU; the payload is
 written by the QKV epilogue directly in the `.rdkv` layout, copied once into
 pinned host memory (the memory tier's DMA-ready form), FNV-1a-hashed natively
-and wrapped without re-hashing.  The device copy stays in the engine's HBM
-placement cache so a query dispatched to the same GPU skips the H2D copy.
+and wrapped without re-hashing.  The KV is also placed in the engine's HBM
+tier (pool blocks) so a query dispatched to the same GPU loads nothing.
 """
 
 from __future__ import annotations
@@ -53,7 +53,8 @@ class KvGenerator:
             torch.cuda.current_stream().synchronize()
         header = make_header(self.profile, ids, len(toks), fnv1a64(host))
         if self.keep_on_device:
-            eng.device_cache.put(KvKey(self.profile.model_hash, ids), kv)
+            with torch.cuda.device(eng.device):
+                eng.make_resident(KvKey(self.profile.model_hash, ids), kv, len(toks))
         return KvBlob.trusted(header, host)
 
     def for_prefix(self, doc_ids: Sequence[int], doc_token_counts: Sequence[int]) -> Callable[[], KvBlob]:

@@ -8,7 +8,8 @@ the query (sim.py:420-422) — are prefilled, attending over the whole context
 the prefill (costs.py:136-138).
 
 Here the load is real (pinned host payload -> HBM on a side stream, then the
-K3 unpack into the paged pool; or straight from the HBM placement cache) and
+K3 unpack into the paged pool; or nothing at all when the prefix is already
+resident in the pool's HBM tier) and
 so is the prefill (tcgen05 GEMMs + attention + LM head).  Both halves are
 timed with CUDA events and returned as the reference's
 ``(seconds, TtftBreakdown(kv_load, prefill))`` plus the first-token logits.
@@ -56,7 +57,8 @@ def prefill_batch(engine: Engine, requests: Sequence[PrefillRequest], timed: boo
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if timed else None
     if timed:
         ev[0].record(main)
-    seqs, owned, jobs, staged, pending_h2d = [], [], [], [], []
+    seqs, owned, jobs, staged, pending_h2d, pinned = [], [], [], [], [], []
+    bs = pool.block_size
     # staging buffers are allocated on `main`; the copy stream must not write
     # them before main's earlier users of that memory are done
     engine.copy_stream.wait_stream(main)
@@ -66,19 +68,34 @@ def prefill_batch(engine: Engine, requests: Sequence[PrefillRequest], timed: boo
             n_cached = int(r.lookup.blob.header.token_count) if hit else 0
             new = np.asarray(r.new_tokens, np.int32) if hit else np.concatenate(
                 [np.asarray(r.prefix_tokens, np.int32), np.asarray(r.new_tokens, np.int32)])
+            entry = engine.resident.acquire(r.key) if hit and r.key is not None else None
+            if entry is not None:
+                # HBM-tier hit: the prefix is already in pool blocks; only the new
+                # tokens get fresh blocks (a partial last block is copied on write)
+                pinned.append(r.key)
+                if entry.n_tokens != n_cached:
+                    raise ValueError("resident entry does not match the lookup's token count")
+                prefix = list(entry.blocks)
+                tail = n_cached % bs
+                fresh = pool.alloc_blocks(pool.blocks_for(n_cached + len(new)) - len(prefix) + (1 if tail else 0))
+                owned.append(fresh)
+                if tail:
+                    engine.copy_block(prefix[-1], fresh[0], tail, stream=main)
+                    prefix[-1] = fresh[0]
+                    fresh = fresh[1:]
+                seqs.append(SeqPlan(new, n_cached, prefix + fresh))
+                continue
             blocks = pool.alloc(n_cached + len(new))
             owned.append(blocks)
             seqs.append(SeqPlan(new, n_cached, blocks))
             if hit:
-                dev = engine.device_cache.get(r.key) if r.key is not None else None
-                if dev is None:
-                    host = r.lookup.blob.payload_tensor()
-                    if stream_layers and not timed:  # copied layer by layer by the streamer
-                        dev = torch.empty(host.numel(), dtype=torch.uint8, device=engine.device).view(torch.bfloat16)
-                        pending_h2d.append((host, dev.view(torch.uint8)))
-                    else:
-                        dev = engine.stage(host, stream=engine.copy_stream)
-                    staged.append(dev)
+                host = r.lookup.blob.payload_tensor()
+                if stream_layers and not timed:  # copied layer by layer by the streamer
+                    dev = torch.empty(host.numel(), dtype=torch.uint8, device=engine.device).view(torch.bfloat16)
+                    pending_h2d.append((host, dev.view(torch.uint8)))
+                else:
+                    dev = engine.stage(host, stream=engine.copy_stream)
+                staged.append(dev)
                 jobs.append((dev, n_cached, i))
         plan = BatchPlan(seqs, pool.block_size, engine.device)
         if staged:
@@ -129,6 +146,8 @@ def prefill_batch(engine: Engine, requests: Sequence[PrefillRequest], timed: boo
     finally:
         for b in owned:
             pool.release(b)
+        for k in pinned:
+            engine.resident.unpin(k)
 
 
 def prefill_with_cached_prefix(engine: Engine, lookup: LookupResult, prefix_tokens, new_tokens,

@@ -140,3 +140,64 @@ def test_graph_replay_matches_eager(setup):
         assert rel_err(gl, e.logits) <= 1e-4
         outs.append(gl)
     assert rel_err(outs[1], outs[2]) > 1e-3  # replays really saw new inputs
+
+
+def test_resident_tier_hit_matches_host_tier_hit():
+    """HBM-tier hits (prefix already in pool blocks, nothing loaded) give the same
+    logits as host-tier hits (H2D + K3 unpack); a partial last block is copied on
+    write, so queries sharing a resident prefix never modify it."""
+    from paper_2504_11765_b200.generator import KvGenerator
+    from paper_2504_11765_b200.prefill import PrefillRequest, prefill_batch
+    from paper_2504_11765_b200.store import KvKey, LookupResult, Outcome
+
+    spec = get_spec("gqa-small-64")
+    per_tok = spec.kv_bytes_per_token()
+    eng = Engine(spec, seed=2, pool_tokens=8192, block_size=64, device_cache_bytes=per_tok * 64 * 16)
+    gen = KvGenerator(eng, keep_on_device=True)
+    prof = spec.profile()
+    combos = [((1, 2), (128, 72)), ((3,), (256,))]          # 200 tokens (ragged tail), 256 (block aligned)
+    keys, blobs = [], []
+    for ids, nt in combos:
+        blobs.append(gen.generate(ids, nt))
+        keys.append(KvKey(prof.model_hash, ids))
+        assert keys[-1] in eng.resident
+    before = [eng.pool.gather(eng.resident.acquire(k).blocks, b.header.token_count).clone() for k, b in zip(keys, blobs)]
+    for k in keys:
+        eng.resident.unpin(k)
+    qs = [query_tokens(70 + i, 33, spec.vocab) for i in range(4)]
+    # two queries per resident prefix in ONE batch
+    idx = [0, 0, 1, 1]
+    res = prefill_batch(eng, [PrefillRequest(LookupResult(Outcome.MEMORY_HIT, blobs[j], 0), None, qs[i], keys[j])
+                              for i, j in enumerate(idx)], timed=False, use_graph=False)
+    host = prefill_batch(eng, [PrefillRequest(LookupResult(Outcome.MEMORY_HIT, blobs[j], 0), None, qs[i], None)
+                               for i, j in enumerate(idx)], timed=False, use_graph=False)
+    torch.cuda.synchronize()
+    assert rel_err(res.logits, host.logits) <= 1e-3
+    assert torch.equal(res.next_token, host.next_token)
+    for k, b, ref in zip(keys, blobs, before):
+        e = eng.resident.acquire(k)
+        assert torch.equal(eng.pool.gather(e.blocks, b.header.token_count), ref)
+        eng.resident.unpin(k)
+    # and against the oracle
+    orc = OracleModel(eng.weights)
+    toks = gen.tokens(*combos[0])
+    _, ref = orc.forward(np.concatenate([toks, qs[0]]))
+    _check_logits(res.logits[0], ref, res.next_token[0])
+
+
+def test_resident_tier_lru_respects_pins():
+    spec = get_spec("gqa-small-64")
+    per_tok = spec.kv_bytes_per_token()
+    eng = Engine(spec, seed=2, pool_tokens=1024, block_size=64, device_cache_bytes=per_tok * 64 * 4)  # 4 blocks
+    pay = lambda n: torch.zeros(spec.layers * 2 * spec.kv_heads * n * spec.head_dim, dtype=torch.bfloat16,
+                                device="cuda")
+    free0 = eng.pool.free_blocks
+    assert eng.make_resident("a", pay(128), 128)      # 2 blocks
+    assert eng.make_resident("b", pay(100), 100)      # 2 blocks (tier full)
+    assert eng.resident.acquire("a") is not None      # pin a (and make it MRU)
+    assert eng.make_resident("c", pay(64), 64)        # evicts b (LRU, unpinned)
+    assert "b" not in eng.resident and "a" in eng.resident and "c" in eng.resident
+    assert not eng.make_resident("d", pay(192), 192)  # 3 blocks: a pinned, cannot fit
+    eng.resident.unpin("a")
+    assert eng.make_resident("d", pay(192), 192)      # now a and c go
+    assert eng.pool.free_blocks == free0 - 3
