@@ -69,10 +69,31 @@ struct TcCfg {
 
 constexpr int THREADS = 384;  // warps 0-3 / 4-7: softmax of Q tile 0 / 1; 8: TMA; 9 / 10: MMA of tile 0 / 1; 11 idle
 constexpr float RESCALE_LOG2 = 8.f;   // lazy O rescale: keep a stale row max until it is 2^8 too small
+#ifndef RDKV_ATTN_TRACE
+#define RDKV_ATTN_TRACE 0  // 1: per-tile clock64 timeline of CTA 0 (debug builds only)
+#endif
+#if RDKV_ATTN_TRACE
+__device__ long long g_attn_trace[4][64][8];
+#define TRACE(who, j, ev) \
+  do { if (blockIdx.x == gridDim.x - 1 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 64) g_attn_trace[who][j][ev] = clock64(); } while (0)
+#else
+#define TRACE(who, j, ev) do { } while (0)
+#endif
 #ifndef RDKV_ATTN_EMU
 #define RDKV_ATTN_EMU 3
 #endif
 constexpr int EMU_OF_8 = RDKV_ATTN_EMU;  // exp2 of this many of every 8 score groups runs as a polynomial
+
+#ifndef RDKV_ATTN_SPIN
+#define RDKV_ATTN_SPIN 1
+#endif
+// MMA issuers spin (prompt wake-up: the issue latency sits on the P -> P.V chain)
+__device__ __forceinline__ void issuer_wait(uint64_t* bar, uint32_t parity) {
+  if (RDKV_ATTN_SPIN)
+    mbar_wait(bar, parity);
+  else
+    mbar_wait_sleep(bar, parity);
+}
 
 // K-major SW128 operand (rows of 128 B, 8-row atoms 1024 B apart)
 __device__ __forceinline__ uint64_t desc_k(uint32_t saddr) { return sdesc_k_sw128(saddr); }
@@ -159,18 +180,24 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
   if (warp == 8) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      const long long row0 = (long long)kvh * (p.head_stride / DH);  // first row of this head in the plane view
-      for (int j = 0; j < n_tiles; ++j) {
-        const int st = j % ST;
-        mbar_wait_sleep(&kv_empty[st], ((j / ST) & 1) ^ 1);
-        int rows[2];
+    // The whole warp walks the tiles: every 32 tiles each lane resolves one
+    // tile's two block-table rows (32 global loads in parallel instead of a
+    // dependent load per tile on the issue path); lane 0 issues the TMA.
+    const long long row0 = (long long)kvh * (p.head_stride / DH);  // first row of this head in the plane view
+    int my_rows[2] = {0, 0};
+    for (int j = 0; j < n_tiles; ++j) {
+      if ((j & 31) == 0 && j + lane < n_tiles) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          int pos = (t_begin + j) * BKV + h * HALF;
-          if (pos >= kv_len) pos = (t_begin + j) * BKV;  // masked half: any valid, finite block
-          rows[h] = (int)(row0 + (long long)bt[pos / p.block_size] * p.block_size + pos % p.block_size);
+          int pos = (t_begin + j + lane) * BKV + h * HALF;
+          if (pos >= kv_len) pos = (t_begin + j + lane) * BKV;  // masked half: any valid, finite block
+          my_rows[h] = (int)(row0 + (long long)bt[pos / p.block_size] * p.block_size + pos % p.block_size);
         }
+      }
+      const int rows[2] = {__shfl_sync(0xffffffffu, my_rows[0], j & 31), __shfl_sync(0xffffffffu, my_rows[1], j & 31)};
+      if (lane == 0) {
+        const int st = j % ST;
+        mbar_wait_sleep(&kv_empty[st], ((j / ST) & 1) ^ 1);
         mbar_arrive_expect_tx(&k_full[st], C::KB);
 #pragma unroll
         for (int c = 0; c < DH / 64; ++c)
@@ -186,6 +213,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             tma_load_2d_nohint(&tmV, &v_full[st], smem + C::OFF_V + st * C::KB + c * (BKV * 128) + h * (HALF * 128),
                                c * 64, rows[h]);
       }
+      __syncwarp();
     }
   } else if (warp == 9 || warp == 10) {
     // ------------------------------------------------------------ MMA issuers
@@ -208,30 +236,32 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         umma_commit(&s_full[i]);
       };
-      mbar_wait_sleep(q_full, 0);
-      mbar_wait_sleep(&k_full[0], 0);
+      issuer_wait(q_full, 0);
+      issuer_wait(&k_full[0], 0);
       tc_fence_after();
       issue_qk(0);
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j % ST;
         const bool more = j + 1 < n_tiles;
         if (!C::ALIAS && more) {  // next S_i while the softmax still works on this tile
-          mbar_wait_sleep(&k_full[(j + 1) % ST], ((j + 1) / ST) & 1);
-          mbar_wait_sleep(&s_empty[i], j & 1);
+          issuer_wait(&k_full[(j + 1) % ST], ((j + 1) / ST) & 1);
+          issuer_wait(&s_empty[i], j & 1);
           tc_fence_after();
           issue_qk(j + 1);
+          TRACE(2 + i, j, 0);
         }
-        mbar_wait_sleep(&v_full[st], (j / ST) & 1);
-        mbar_wait_sleep(&p_full[i], j & 1);
+        issuer_wait(&v_full[st], (j / ST) & 1);
+        issuer_wait(&p_full[i], j & 1);
         tc_fence_after();
         const uint32_t va = sb + C::OFF_V + st * C::KB;
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)  // O_i (+)= P_i . V(j), P_i from TMEM
           umma_bf16_ts(tO, tP + kk * 8, desc_mn(va + kk * 2048, BKV * 128), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
         umma_commit(&o_done[i]);
+        TRACE(2 + i, j, 1);
         umma_commit(&kv_empty[st]);
         if (C::ALIAS && more) {  // S_i overwrites P_i only after the P.V above (issue order)
-          mbar_wait_sleep(&k_full[(j + 1) % ST], ((j + 1) / ST) & 1);
+          issuer_wait(&k_full[(j + 1) % ST], ((j + 1) / ST) & 1);
           tc_fence_after();
           issue_qk(j + 1);
         }
@@ -272,7 +302,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       float m_used = -INFINITY;  // row max the P values and O are scaled to (log2 domain)
       float l = 0.f;             // row sum at scale m_used
       for (int j = 0; j < n_tiles; ++j) {
+        if (quad == 0 && lane == 0) TRACE(i, j, 0);
         mbar_wait(&s_full[i], j & 1);
+        if (quad == 0 && lane == 0) TRACE(i, j, 1);
         tc_fence_after();
         uint32_t sv[BKV];
 #pragma unroll
@@ -294,6 +326,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int u = 0; u < 4; ++u)
             mx4[u] = fmax3(mx4[u], __uint_as_float(sv[e + 2 * u]), __uint_as_float(sv[e + 2 * u + 1]));
         const float mt = fmax3(fmaxf(mx4[0], mx4[1]), mx4[2], mx4[3]) * sl2;
+        if (quad == 0 && lane == 0) TRACE(i, j, 2);
         // lazy rescale: move the reference max only when it grew by more than 2^8
         const bool need = mt > m_used + RESCALE_LOG2;
         const bool rescale = __any_sync(0xffffffffu, need) && j > 0;
@@ -327,6 +360,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           pk[k / 2] = pack_bf16(x0, x1);
           pk[k / 2 + 1] = pack_bf16(x2, x3);
         }
+        if (quad == 0 && lane == 0) TRACE(i, j, 3);
         // P_i (and O_i) are free once P_i.V(j-1) has retired (implied by s_full when P aliases S)
         if (j > 0) {
           mbar_wait(&o_done[i], (j - 1) & 1);
@@ -355,6 +389,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[i]);
+        if (quad == 0 && lane == 0) TRACE(i, j, 4);
       }
       // final O row: wait for the last P.V, normalise, store
       mbar_wait(&o_done[i], (n_tiles - 1) & 1);
@@ -467,6 +502,12 @@ int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
 }
 
 }  // namespace
+
+#if RDKV_ATTN_TRACE
+extern "C" RDKV_API int rdkv_debug_attn_trace(long long* out) {
+  return cudaMemcpyFromSymbol(out, g_attn_trace, sizeof(g_attn_trace)) == cudaSuccess ? 0 : -8;
+}
+#endif
 
 bool attention_tc_supported(const AttnParams& p, int head_dim) {
   const int G = p.hq / p.hkv;
