@@ -349,6 +349,8 @@ def run_ours(a):
         "kv_load": {"unpack_gbps": ach, "hbm_peak_gbs": pk["hbm_gbs"], "unpack_frac": ach / pk["hbm_gbs"],
                     "h2d_gbps_e2e": e2e * comp_bytes / 1e9},
     }
+    if ws > 1:
+        out["peer_fetch"] = _peer_leg(a, eng, keys, comp_bytes, ws, rank, dev)
     if not a.no_extras:
         out.update(_extras(a, eng, gen, spec, items, blobs, keys, qtoks, ws, rank, dev))
     if rank == 0 and ws == 1:
@@ -360,6 +362,42 @@ def run_ours(a):
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def _peer_leg(a, eng, keys, comp_bytes, ws, rank, dev):
+    """K3p over NVLink: every rank pulls the B composites resident in rank
+    (rank+1) % N's HBM tier (CUDA IPC mapping of the peer pool), a.steps times;
+    device time, max over ranks.  Bytes = composite payloads moved."""
+    from paper_2504_11765_b200.multi import PeerPools, ResidentDirectory
+
+    peers = PeerPools(eng)
+    directory = ResidentDirectory.exchange(eng)
+    src = (rank + 1) % ws
+    theirs = [directory.entry(k) for k in directory.where if directory.holder(k) == src]
+    pool = eng.pool
+    n_blocks = sum(len(b) for _, b, _ in theirs)
+    dst = pool.alloc_blocks(n_blocks)
+    try:
+        src_blocks = [blk for _, b, _ in theirs for blk in b]
+        for _ in range(2):
+            peers.gather(src, src_blocks, dst)
+        torch.cuda.synchronize()
+        _barrier(ws)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.steps):
+            peers.gather(src, src_blocks, dst)
+        e1.record()
+        torch.cuda.synchronize()
+        t = _max_over_ranks(e0.elapsed_time(e1) / 1e3, ws, dev)
+        _barrier(ws)  # holders keep their entries until every rank has pulled
+        nbytes = n_blocks * pool.block_size * eng.spec.kv_bytes_per_token()
+        return {"gbps_per_gpu": nbytes * a.steps / t / 1e9, "bytes_per_step_per_gpu": nbytes,
+                "composites_per_step_per_gpu": len(theirs), "from": "rank+1 (CUDA IPC, NVLink P2P loads)",
+                "nvlink_peak_gbs_per_direction": 900.0}
+    finally:
+        pool.release(dst)
+        peers.close()
 
 
 def _time_unpack(eng, blobs, steps):

@@ -163,6 +163,26 @@ RDKV_API int rdkv_kv_unpack(const rdkv_unpack_job* jobs_dev, int n_jobs, int max
 RDKV_API int rdkv_kv_copy_block(void* pool_base, int layers, int kv_heads, int head_dim, int64_t pool_slots,
                                 int block_size, int src_block, int dst_block, int n_tokens, void* stream);
 
+/* --------------------------- multi-instance sharing: peer HBM tier (K3p) */
+
+/* CUDA IPC handle (64 bytes) of the device allocation containing dev_ptr, and
+ * dev_ptr's byte offset inside it, so a peer process can map this rank's KV
+ * pool.  Replaces nothing in the reference: its instances share KV only via the
+ * filesystem / TCP (store.py, service.py:143-414); SURVEY §8e. */
+RDKV_API int rdkv_ipc_handle(const void* dev_ptr, void* handle_out, int64_t* offset_out);
+/* Map a peer's allocation (peer access enabled lazily); *base_out is its base. */
+RDKV_API int rdkv_ipc_open(const void* handle, void** base_out);
+RDKV_API int rdkv_ipc_close(void* base);
+
+/* K3p: copy n_blocks KV blocks src_blocks[i] of pool src (possibly a peer's,
+ * through rdkv_ipc_open) into dst_blocks[i] of the local pool dst, every
+ * (layer, K|V, head) plane.  Pools are [L][2][Hkv][slots][dh] bf16; block
+ * index arrays are device int32.  Bytes moved = payload of the blocks (NVLink
+ * read + HBM write). */
+RDKV_API int rdkv_kv_peer_gather(const void* src_pool, int64_t src_slots, const int32_t* src_blocks,
+                                 void* dst_pool, int64_t dst_slots, const int32_t* dst_blocks, int n_blocks,
+                                 int layers, int kv_heads, int head_dim, int block_size, void* stream);
+
 /* ------------------------------------------------ K2/K4: prefill attention */
 
 /* Causal GQA attention of n_tokens new query rows over each sequence's cached

@@ -67,6 +67,11 @@ _N_SIG = {
                                  C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_void_p]),
     "rdkv_kv_copy_block": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int,
                                      C.c_int, C.c_void_p]),
+    "rdkv_ipc_handle": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),
+    "rdkv_ipc_open": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "rdkv_ipc_close": (C.c_int, [C.c_void_p]),
+    "rdkv_kv_peer_gather": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int,
+                                      C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]),
     "rdkv_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
     "rdkv_profile_collect": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                        C.POINTER(C.c_double)]),
@@ -480,6 +485,10 @@ class ResidentKvTier:
 
     def __len__(self) -> int:
         return len(self._d)
+
+    def items(self) -> list:
+        with self._lock:
+            return list(self._d.items())
 
     def acquire(self, key) -> ResidentEntry | None:
         """Pin and return the entry (MRU), or None."""

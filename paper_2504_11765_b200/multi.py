@@ -67,6 +67,119 @@ class PeerDirectory:
         return self.where.get(key)
 
 
+class ResidentDirectory:
+    """Which rank holds which key in its HBM tier, and in which pool blocks.
+
+    Built by an all-gather of (key, blocks, n_tokens) over a process group
+    (gloo or nccl object collective: metadata only).  It is a snapshot: the
+    holders must not evict the listed entries until the fetch phase that
+    uses it has ended (``PeerPools.fetch`` callers bracket it with barriers)."""
+
+    def __init__(self, holdings: Sequence[Sequence[tuple]]) -> None:
+        self.where: dict[KvKey, tuple[int, list[int], int]] = {}
+        for r, entries in enumerate(holdings):
+            for key, blocks, n in entries:
+                self.where.setdefault(key, (r, list(blocks), int(n)))
+
+    @classmethod
+    def exchange(cls, engine, group=None) -> "ResidentDirectory":
+        import torch.distributed as dist
+
+        torch.cuda.synchronize(engine.device)  # the listed blocks are fully written before anyone reads them
+        mine = [((k.model_hash, k.doc_ids), e.blocks, e.n_tokens) for k, e in engine.resident.items()
+                if isinstance(k, KvKey)]
+        out: list = [None] * dist.get_world_size(group)
+        dist.all_gather_object(out, mine, group=group)
+        return cls([[(KvKey(m, ids), b, n) for (m, ids), b, n in lst] for lst in out])
+
+    def holder(self, key: KvKey) -> int | None:
+        hit = self.where.get(key)
+        return hit[0] if hit else None
+
+    def entry(self, key: KvKey):
+        return self.where.get(key)
+
+
+class PeerPools:
+    """Every rank's paged KV pool mapped into this process (CUDA IPC), so K3p
+    (``rdkv_kv_peer_gather``) can read a peer's HBM-tier blocks over NVLink."""
+
+    def __init__(self, engine, group=None) -> None:
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        from . import _lib
+        from .engine import _L
+
+        self.engine = engine
+        lib = _L()
+        pool = engine.pool
+        h = (C.c_ubyte * 64)()
+        off = C.c_int64()
+        _lib.check(lib.rdkv_ipc_handle(C.c_void_p(pool.data.data_ptr()), h, C.byref(off)))
+        info = (bytes(h), int(off.value), int(pool.slots))
+        world = dist.get_world_size(group)
+        me = dist.get_rank(group)
+        allinfo: list = [None] * world
+        dist.all_gather_object(allinfo, info, group=group)
+        self.ptr: dict[int, int] = {}
+        self.slots: dict[int, int] = {}
+        self._opened: list[int] = []
+        for r, (hb, o, slots) in enumerate(allinfo):
+            self.slots[r] = slots
+            if r == me:
+                self.ptr[r] = pool.data.data_ptr()
+                continue
+            base = C.c_void_p()
+            _lib.check(lib.rdkv_ipc_open((C.c_ubyte * 64).from_buffer_copy(hb), C.byref(base)))
+            self._opened.append(base.value)
+            self.ptr[r] = base.value + o
+
+    def close(self) -> None:
+        from .engine import _L
+
+        for b in self._opened:
+            _L().rdkv_ipc_close(b)
+        self._opened = []
+
+    def gather(self, src_rank: int, src_blocks: Sequence[int], dst_blocks: Sequence[int],
+               stream: torch.cuda.Stream | None = None) -> None:
+        """K3p: copy blocks from rank ``src_rank``'s pool into this rank's pool."""
+        from . import _lib
+        from .engine import _L, _stream_ptr
+
+        eng, s = self.engine, self.engine.spec
+        dev = eng.device
+        sb = torch.tensor(list(src_blocks), dtype=torch.int32).pin_memory().to(dev, non_blocking=True)
+        db = torch.tensor(list(dst_blocks), dtype=torch.int32).pin_memory().to(dev, non_blocking=True)
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        _lib.check(_L().rdkv_kv_peer_gather(self.ptr[src_rank], self.slots[src_rank], sb.data_ptr(),
+                                            eng.pool.data.data_ptr(), eng.pool.slots, db.data_ptr(), len(db),
+                                            s.layers, s.kv_heads, s.head_dim, eng.pool.block_size,
+                                            _stream_ptr(st)))
+        sb.record_stream(st)
+        db.record_stream(st)
+
+    def fetch(self, directory: ResidentDirectory, key: KvKey, stream: torch.cuda.Stream | None = None) -> bool:
+        """Place ``key`` in this rank's HBM tier from the peer that holds it
+        (False if no peer holds it or it does not fit).  The store still
+        decides the logical outcome of the access; this only moves bytes."""
+        hit = directory.entry(key)
+        if hit is None:
+            return False
+        rank, src_blocks, n = hit
+        eng = self.engine
+        if key in eng.resident:
+            return True
+        dst = eng.resident.reserve(n)
+        if dst is None:
+            return False
+        self.gather(rank, src_blocks, dst, stream)
+        eng.resident.commit(key, dst, n)
+        return True
+
+
 def peer_fetch(src: torch.Tensor, device: torch.device, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
     """Copy a payload resident on a peer GPU into ``device``'s HBM over NVLink
     (cudaMemcpyPeerAsync under the hood when peer access is enabled)."""
