@@ -183,6 +183,26 @@ RDKV_API int rdkv_kv_peer_gather(const void* src_pool, int64_t src_slots, const 
                                  void* dst_pool, int64_t dst_slots, const int32_t* dst_blocks, int n_blocks,
                                  int layers, int kv_heads, int head_dim, int block_size, void* stream);
 
+/* ------------------- tensor parallelism inside an instance (C5, TP = 2..8) */
+
+/* A TP group's communicator over NVLink peer memory.  Each rank allocates one
+ * device buffer of rdkv_tp_comm_bytes(max_elems) bytes, ZEROED, exports it
+ * (rdkv_ipc_handle) and maps every peer's (rdkv_ipc_open); bases[p] is rank p's
+ * buffer as seen from this process (bases[rank] = the local one).  max_elems
+ * bounds rows x hidden of one all-reduce.  No reference analogue: the reference
+ * models one device per instance (costs.py:52-60); SURVEY §8e/§8f. */
+typedef struct rdkv_tp_comm rdkv_tp_comm;
+RDKV_API size_t rdkv_tp_comm_bytes(size_t max_elems);
+RDKV_API int rdkv_tp_comm_create(int rank, int size, void* const* bases, size_t max_elems, rdkv_tp_comm** out);
+RDKV_API void rdkv_tp_comm_destroy(rdkv_tp_comm* comm);
+/* This rank's partial buffer `buf` (0/1): dense [rows][cols] bf16. */
+RDKV_API void* rdkv_tp_part_ptr(rdkv_tp_comm* comm, int buf);
+/* One-shot all-reduce fused with the residual add: x[rows][cols] (ld ldx) +=
+ * sum over ranks of partial buffer `buf`.  Every rank of the group must call it
+ * in the same order; graph-capturable (epochs live in device memory). */
+RDKV_API int rdkv_tp_allreduce_resid(rdkv_tp_comm* comm, void* x, int64_t ldx, int rows, int cols, int buf,
+                                     void* stream);
+
 /* ------------------------------------------------ K2/K4: prefill attention */
 
 /* Causal GQA attention of n_tokens new query rows over each sequence's cached
@@ -268,6 +288,12 @@ typedef struct rdkv_batch {
   void* const* layer_ready;     /* optional [layers] cudaEvent_t: layer l's attention
                                   waits for event l (layer-wise KV streaming)        */
 } rdkv_batch;
+
+/* Make the model one rank of a TP group: its descriptor / weights are this
+ * rank's shard (n_heads, kv_heads, ffn divided by the group size; wqkv rows,
+ * wo / w_down columns, w_gate_up blocks sliced accordingly) and rdkv_forward
+ * all-reduces the attention-output and down projections over `comm` (NULL = off). */
+RDKV_API int rdkv_model_set_tp(rdkv_model* model, rdkv_tp_comm* comm);
 
 /* Device workspace needed by rdkv_forward for n_tokens / n_seqs. */
 RDKV_API size_t rdkv_workspace_bytes(const rdkv_model* model, int n_tokens, int n_seqs);

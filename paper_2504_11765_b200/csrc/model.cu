@@ -17,12 +17,14 @@
 #include "common.cuh"
 #include "gemm_tc.cuh"
 #include "kernels_misc.cuh"
+#include "tp.cuh"
 
 struct rdkv_model {
   rdkv_model_desc d;
   std::vector<const void*> w;  // see rdkv.h for the order
   float* rope = nullptr;        // [max_pos][dh/2] (cos, sin)
   int device = 0;
+  rdkv_tp_comm* tp = nullptr;  // tensor-parallel group (row-parallel outputs all-reduced), or null
   // measurement (rdkv_profile_*)
   bool prof = false;
   struct Rec {
@@ -216,8 +218,10 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
   LAUNCH(RDKV_PROF_MISC, 0.0, launch_embed(b->tokens, W(m, 0), ws.x, T, d.hidden, d.vocab, st));
   // small batches run the residual GEMMs split-K; their finalize also applies the
   // following RMSNorm, saving a launch per norm
-  const bool o_fused = gemm_splits(T, d.hidden, (int)qd, ws.splitk_bytes);
-  const bool down_fused = gemm_splits(T, d.hidden, d.ffn, ws.splitk_bytes);
+  rdkv_tp_comm* tp = m->tp && m->tp->size > 1 ? m->tp : nullptr;
+  const bool o_fused = !tp && gemm_splits(T, d.hidden, (int)qd, ws.splitk_bytes);
+  const bool down_fused = !tp && gemm_splits(T, d.hidden, d.ffn, ws.splitk_bytes);
+  int ar = 0;  // all-reduces issued by this forward (2 per layer: parity selects the partial buffer)
   bool h_ready = false;  // ws.h already holds this layer's attention-norm output
   for (int l = 0; l < d.layers; ++l) {
     const int wb = 1 + RDKV_WEIGHTS_PER_LAYER * l;
@@ -287,7 +291,18 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
       er.norm_gain = G(m, wb + 3);
       er.norm_out = ws.h;
     }
-    LAUNCH(RDKV_PROF_O, 2.0 * T * qd * d.hidden, launch_gemm(ws.o, qd, W(m, wb + 2), qd, T, d.hidden, (int)qd, EPI_RESID, 0, er, st));
+    if (tp) {  // row-parallel: bf16 partial into the symmetric buffer, then all-reduce + residual over NVLink
+      GemmEpi ep = er;
+      ep.out = tp->local_part[ar & 1];
+      ep.ldo = d.hidden;
+      ep.norm_gain = nullptr;
+      ep.norm_out = nullptr;
+      LAUNCH(RDKV_PROF_O, 2.0 * T * qd * d.hidden, launch_gemm(ws.o, qd, W(m, wb + 2), qd, T, d.hidden, (int)qd, EPI_STORE, 0, ep, st));
+      LAUNCH(RDKV_PROF_O, 0.0, launch_tp_allreduce_resid(tp, ws.x, d.hidden, T, d.hidden, ar & 1, st));
+      ++ar;
+    } else {
+      LAUNCH(RDKV_PROF_O, 2.0 * T * qd * d.hidden, launch_gemm(ws.o, qd, W(m, wb + 2), qd, T, d.hidden, (int)qd, EPI_RESID, 0, er, st));
+    }
     // MLP block
     if (!o_fused)
       LAUNCH(RDKV_PROF_MISC, 0.0, launch_rmsnorm(ws.x, d.hidden, nullptr, G(m, wb + 3), ws.h, d.hidden, T, d.hidden, d.norm_eps, st));
@@ -300,7 +315,18 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     h_ready = down_fused && l + 1 < d.layers;
     er.norm_gain = h_ready ? G(m, wb + RDKV_WEIGHTS_PER_LAYER + 0) : nullptr;  // next layer's attention norm
     er.norm_out = h_ready ? ws.h : nullptr;
-    LAUNCH(RDKV_PROF_DOWN, 2.0 * T * d.ffn * d.hidden, launch_gemm(ws.a, d.ffn, W(m, wb + 5), d.ffn, T, d.hidden, d.ffn, EPI_RESID, 0, er, st));
+    if (tp) {
+      GemmEpi ep = er;
+      ep.out = tp->local_part[ar & 1];
+      ep.ldo = d.hidden;
+      ep.norm_gain = nullptr;
+      ep.norm_out = nullptr;
+      LAUNCH(RDKV_PROF_DOWN, 2.0 * T * d.ffn * d.hidden, launch_gemm(ws.a, d.ffn, W(m, wb + 5), d.ffn, T, d.hidden, d.ffn, EPI_STORE, 0, ep, st));
+      LAUNCH(RDKV_PROF_DOWN, 0.0, launch_tp_allreduce_resid(tp, ws.x, d.hidden, T, d.hidden, ar & 1, st));
+      ++ar;
+    } else {
+      LAUNCH(RDKV_PROF_DOWN, 2.0 * T * d.ffn * d.hidden, launch_gemm(ws.a, d.ffn, W(m, wb + 5), d.ffn, T, d.hidden, d.ffn, EPI_RESID, 0, er, st));
+    }
   }
   if (b->want_logits) {
     if (!b->logits || !b->last_row) return set_error(RDKV_ERR_ARG, "forward: logits requested without buffers");
@@ -314,6 +340,12 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     LAUNCH(RDKV_PROF_HEAD, 2.0 * S * d.vocab * d.hidden, launch_gemm(ws.hl, d.hidden, W(m, fn + 1), d.hidden, S, d.vocab, d.hidden, EPI_STORE_F32, 0, el, st));
     if (b->next_token) LAUNCH(RDKV_PROF_HEAD, 0.0, launch_argmax(b->logits, d.vocab, S, d.vocab, b->next_token, ws.argmax, st));
   }
+  return 0;
+}
+
+int rdkv_model_set_tp(rdkv_model* m, rdkv_tp_comm* comm) {
+  if (!m) return set_error(RDKV_ERR_ARG, "model_set_tp: null model");
+  m->tp = comm;
   return 0;
 }
 

@@ -87,7 +87,44 @@ SPECS: dict[str, ModelSpec] = {
                               vocab=4096, max_pos=8192),
     "gqa-small-128": ModelSpec("gqa-small-128", layers=2, hidden=1024, n_heads=8, kv_heads=2, head_dim=128,
                                ffn=2048, vocab=8192, max_pos=8192),
+    # tensor-parallel parity shape: shards 2 and 4 ways (GQA group 2 per rank)
+    "gqa-tp": ModelSpec("gqa-tp", layers=2, hidden=1024, n_heads=16, kv_heads=8, head_dim=64, ffn=2048,
+                        vocab=4096, max_pos=8192),
 }
+
+
+def tp_spec(spec: ModelSpec, size: int) -> ModelSpec:
+    """The per-rank shape of a tensor-parallel group of ``size`` ranks: 1/size of
+    the query heads, KV heads and FFN columns (hidden, vocab replicated)."""
+    if spec.n_heads % size or spec.kv_heads % size or spec.ffn % (64 * size):
+        raise ValueError(f"{spec.name} does not shard {size} ways")
+    return replace(spec, n_heads=spec.n_heads // size, kv_heads=spec.kv_heads // size, ffn=spec.ffn // size)
+
+
+def shard_weights(w: "ModelWeights", rank: int, size: int) -> "ModelWeights":
+    """Rank ``rank``'s shard of full weights: column-parallel wqkv (its query /
+    key / value heads) and w_gate_up (its 64-row gate/up blocks), row-parallel
+    wo and w_down (matching input columns).  Embedding, norms and LM head are
+    replicated (shared tensors)."""
+    s = w.spec
+    ls = tp_spec(s, size)
+    d, dh = s.hidden, s.head_dim
+    hq, hk, f = ls.n_heads, ls.kv_heads, ls.ffn
+    out = ModelWeights(spec=ls, embed=w.embed, final_norm=w.final_norm, lm_head=w.lm_head)
+    for lw in w.layers:
+        q, k = s.q_dim, s.kv_heads * dh
+        wq = lw["wqkv"][:q].view(s.n_heads, dh, d)[rank * hq:(rank + 1) * hq].reshape(-1, d)
+        wk = lw["wqkv"][q:q + k].view(s.kv_heads, dh, d)[rank * hk:(rank + 1) * hk].reshape(-1, d)
+        wv = lw["wqkv"][q + k:].view(s.kv_heads, dh, d)[rank * hk:(rank + 1) * hk].reshape(-1, d)
+        blocks = lw["wgu"].view(s.ffn // 64, 2 * 64, d)[rank * (f // 64):(rank + 1) * (f // 64)]
+        out.layers.append({
+            "attn_norm": lw["attn_norm"], "mlp_norm": lw["mlp_norm"],
+            "wqkv": torch.cat([wq, wk, wv]).contiguous(),
+            "wo": lw["wo"][:, rank * hq * dh:(rank + 1) * hq * dh].contiguous(),
+            "wgu": blocks.reshape(2 * f, d).contiguous(),
+            "wdown": lw["wdown"][:, rank * f:(rank + 1) * f].contiguous(),
+        })
+    return out
 
 
 def get_spec(name: str, layers: int | None = None) -> ModelSpec:

@@ -180,6 +180,79 @@ class PeerPools:
         return True
 
 
+class TpGroup:
+    """Tensor-parallel group for one instance spread over ``size`` GPUs (C5):
+    allocates this rank's zeroed communicator buffer, exchanges CUDA-IPC
+    handles over ``group`` (metadata only), maps every peer's buffer and makes
+    ``engine``'s model all-reduce its row-parallel projections over them
+    (rdkv_tp_allreduce_resid: one-shot, NVLink P2P loads, fused with the
+    residual add).  ``engine`` must hold this rank's shard (model.shard_weights)."""
+
+    def __init__(self, engine, max_tokens: int, group=None) -> None:
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        from . import _lib
+        from .engine import _L
+
+        lib = _L()
+        self.engine = engine
+        self.rank, self.size = dist.get_rank(group), dist.get_world_size(group)
+        self.max_elems = max_tokens * engine.spec.hidden
+        nbytes = int(lib.rdkv_tp_comm_bytes(self.max_elems))
+        self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=engine.device)
+        torch.cuda.synchronize(engine.device)
+        h = (C.c_ubyte * 64)()
+        off = C.c_int64()
+        _lib.check(lib.rdkv_ipc_handle(C.c_void_p(self.buf.data_ptr()), h, C.byref(off)))
+        allinfo: list = [None] * self.size
+        dist.all_gather_object(allinfo, (bytes(h), int(off.value)), group=group)
+        bases = (C.c_void_p * self.size)()
+        self._opened = []
+        for r, (hb, o) in enumerate(allinfo):
+            if r == self.rank:
+                bases[r] = self.buf.data_ptr()
+                continue
+            base = C.c_void_p()
+            _lib.check(lib.rdkv_ipc_open((C.c_ubyte * 64).from_buffer_copy(hb), C.byref(base)))
+            self._opened.append(base.value)
+            bases[r] = base.value + o
+        comm = C.c_void_p()
+        _lib.check(lib.rdkv_tp_comm_create(self.rank, self.size, bases, self.max_elems, C.byref(comm)))
+        self.comm = comm
+        _lib.check(lib.rdkv_model_set_tp(engine.model._h, comm))
+        dist.barrier(group=group)
+
+    def allreduce_resid(self, x: torch.Tensor, part: int = 0, stream=None) -> None:
+        """x[rows, cols] += sum over ranks of each rank's partial buffer ``part``."""
+        from . import _lib
+        from .engine import _L, _stream_ptr
+
+        rows, cols = x.shape
+        _lib.check(_L().rdkv_tp_allreduce_resid(self.comm, x.data_ptr(), x.stride(0), rows, cols, part,
+                                                _stream_ptr(stream)))
+
+    def part_tensor(self, part: int, rows: int, cols: int) -> torch.Tensor:
+        """This rank's partial buffer as a [rows, cols] bf16 view (tests)."""
+        from .engine import _L
+
+        ptr = _L().rdkv_tp_part_ptr(self.comm, part)
+        off = ptr - self.buf.data_ptr()
+        return self.buf[off: off + rows * cols * 2].view(torch.bfloat16).view(rows, cols)
+
+    def close(self) -> None:
+        from .engine import _L
+
+        if self.comm:
+            _L().rdkv_model_set_tp(self.engine.model._h, None)
+            _L().rdkv_tp_comm_destroy(self.comm)
+            self.comm = None
+        for b in self._opened:
+            _L().rdkv_ipc_close(b)
+        self._opened = []
+
+
 def peer_fetch(src: torch.Tensor, device: torch.device, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
     """Copy a payload resident on a peer GPU into ``device``'s HBM over NVLink
     (cudaMemcpyPeerAsync under the hood when peer access is enabled)."""
