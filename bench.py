@@ -312,7 +312,9 @@ def run_ours(a):
 
     # ---------------- roofline: every kernel, headline = the dominant one
     pk = _peaks()
-    tensor_peak = pk["bf16_sus"] or pk["bf16"]
+    # the step is ~5 ms of short kernels: the burst figure applies (the sustained one is a
+    # 4-s back-to-back matmul under the power cap, which our GEMMs exceed inside the step)
+    tensor_peak = pk["bf16"]
     kernels = {}
     for name, c in classes.items():
         if c["ms"] <= 0:
@@ -330,7 +332,8 @@ def run_ours(a):
     kd = kernels[dom]
     roof = {"kernel": dom, "bound": kd["bound"], "achieved": kd["achieved"], "peak": kd["peak"], "unit": kd["unit"],
             "frac": kd["frac"], "share_of_step": kd["ms_per_step"] / (t_prof / a.steps * 1e3),
-            "peak_source": pk["src"] + (" sustained" if kd["bound"] == "tensor" else " copy"),
+            "peak_source": pk["src"] + (" burst bf16" if kd["bound"] == "tensor" else " copy"),
+            "sustained_frac": kd["achieved"] / pk["bf16_sus"] if kd["bound"] == "tensor" and pk["bf16_sus"] else None,
             "traffic": _traffic_from_profiles(dom)}
     launches = sum(v["launches"] for v in classes.values())
     kernels["kv_unpack"] = k3
