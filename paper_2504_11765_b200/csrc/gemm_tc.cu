@@ -20,6 +20,9 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
+// warps 0 TMA, 1 MMA, 2 TMEM, 3 idle, 4-7 and 8-11: two epilogue warpgroups that
+// split each tile's columns (a single-wave GEMM cannot hide its epilogue)
+constexpr int GEMM_THREADS = 384;
 
 template <int BN>
 struct GemmCfg {
@@ -45,13 +48,16 @@ __device__ __forceinline__ void st_bf16x32(__nv_bfloat16* dst, const uint32_t (&
 template <int DH>
 __device__ __forceinline__ void qkv_head_out(float (&v)[DH], int g, int row, int p, int sl, const GemmEpi& ep) {
   if (g < ep.hq + ep.hkv) {
-    const float2* cs = reinterpret_cast<const float2*>(ep.rope) + (long long)p * (DH / 2);
+    // the position's (cos, sin) row is DH contiguous floats: 16-B loads, two pairs each
+    const float4* cs = reinterpret_cast<const float4*>(ep.rope + (long long)p * DH);
 #pragma unroll
-    for (int i = 0; i < DH / 2; ++i) {
-      const float2 t = cs[i];
-      const float x1 = v[i], x2 = v[i + DH / 2];
-      v[i] = x1 * t.x - x2 * t.y;
-      v[i + DH / 2] = x2 * t.x + x1 * t.y;
+    for (int i = 0; i < DH / 4; ++i) {
+      const float4 t = cs[i];
+      const float a1 = v[2 * i], a2 = v[2 * i + DH / 2], b1 = v[2 * i + 1], b2 = v[2 * i + 1 + DH / 2];
+      v[2 * i] = a1 * t.x - a2 * t.y;
+      v[2 * i + DH / 2] = a2 * t.x + a1 * t.y;
+      v[2 * i + 1] = b1 * t.z - b2 * t.w;
+      v[2 * i + 1 + DH / 2] = b2 * t.z + b1 * t.w;
     }
   }
   __nv_bfloat16* dst;
@@ -74,12 +80,12 @@ __device__ __forceinline__ void qkv_head_out(float (&v)[DH], int g, int row, int
 // (its TMEM lane), `taddr` the tile's TMEM address for this warp's lane quadrant.
 template <int BN, int EPI, int DH>
 __device__ __forceinline__ void epilogue_rows(uint32_t taddr, int row, int nb, int sp, int M, int N,
-                                              const GemmEpi& ep) {
+                                              const GemmEpi& ep, int half) {
   const bool row_ok = row < M;
 
   if constexpr (EPI == EPI_STORE || EPI == EPI_STORE_F32 || EPI == EPI_RESID || EPI == EPI_PARTIAL) {
 #pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
+    for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
       uint32_t r[32];
       tmem_ld32(taddr + c * 32, r);
       tmem_ld_wait();
@@ -119,13 +125,13 @@ __device__ __forceinline__ void epilogue_rows(uint32_t taddr, int row, int nb, i
   } else if constexpr (EPI == EPI_SWIGLU) {
     // weights interleaved in 64-row blocks: tile column block 2i = gate, 2i+1 = up
 #pragma unroll 1
-    for (int c = 0; c < BN / 64; ++c) {
-      const int pb = c >> 1, half = c & 1;
+    for (int c = half * (BN / 128); c < (half + 1) * (BN / 128); ++c) {
+      const int pb = c >> 1, hf = c & 1;
       uint32_t g[32], v[32];
-      tmem_ld32(taddr + pb * 128 + half * 32, g);
-      tmem_ld32(taddr + pb * 128 + 64 + half * 32, v);
+      tmem_ld32(taddr + pb * 128 + hf * 32, g);
+      tmem_ld32(taddr + pb * 128 + 64 + hf * 32, v);
       tmem_ld_wait();
-      const int col = nb * (BN / 2) + pb * 64 + half * 32;  // output column
+      const int col = nb * (BN / 2) + pb * 64 + hf * 32;  // output column
       if (row_ok && col < N / 2) {
         uint32_t w[16];
 #pragma unroll
@@ -141,8 +147,9 @@ __device__ __forceinline__ void epilogue_rows(uint32_t taddr, int row, int nb, i
     static_assert(BN % DH == 0, "tile must hold whole heads");
     const int p = row_ok ? ep.pos[row] : 0;
     const int sl = row_ok ? ep.slot[row] : 0;
+    constexpr int HEADS = BN / DH, PER = HEADS > 1 ? HEADS / 2 : 1;
 #pragma unroll 1
-    for (int hh = 0; hh < BN / DH; ++hh) {
+    for (int hh = half * PER; hh < (half + 1) * PER && hh < HEADS; ++hh) {
       float v[DH];
 #pragma unroll
       for (int c = 0; c < DH / 32; ++c) {
@@ -160,7 +167,7 @@ __device__ __forceinline__ void epilogue_rows(uint32_t taddr, int row, int nb, i
 }
 
 template <int BN, int EPI, int DH>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         int M, int N, int K, int splits, GemmEpi ep) {
   using C = GemmCfg<BN>;
@@ -202,7 +209,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], 8);  // 2 epilogue warpgroups x 4 warps
     }
     fence_barrier_init();
   }
@@ -280,7 +287,7 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_after();
       const int row = mb * BM + wq * 32 + lane;
       const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(wq * 32) << 16);
-      epilogue_rows<BN, EPI, DH>(taddr, row, nb, sp, M, N, ep);
+      epilogue_rows<BN, EPI, DH>(taddr, row, nb, sp, M, N, ep, (warp - 4) >> 2);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -310,7 +317,7 @@ struct PairCfg {
 };
 
 template <int BN, int EPI, int DH>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
                          int N, int K, GemmEpi ep) {
   using C = PairCfg<BN>;
@@ -344,7 +351,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);  // 4 epilogue warps in each CTA of the pair
+      mbar_init(&tempty[a], 16);  // 2 epilogue warpgroups x 4 warps in each CTA of the pair
     }
     fence_barrier_init();
   }
@@ -415,7 +422,7 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_after();
       const int row = mb * 256 + (int)rank * 128 + wq * 32 + lane;
       const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(wq * 32) << 16);
-      epilogue_rows<BN, EPI, DH>(taddr, row, nb, 0, M, N, ep);
+      epilogue_rows<BN, EPI, DH>(taddr, row, nb, 0, M, N, ep, (warp - 4) >> 2);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(acc ? tempty1 : tempty0);
@@ -446,7 +453,7 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int 
   const int pairs = units < max_pairs ? units : max_pairs;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * pairs);
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(GEMM_THREADS);
   cfg.dynamicSmemBytes = SMEM;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
@@ -772,7 +779,7 @@ int launch_impl(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int 
   }
   const int units = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * splits;
   const int grid = units < num_sms() ? units : num_sms();
-  CUDA_TRY(launch_k(kern, dim3(grid), dim3(256), C::SMEM, stream, ta, tb, M, N, K, splits, ep));
+  CUDA_TRY(launch_k(kern, dim3(grid), dim3(GEMM_THREADS), C::SMEM, stream, ta, tb, M, N, K, splits, ep));
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
