@@ -310,6 +310,9 @@ def run_ours(a):
     h2d = B * comp_bytes + 4 * (B * (a.q_tokens * 3 + 8)) + 24 * B
     d2h = first.numel() * first.element_size()
 
+    # ---------------- PCIe roofline of the e2e leg: one large pinned H2D copy
+    h2d_peak = _h2d_peak_gbs(dev)
+
     # ---------------- roofline: every kernel, headline = the dominant one
     pk = _peaks()
     # the step is ~5 ms of short kernels: the burst figure applies (the sustained one is a
@@ -350,7 +353,8 @@ def run_ours(a):
         "kernels": kernels,
         "profiled_ms_per_step": t_prof / a.steps * 1e3,
         "kv_load": {"unpack_gbps": ach, "hbm_peak_gbs": pk["hbm_gbs"], "unpack_frac": ach / pk["hbm_gbs"],
-                    "h2d_gbps_e2e": e2e * comp_bytes / 1e9},
+                    "h2d_gbps_e2e": e2e * comp_bytes / 1e9, "h2d_peak_gbs": h2d_peak,
+                    "e2e_pcie_frac": e2e * comp_bytes / 1e9 / h2d_peak},
     }
     if ws > 1:
         out["peer_fetch"] = _peer_leg(a, eng, keys, comp_bytes, ws, rank, dev)
@@ -401,6 +405,21 @@ def _peer_leg(a, eng, keys, comp_bytes, ws, rank, dev):
     finally:
         pool.release(dst)
         peers.close()
+
+
+def _h2d_peak_gbs(dev, nbytes: int = 1 << 30, reps: int = 5) -> float:
+    """Pinned host -> HBM copy bandwidth of this box (the e2e leg's roofline)."""
+    host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    d.copy_(host, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        d.copy_(host, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    return nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
 
 
 def _time_unpack(eng, blobs, steps):
