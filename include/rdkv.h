@@ -186,22 +186,27 @@ RDKV_API int rdkv_kv_peer_gather(const void* src_pool, int64_t src_slots, const 
 /* ------------------- tensor parallelism inside an instance (C5, TP = 2..8) */
 
 /* A TP group's communicator over NVLink peer memory.  Each rank allocates one
- * device buffer of rdkv_tp_comm_bytes(max_elems) bytes, ZEROED, exports it
+ * device buffer of rdkv_tp_comm_bytes(max_elems, size) bytes, ZEROED, exports it
  * (rdkv_ipc_handle) and maps every peer's (rdkv_ipc_open); bases[p] is rank p's
  * buffer as seen from this process (bases[rank] = the local one).  max_elems
- * bounds rows x hidden of one all-reduce.  No reference analogue: the reference
- * models one device per instance (costs.py:52-60); SURVEY §8e/§8f. */
+ * bounds rows x hidden of one all-reduce.  The buffer holds flags, an epoch
+ * counter and double-buffered receive slots [2][size][max_elems] bf16.  No
+ * reference analogue: the reference models one device per instance
+ * (costs.py:52-60); SURVEY §8e/§8f. */
 typedef struct rdkv_tp_comm rdkv_tp_comm;
-RDKV_API size_t rdkv_tp_comm_bytes(size_t max_elems);
+RDKV_API size_t rdkv_tp_comm_bytes(size_t max_elems, int size);
 RDKV_API int rdkv_tp_comm_create(int rank, int size, void* const* bases, size_t max_elems, rdkv_tp_comm** out);
 RDKV_API void rdkv_tp_comm_destroy(rdkv_tp_comm* comm);
-/* This rank's partial buffer `buf` (0/1): dense [rows][cols] bf16. */
-RDKV_API void* rdkv_tp_part_ptr(rdkv_tp_comm* comm, int buf);
-/* One-shot all-reduce fused with the residual add: x[rows][cols] (ld ldx) +=
- * sum over ranks of partial buffer `buf`.  Every rank of the group must call it
- * in the same order; graph-capturable (epochs live in device memory). */
-RDKV_API int rdkv_tp_allreduce_resid(rdkv_tp_comm* comm, void* x, int64_t ldx, int rows, int cols, int buf,
-                                     void* stream);
+/* Store a dense [rows][cols] bf16 partial into this rank's slot of parity `buf`
+ * in every rank's buffer (P2P stores).  rdkv_forward does this from inside the
+ * row-parallel GEMMs' epilogue instead; exposed for tests and custom layers. */
+RDKV_API int rdkv_tp_push(rdkv_tp_comm* comm, const void* src, int rows, int cols, int buf, void* stream);
+/* x[rows][cols] (ld ldx) += sum of the partials every rank pushed in parity
+ * `buf`: publish / await the epoch over NVLink flags, reduce the local receive
+ * slots in fp32 with the residual.  Every rank of the group calls it in the same
+ * order; graph-capturable (epochs live in device memory). */
+RDKV_API int rdkv_tp_reduce_resid(rdkv_tp_comm* comm, void* x, int64_t ldx, int rows, int cols, int buf,
+                                  void* stream);
 
 /* ------------------------------------------------ K2/K4: prefill attention */
 

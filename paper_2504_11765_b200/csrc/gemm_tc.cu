@@ -83,7 +83,7 @@ __device__ __forceinline__ void epilogue_rows(uint32_t taddr, int row, int nb, i
                                               const GemmEpi& ep, int half) {
   const bool row_ok = row < M;
 
-  if constexpr (EPI == EPI_STORE || EPI == EPI_STORE_F32 || EPI == EPI_RESID || EPI == EPI_PARTIAL) {
+  if constexpr (EPI == EPI_STORE || EPI == EPI_STORE_F32 || EPI == EPI_RESID || EPI == EPI_PARTIAL || EPI == EPI_PUSH) {
 #pragma unroll 1
     for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
       uint32_t r[32];
@@ -118,7 +118,11 @@ __device__ __forceinline__ void epilogue_rows(uint32_t taddr, int row, int nb, i
 #pragma unroll
             for (int i = 0; i < 16; ++i) w[i] = pack_bf16(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
           }
-          st_bf16x32(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + col, w);
+          if constexpr (EPI == EPI_PUSH) {
+            for (int p = 0; p < ep.npush; ++p) st_bf16x32(ep.push[p] + (long long)row * ep.ldo + col, w);
+          } else {
+            st_bf16x32(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + col, w);
+          }
         }
       }
     }
@@ -288,6 +292,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int row = mb * BM + wq * 32 + lane;
       const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(wq * 32) << 16);
       epilogue_rows<BN, EPI, DH>(taddr, row, nb, sp, M, N, ep, (warp - 4) >> 2);
+      if constexpr (EPI == EPI_PUSH) __threadfence_system();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -423,6 +428,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int row = mb * 256 + (int)rank * 128 + wq * 32 + lane;
       const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(wq * 32) << 16);
       epilogue_rows<BN, EPI, DH>(taddr, row, nb, 0, M, N, ep, (warp - 4) >> 2);
+      if constexpr (EPI == EPI_PUSH) __threadfence_system();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(acc ? tempty1 : tempty0);
@@ -703,7 +709,12 @@ __global__ void __launch_bounds__(256) splitk_finalize_kernel(const float* __res
       uint2 w;
       w.x = pack_bf16(s.x, s.y);
       w.y = pack_bf16(s.z, s.w);
-      *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + j) = w;
+      if constexpr (EPI == EPI_PUSH) {
+        for (int p = 0; p < ep.npush; ++p) *reinterpret_cast<uint2*>(ep.push[p] + (long long)row * ep.ldo + j) = w;
+        __threadfence_system();
+      } else {
+        *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + j) = w;
+      }
     }
   }
 }
@@ -892,6 +903,7 @@ int finalize(int kind, int dh, const float* part, int splits, int M, int N, cons
       }
       return launch_finalize<EPI_RESID, 0>(part, splits, M, N, ep, stream);
     case EPI_SWIGLU: return launch_finalize<EPI_SWIGLU, 0>(part, splits, M, N, ep, stream);
+    case EPI_PUSH: return launch_finalize<EPI_PUSH, 0>(part, splits, M, N, ep, stream);
     case EPI_QKV:
       if (dh == 64) return launch_finalize<EPI_QKV, 64>(part, splits, M, N, ep, stream);
       if (dh == 128) return launch_finalize<EPI_QKV, 128>(part, splits, M, N, ep, stream);
@@ -934,6 +946,7 @@ int dispatch(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long
     case EPI_STORE_F32: return launch_impl<BN, EPI_STORE_F32, 0>(ta, tb, M, N, K, 1, ep, stream);
     case EPI_RESID: return launch_impl<BN, EPI_RESID, 0>(ta, tb, M, N, K, 1, ep, stream);
     case EPI_SWIGLU: return launch_impl<BN, EPI_SWIGLU, 0>(ta, tb, M, N, K, 1, ep, stream);
+    case EPI_PUSH: return launch_impl<BN, EPI_PUSH, 0>(ta, tb, M, N, K, 1, ep, stream);
     case EPI_QKV:
       if (dh == 64) return launch_impl<BN, EPI_QKV, 64>(ta, tb, M, N, K, 1, ep, stream);
       if (dh == 128) return launch_impl<BN, EPI_QKV, 128>(ta, tb, M, N, K, 1, ep, stream);
@@ -953,6 +966,7 @@ int dispatch_pair(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B,
     case EPI_STORE_F32: return launch_pair<BN, EPI_STORE_F32, 0>(ta, tb, M, N, K, ep, stream);
     case EPI_RESID: return launch_pair<BN, EPI_RESID, 0>(ta, tb, M, N, K, ep, stream);
     case EPI_SWIGLU: return launch_pair<BN, EPI_SWIGLU, 0>(ta, tb, M, N, K, ep, stream);
+    case EPI_PUSH: return launch_pair<BN, EPI_PUSH, 0>(ta, tb, M, N, K, ep, stream);
     case EPI_QKV:
       if (dh == 64) return launch_pair<BN, EPI_QKV, 64>(ta, tb, M, N, K, ep, stream);
       if (dh == 128) return launch_pair<BN, EPI_QKV, 128>(ta, tb, M, N, K, ep, stream);

@@ -15,13 +15,15 @@
 //   SWIGLU     weights interleaved in BN/2 blocks [gate | up]; D = silu(g) * u
 //   QKV        RoPE on q/k heads, q -> token-major buffer, k/v -> head-major
 //              KV planes at per-row slots (document blob layout or paged pool)
+//   PUSH       bf16 D stored into every TP rank's receive slot (NVLink P2P
+//              stores): the GEMM and the all-reduce's data movement are one kernel
 #pragma once
 #include <cuda_runtime.h>
 #include "ptx.cuh"
 
 namespace rdkv {
 
-enum EpiKind : int { EPI_STORE = 0, EPI_STORE_F32 = 1, EPI_RESID = 2, EPI_SWIGLU = 3, EPI_QKV = 4, EPI_PARTIAL = 5 };
+enum EpiKind : int { EPI_STORE = 0, EPI_STORE_F32 = 1, EPI_RESID = 2, EPI_SWIGLU = 3, EPI_QKV = 4, EPI_PARTIAL = 5, EPI_PUSH = 6 };
 
 struct GemmEpi {
   void* out;                 // bf16 (or fp32 for STORE_F32)
@@ -45,6 +47,11 @@ struct GemmEpi {
   const float* norm_gain;
   __nv_bfloat16* norm_out;
   float norm_eps;
+  // PUSH (tensor-parallel row-parallel projections): the bf16 tile is stored into
+  // every rank's receive slot for this rank (dense [M][ldo]); peers' slots are
+  // CUDA-IPC mappings, so the stores cross NVLink while later tiles still compute
+  __nv_bfloat16* push[8];
+  int npush;
 };
 
 // True when launch_gemm will take the split-K path for this shape (small M).

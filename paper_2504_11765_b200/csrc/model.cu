@@ -197,6 +197,21 @@ size_t rdkv_workspace_bytes(const rdkv_model* m, int n_tokens, int n_seqs) {
   return ws_layout(m->d, n_tokens, n_seqs, nullptr, nullptr);
 }
 
+namespace {
+// PUSH epilogue for all-reduce number `ar` of this forward: this rank's slot in
+// every rank's receive buffer of parity ar & 1 (dense rows of `cols`).
+rdkv::GemmEpi tp_push_epi(const rdkv::GemmEpi& base, const rdkv_tp_comm* tp, int ar, int cols) {
+  rdkv::GemmEpi ep = base;
+  ep.out = nullptr;
+  ep.ldo = cols;
+  ep.norm_gain = nullptr;
+  ep.norm_out = nullptr;
+  ep.npush = tp->size;
+  for (int p = 0; p < tp->size; ++p) ep.push[p] = tp->args.push[ar & 1][p];
+  return ep;
+}
+}  // namespace
+
 int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_bytes, void* stream) {
   if (!m || !b) return set_error(RDKV_ERR_ARG, "forward: null argument");
   const rdkv_model_desc& d = m->d;
@@ -291,14 +306,10 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
       er.norm_gain = G(m, wb + 3);
       er.norm_out = ws.h;
     }
-    if (tp) {  // row-parallel: bf16 partial into the symmetric buffer, then all-reduce + residual over NVLink
-      GemmEpi ep = er;
-      ep.out = tp->local_part[ar & 1];
-      ep.ldo = d.hidden;
-      ep.norm_gain = nullptr;
-      ep.norm_out = nullptr;
-      LAUNCH(RDKV_PROF_O, 2.0 * T * qd * d.hidden, launch_gemm(ws.o, qd, W(m, wb + 2), qd, T, d.hidden, (int)qd, EPI_STORE, 0, ep, st));
-      LAUNCH(RDKV_PROF_O, 0.0, launch_tp_allreduce_resid(tp, ws.x, d.hidden, T, d.hidden, ar & 1, st));
+    if (tp) {  // row-parallel: the GEMM pushes its bf16 tiles to every rank (NVLink), then reduce + residual
+      const GemmEpi ep = tp_push_epi(er, tp, ar, d.hidden);
+      LAUNCH(RDKV_PROF_O, 2.0 * T * qd * d.hidden, launch_gemm(ws.o, qd, W(m, wb + 2), qd, T, d.hidden, (int)qd, EPI_PUSH, 0, ep, st));
+      LAUNCH(RDKV_PROF_O, 0.0, launch_tp_reduce_resid(tp, ws.x, d.hidden, T, d.hidden, ar & 1, st));
       ++ar;
     } else {
       LAUNCH(RDKV_PROF_O, 2.0 * T * qd * d.hidden, launch_gemm(ws.o, qd, W(m, wb + 2), qd, T, d.hidden, (int)qd, EPI_RESID, 0, er, st));
@@ -316,13 +327,9 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     er.norm_gain = h_ready ? G(m, wb + RDKV_WEIGHTS_PER_LAYER + 0) : nullptr;  // next layer's attention norm
     er.norm_out = h_ready ? ws.h : nullptr;
     if (tp) {
-      GemmEpi ep = er;
-      ep.out = tp->local_part[ar & 1];
-      ep.ldo = d.hidden;
-      ep.norm_gain = nullptr;
-      ep.norm_out = nullptr;
-      LAUNCH(RDKV_PROF_DOWN, 2.0 * T * d.ffn * d.hidden, launch_gemm(ws.a, d.ffn, W(m, wb + 5), d.ffn, T, d.hidden, d.ffn, EPI_STORE, 0, ep, st));
-      LAUNCH(RDKV_PROF_DOWN, 0.0, launch_tp_allreduce_resid(tp, ws.x, d.hidden, T, d.hidden, ar & 1, st));
+      const GemmEpi ep = tp_push_epi(er, tp, ar, d.hidden);
+      LAUNCH(RDKV_PROF_DOWN, 2.0 * T * d.ffn * d.hidden, launch_gemm(ws.a, d.ffn, W(m, wb + 5), d.ffn, T, d.hidden, d.ffn, EPI_PUSH, 0, ep, st));
+      LAUNCH(RDKV_PROF_DOWN, 0.0, launch_tp_reduce_resid(tp, ws.x, d.hidden, T, d.hidden, ar & 1, st));
       ++ar;
     } else {
       LAUNCH(RDKV_PROF_DOWN, 2.0 * T * d.ffn * d.hidden, launch_gemm(ws.a, d.ffn, W(m, wb + 5), d.ffn, T, d.hidden, d.ffn, EPI_RESID, 0, er, st));

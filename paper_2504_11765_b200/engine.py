@@ -72,11 +72,11 @@ _N_SIG = {
     "rdkv_ipc_close": (C.c_int, [C.c_void_p]),
     "rdkv_kv_peer_gather": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int,
                                       C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]),
-    "rdkv_tp_comm_bytes": (C.c_size_t, [C.c_size_t]),
+    "rdkv_tp_comm_bytes": (C.c_size_t, [C.c_size_t, C.c_int]),
     "rdkv_tp_comm_create": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
     "rdkv_tp_comm_destroy": (None, [C.c_void_p]),
-    "rdkv_tp_part_ptr": (C.c_void_p, [C.c_void_p, C.c_int]),
-    "rdkv_tp_allreduce_resid": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_void_p]),
+    "rdkv_tp_push": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]),
+    "rdkv_tp_reduce_resid": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_void_p]),
     "rdkv_model_set_tp": (C.c_int, [C.c_void_p, C.c_void_p]),
     "rdkv_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
     "rdkv_profile_collect": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64),

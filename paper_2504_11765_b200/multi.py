@@ -184,9 +184,11 @@ class TpGroup:
     """Tensor-parallel group for one instance spread over ``size`` GPUs (C5):
     allocates this rank's zeroed communicator buffer, exchanges CUDA-IPC
     handles over ``group`` (metadata only), maps every peer's buffer and makes
-    ``engine``'s model all-reduce its row-parallel projections over them
-    (rdkv_tp_allreduce_resid: one-shot, NVLink P2P loads, fused with the
-    residual add).  ``engine`` must hold this rank's shard (model.shard_weights)."""
+    ``engine``'s model all-reduce its row-parallel projections over them: the
+    O / down GEMMs push their bf16 tiles into every rank's receive slot from
+    the epilogue (NVLink P2P stores), then rdkv_tp_reduce_resid sums the local
+    slots with the residual.  ``engine`` must hold this rank's shard
+    (model.shard_weights)."""
 
     def __init__(self, engine, max_tokens: int, group=None) -> None:
         import ctypes as C
@@ -200,7 +202,7 @@ class TpGroup:
         self.engine = engine
         self.rank, self.size = dist.get_rank(group), dist.get_world_size(group)
         self.max_elems = max_tokens * engine.spec.hidden
-        nbytes = int(lib.rdkv_tp_comm_bytes(self.max_elems))
+        nbytes = int(lib.rdkv_tp_comm_bytes(self.max_elems, self.size))
         self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=engine.device)
         torch.cuda.synchronize(engine.device)
         h = (C.c_ubyte * 64)()
@@ -224,22 +226,23 @@ class TpGroup:
         _lib.check(lib.rdkv_model_set_tp(engine.model._h, comm))
         dist.barrier(group=group)
 
-    def allreduce_resid(self, x: torch.Tensor, part: int = 0, stream=None) -> None:
-        """x[rows, cols] += sum over ranks of each rank's partial buffer ``part``."""
+    def push(self, partial: torch.Tensor, buf: int = 0, stream=None) -> None:
+        """Store this rank's dense [rows, cols] bf16 partial into its slot of parity
+        ``buf`` in every rank's buffer (what the PUSH GEMM epilogue does in-kernel)."""
+        from . import _lib
+        from .engine import _L, _stream_ptr
+
+        rows, cols = partial.shape
+        _lib.check(_L().rdkv_tp_push(self.comm, partial.data_ptr(), rows, cols, buf, _stream_ptr(stream)))
+
+    def reduce_resid(self, x: torch.Tensor, buf: int = 0, stream=None) -> None:
+        """x[rows, cols] += sum of the partials every rank pushed in parity ``buf``."""
         from . import _lib
         from .engine import _L, _stream_ptr
 
         rows, cols = x.shape
-        _lib.check(_L().rdkv_tp_allreduce_resid(self.comm, x.data_ptr(), x.stride(0), rows, cols, part,
-                                                _stream_ptr(stream)))
-
-    def part_tensor(self, part: int, rows: int, cols: int) -> torch.Tensor:
-        """This rank's partial buffer as a [rows, cols] bf16 view (tests)."""
-        from .engine import _L
-
-        ptr = _L().rdkv_tp_part_ptr(self.comm, part)
-        off = ptr - self.buf.data_ptr()
-        return self.buf[off: off + rows * cols * 2].view(torch.bfloat16).view(rows, cols)
+        _lib.check(_L().rdkv_tp_reduce_resid(self.comm, x.data_ptr(), x.stride(0), rows, cols, buf,
+                                             _stream_ptr(stream)))
 
     def close(self) -> None:
         from .engine import _L

@@ -1,9 +1,12 @@
 """Tensor parallelism inside one instance (C5 shape class): TP ranks, one
-process each, all on cuda:0 of the GPU box (the CUDA-IPC mapping and the
-one-shot all-reduce kernel are the same code that runs across NVLink peers).
+process each, all on cuda:0 of the GPU box (the CUDA-IPC mappings, the PUSH
+GEMM epilogue and the reduce kernel are the same code that runs across NVLink
+peers).  The forward tests cover both GEMM paths of the push: the CTA-pair
+kernel (document prefill, M >= 256) and the split-K finalize (query, M = 48).
 
-* the all-reduce fused with the residual add equals the fp32 sum of the ranks'
-  partials plus the residual, over consecutive epochs on both buffers;
+* push (P2P stores into every rank's receive slot) + reduce fused with the
+  residual add equals the fp32 sum of the ranks' partials plus the residual,
+  over consecutive epochs on both parities;
 * a TP=2 / TP=4 forward (document prefill, then query prefill over the cached
   prefix, per-rank KV heads) reproduces the single-GPU logits of the same
   weights within the bf16 tolerance (rel err <= 2e-2, same first token when
@@ -67,9 +70,9 @@ def _ar_worker(rank, world, port, q):
         for epoch in range(5):
             buf = epoch & 1
             part = ((rank + 1 + epoch) * base / world).bfloat16()
-            tp.part_tensor(buf, rows, cols).copy_(part)
             ref = x.float() + sum(((r + 1 + epoch) * base / world).bfloat16().float() for r in range(world))
-            tp.allreduce_resid(x, buf)
+            tp.push(part, buf)
+            tp.reduce_resid(x, buf)
             torch.cuda.synchronize()
             errs.append(float((x.float() - ref).abs().max() / ref.abs().max()))
             x = ref.bfloat16()
