@@ -357,7 +357,10 @@ def run_ours(a):
                     "e2e_pcie_frac": e2e * comp_bytes / 1e9 / h2d_peak},
     }
     if ws > 1:
-        out["peer_fetch"] = _peer_leg(a, eng, keys, comp_bytes, ws, rank, dev)
+        try:
+            out["peer_fetch"] = _peer_leg(a, eng, keys, comp_bytes, ws, rank, dev)
+        except Exception as exc:  # the headline legs above stand on their own
+            out["peer_fetch"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     if not a.no_extras:
         out.update(_extras(a, eng, gen, spec, items, blobs, keys, qtoks, ws, rank, dev))
     if rank == 0 and ws == 1:
