@@ -60,6 +60,18 @@ RDKV_API uint64_t rdkv_fnv1a64(const void* data, size_t len, uint64_t seed);
 RDKV_API void rdkv_fnv1a64_many(const void* const* bufs, const size_t* lens, size_t n, uint64_t* out,
                        int threads);
 
+/* FNV-1a of `len` bytes of DEVICE memory, computed in parallel on the GPU and
+ * bit-exact with rdkv_fnv1a64: the low byte of the state is a 256-state
+ * automaton (run from every start byte per 16-KiB chunk, then stitched), and
+ * given it the 64-bit update is affine, so chunks compose.  The result lands in
+ * *out_dev (device uint64) asynchronously on `stream`; `scratch` is device
+ * memory of rdkv_fnv1a64_device_scratch(len) bytes.  Used for the payload
+ * checksum of generated KV (codec.py:148/222) and of disk hits (codec.py:293),
+ * which a single core computes at ~0.6 GB/s. */
+RDKV_API size_t rdkv_fnv1a64_device_scratch(size_t len);
+RDKV_API int rdkv_fnv1a64_device(const void* data, size_t len, uint64_t seed, void* scratch, size_t scratch_bytes,
+                                 uint64_t* out_dev, void* stream);
+
 /* Fixed-width view of the .rdkv header (codec.py:8-13, 35-36, 110-137). */
 typedef struct rdkv_header {
   uint64_t model_hash;

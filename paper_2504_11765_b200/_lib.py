@@ -72,6 +72,8 @@ SIGNATURES: dict[str, tuple] = {
                               C.POINTER(_sz), C.POINTER(_sz)]),
     "rdkv_drop_page_cache": (_i32, [_cp]),
     "rdkv_gemm_bf16": (_i32, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _i32, _i32, _vp]),
+    "rdkv_fnv1a64_device_scratch": (_sz, [_sz]),
+    "rdkv_fnv1a64_device": (_i32, [_vp, _sz, _u64, _vp, _sz, _vp, _vp]),
     "rdkv_attention": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32,
                               _i32, _i32, _i32, _i32, _i32, _vp, _sz, _vp]),
     "rdkv_attention_scratch_bytes": (_sz, [_i32, _i32, _i32]),

@@ -100,6 +100,26 @@ def fnv1a64(data, seed: int = FNV_OFFSET) -> int:
     return int(_lib.lib().rdkv_fnv1a64(addr, n, seed & _U64))
 
 
+def fnv1a64_device(data, seed: int = FNV_OFFSET, stream=None) -> int:
+    """64-bit FNV-1a of a CUDA uint8 tensor, computed on its GPU (rdkv_fnv1a64_device:
+    low-byte automaton + affine chunk composition, bit-exact with codec.py:64-69)."""
+    import torch
+
+    if not (hasattr(data, "is_cuda") and data.is_cuda):
+        raise TypeError("fnv1a64_device needs a CUDA tensor")
+    L = _lib.lib()
+    raw = data.reshape(-1).view(torch.uint8) if data.dtype != torch.uint8 else data.reshape(-1)
+    n = raw.numel()
+    need = int(L.rdkv_fnv1a64_device_scratch(n))
+    ws = torch.empty(need, dtype=torch.uint8, device=raw.device)
+    out = torch.empty(1, dtype=torch.int64, device=raw.device)
+    st = stream if stream is not None else torch.cuda.current_stream(raw.device)
+    _lib.check(L.rdkv_fnv1a64_device(raw.data_ptr(), n, seed & _U64, ws.data_ptr(), need, out.data_ptr(),
+                                     st.cuda_stream))
+    st.synchronize()
+    return int(out.item()) & _U64
+
+
 def fnv1a64_many(buffers: Sequence, threads: int = 8) -> list[int]:
     """FNV-1a of several independent buffers in parallel (one chain per buffer)."""
     n = len(buffers)
@@ -193,7 +213,7 @@ class KvBlob:
     codec.py:148 and :222).
     """
 
-    __slots__ = ("header", "payload")
+    __slots__ = ("header", "payload", "device")  # device: optional HBM copy of the payload (load-path cache)
 
     def __init__(self, header: KvBlobHeader, payload) -> None:
         _, n = buffer_address(payload)
@@ -203,12 +223,14 @@ class KvBlob:
             raise ValueError("payload checksum does not match header")
         object.__setattr__(self, "header", header)
         object.__setattr__(self, "payload", payload)
+        object.__setattr__(self, "device", None)
 
     @classmethod
-    def trusted(cls, header: KvBlobHeader, payload) -> "KvBlob":
+    def trusted(cls, header: KvBlobHeader, payload, device=None) -> "KvBlob":
         obj = object.__new__(cls)
         object.__setattr__(obj, "header", header)
         object.__setattr__(obj, "payload", payload)
+        object.__setattr__(obj, "device", device)
         return obj
 
     def __setattr__(self, name, value):

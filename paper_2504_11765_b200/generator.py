@@ -8,9 +8,9 @@ key, header matching the key, exceptions propagate to every waiter.
 
 A call runs the document prefill over the ordered combination's concatenated
 tokens (positions 0..n-1, prefetch.py:6-8) on the engine's GPU; the payload is
-written by the QKV epilogue directly in the `.rdkv` layout, copied once into
-pinned host memory (the memory tier's DMA-ready form), FNV-1a-hashed natively
-and wrapped without re-hashing.  The KV is also placed in the engine's HBM
+written by the QKV epilogue directly in the `.rdkv` layout, FNV-1a-hashed on
+the GPU (codec.fnv1a64_device, bit-exact) while it is copied once into pinned
+host memory (the memory tier's DMA-ready form), and wrapped without re-hashing.  The KV is also placed in the engine's HBM
 tier (pool blocks) so a query dispatched to the same GPU loads nothing.
 """
 
@@ -21,7 +21,7 @@ from typing import Callable, Sequence
 import numpy as np
 import torch
 
-from .codec import KvBlob, fnv1a64, make_header
+from .codec import KvBlob, fnv1a64_device, make_header
 from .engine import Engine
 from .model import combo_tokens
 from .store import KvKey
@@ -48,10 +48,16 @@ class KvGenerator:
         with torch.cuda.device(eng.device):
             kv = eng.generate_doc_kv(toks)
             raw = kv.view(torch.uint8)
+            main = torch.cuda.current_stream()
+            # D2H into the host tier on the copy stream while the GPU hashes the payload
+            eng.copy_stream.wait_stream(main)
             host = torch.empty(raw.numel(), dtype=torch.uint8, pin_memory=True)
-            host.copy_(raw, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-        header = make_header(self.profile, ids, len(toks), fnv1a64(host))
+            with torch.cuda.stream(eng.copy_stream):
+                host.copy_(raw, non_blocking=True)
+            raw.record_stream(eng.copy_stream)
+            checksum = fnv1a64_device(raw)
+            eng.copy_stream.synchronize()
+        header = make_header(self.profile, ids, len(toks), checksum)
         if self.keep_on_device:
             with torch.cuda.device(eng.device):
                 eng.make_resident(KvKey(self.profile.model_hash, ids), kv, len(toks))

@@ -90,6 +90,12 @@ def prefill_batch(engine: Engine, requests: Sequence[PrefillRequest], timed: boo
             seqs.append(SeqPlan(new, n_cached, blocks))
             if hit:
                 host = r.lookup.blob.payload_tensor()
+                dev_copy = r.lookup.blob.device
+                if dev_copy is not None and dev_copy.device == engine.device:  # already in HBM (GPU-verified disk hit)
+                    dev = dev_copy.view(torch.bfloat16)
+                    staged.append(dev)
+                    jobs.append((dev, n_cached, i))
+                    continue
                 if stream_layers and not timed:  # copied layer by layer by the streamer
                     dev = torch.empty(host.numel(), dtype=torch.uint8, device=engine.device).view(torch.bfloat16)
                     pending_h2d.append((host, dev.view(torch.uint8)))
