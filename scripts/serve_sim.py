@@ -23,7 +23,7 @@ from paper_2504_11765_b200.model import get_spec
 from paper_2504_11765_b200.service import SharedCacheService
 from paper_2504_11765_b200.serving import MeasuredExecutor, summarize
 from paper_2504_11765_b200.sim import ArrivalSpec, SimConfig, run
-from paper_2504_11765_b200.store import KvStore
+from paper_2504_11765_b200.store import GpuVerifier, KvStore
 from paper_2504_11765_b200.workload import zipf_stream
 
 
@@ -45,7 +45,7 @@ def main():
     spec = get_spec(a.model, a.layers)
     eng = Engine(spec, seed=0, pool_tokens=a.k * a.doc_tokens + a.q_tokens + 4096)
     root = Path(tempfile.mkdtemp(prefix="rdkv_serve_"))
-    svc = SharedCacheService(KvStore(root, memory_capacity_bytes=0))
+    svc = SharedCacheService(KvStore(root, memory_capacity_bytes=0, verifier=GpuVerifier(eng.device)))
     inst = DeviceProfile("b200-0", DeviceKind.INFERENCE_GPU, 1.0)
     if a.configuration == "a":
         cfg_kind, devices = Configuration.SHARED_GPU_N, (inst, DeviceProfile("b200-gen", DeviceKind.GENERATOR_GPU, 1.0))
