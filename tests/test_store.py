@@ -155,3 +155,19 @@ def test_reference_store_reads_our_files(tmp_path):
         r = ref.get(rstore.key_for(rp, ids))
         assert r.outcome is rstore.Outcome.DISK_HIT
         assert r.blob.payload == blob(ids, tokens=len(ids)).payload
+
+
+def test_large_blob_file_roundtrip_parallel_read(tmp_path):
+    # > 2 MiB files are read by several threads; sizes just past a piece boundary
+    # must still include the tail bytes (header + payload + checksum verify)
+    from paper_2504_11765_b200.codec import ModelProfile, synth_blob
+    from paper_2504_11765_b200.store import KvKey, KvStore, Outcome
+    prof = ModelProfile("tiny", 2, 256, 4, 64, 2)
+    for tokens in (1025, 2049, 8192 + 3):             # 2 MiB + 2 KiB, 4 MiB + 2 KiB, 16 MiB + 6 KiB payloads
+        key = KvKey(prof.model_hash, (tokens,))
+        store = KvStore(tmp_path / str(tokens), memory_capacity_bytes=0)
+        blob = synth_blob(prof, key.doc_ids, tokens)
+        store.put(key, blob)
+        look = store.get(key)
+        assert look.outcome is Outcome.DISK_HIT
+        assert look.blob == blob
