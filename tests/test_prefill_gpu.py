@@ -201,3 +201,30 @@ def test_resident_tier_lru_respects_pins():
     eng.resident.unpin("a")
     assert eng.make_resident("d", pay(192), 192)      # now a and c go
     assert eng.pool.free_blocks == free0 - 3
+
+
+def test_c2_full_shape_bench_path_matches_oracle():
+    """The bench configuration itself (BASELINE configs[1]): Llama-3.2-1B shape at
+    full depth, a 5 x 512 composite generated on the GPU and served from the HBM
+    tier, 64 query tokens — first-token logits vs the fp32 oracle over the same
+    ordered prompt (full-prompt semantics, costs.py:89-99)."""
+    from paper_2504_11765_b200.generator import KvGenerator
+    from paper_2504_11765_b200.prefill import PrefillRequest, prefill_batch
+    from paper_2504_11765_b200.store import KvKey, LookupResult, Outcome
+
+    spec = get_spec("llama-3.2-1b")
+    eng = Engine(spec, seed=0, pool_tokens=4096, device_cache_bytes=spec.kv_bytes_per_token() * 2600)
+    gen = KvGenerator(eng, keep_on_device=True)
+    docs, ntok = (4211, 17, 905, 3, 77), (512,) * 5
+    blob = gen.generate(docs, ntok)
+    key = KvKey(spec.profile().model_hash, docs)
+    q = query_tokens(12345, 64, spec.vocab)
+    r = prefill_batch(eng, [PrefillRequest(LookupResult(Outcome.MEMORY_HIT, blob, 0), None, q, key)], timed=False)
+    torch.cuda.synchronize()
+    orc = OracleModel(eng.weights)
+    kref, ref = orc.forward(np.concatenate([gen.tokens(docs, ntok), q]))
+    _check_logits(r.logits[0], ref, r.next_token[0])
+    # the cached composite itself (KV written by the QKV epilogue) vs the oracle's KV of the prefix
+    got = eng.pool.gather(eng.resident.acquire(key).blocks, 2560).float().cpu()
+    eng.resident.unpin(key)
+    assert rel_err(got, kref[:, :, :, :2560]) <= TOL
