@@ -121,6 +121,37 @@ class MeasuredExecutor:
         return (per,) * len(ids)
 
 
+@dataclass
+class CalibratedExecutor:
+    """Executor for ``sim.run`` whose costs are B200 *measurements* taken on one
+    GPU (scripts/calibrate_costs.py): prefill time by cached-prefix level,
+    host-tier and disk load time per byte, generation time by prefix length.
+    Lets the reference policy project multi-instance runs (C4: 8 instances)
+    that one GPU cannot host; results are modeled, and labeled as such."""
+
+    costs: dict
+
+    def bind(self, config: SimConfig, cache: TierMirror) -> None:
+        self.cfg = config
+        c = self.costs
+        if config.k != c["k"]:
+            raise ValueError(f"costs were measured for k={c['k']}, config has k={config.k}")
+
+    def serve(self, d: Dispatch) -> tuple[float, float]:
+        c = self.costs
+        prefill = c["prefill_s_by_cached_docs"][d.best]
+        if d.best == 0:
+            return 0.0, prefill
+        per = c["host_tier_load_s_per_byte"] if d.tier is Tier.MEMORY else c["disk_read_verify_s_per_byte"]
+        return per * d.size_bytes, prefill
+
+    def generation_time(self, task: GenTask) -> float:
+        return self.costs["generation_s_by_docs"][len(task.prefix) - 1]
+
+    def generated(self, task: GenTask) -> None:
+        pass
+
+
 def summarize(records, access_log=None) -> dict:
     """TTFT percentiles (both definitions) and throughput of a run."""
     lat = np.array([r.first_token - r.arrival for r in records])
