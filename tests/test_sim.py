@@ -100,3 +100,32 @@ def test_invariants_n_instances():
         for a, b in zip(rows, rows[1:]):
             assert b.dispatch >= a.dispatch + a.kv_load + a.prefill - 1e-12
     assert report.origin_counts.get("generated", 0) > 0
+
+
+def test_calibrated_executor_uses_measured_costs():
+    """serving.CalibratedExecutor answers the policy from a B200 cost table:
+    prefill by cached-prefix level, per-byte load by tier, generation by length."""
+    from paper_2504_11765_b200.costs import (Configuration, CostParams, DeviceKind, DeviceProfile, ModelProfile,
+                                             Tier)
+    from paper_2504_11765_b200.serving import CalibratedExecutor
+    from paper_2504_11765_b200.sim import ArrivalSpec, Dispatch, GenTask, SimConfig, run
+    from paper_2504_11765_b200.workload import zipf_stream
+
+    costs = {"k": 2, "prefill_s_by_cached_docs": [0.03, 0.02, 0.01], "host_tier_load_s_per_byte": 1e-11,
+             "disk_read_verify_s_per_byte": 1e-9, "generation_s_by_docs": [0.05, 0.09]}
+    prof = ModelProfile("m", 2, 8, 2, 4, 2)
+    devs = tuple(DeviceProfile(f"g{i}", DeviceKind.INFERENCE_GPU, 1.0) for i in range(2))
+    cfg = SimConfig(configuration=Configuration.SHARED_GPU_N, devices=devs, cost=CostParams(model=prof),
+                    arrival=ArrivalSpec(rate=5.0), k=2, tries=1, seed=3)
+    ex = CalibratedExecutor(costs)
+    ex.bind(cfg, None)
+    it = zipf_stream(50, 1.0, 1, seed=0, k=2, q_tokens=4, doc_tokens=8)[0]
+    miss = Dispatch(0, it, it.doc_ids[:2], it.doc_tokens[:2], 0, None, 0, 20, 0)
+    assert ex.serve(miss) == (0.0, 0.03)
+    disk = Dispatch(0, it, it.doc_ids[:2], it.doc_tokens[:2], 1, Tier.DISK, 8, 12, 1000)
+    assert ex.serve(disk) == (1000 * 1e-9, 0.02)
+    mem = Dispatch(0, it, it.doc_ids[:2], it.doc_tokens[:2], 2, Tier.MEMORY, 16, 4, 1000)
+    assert ex.serve(mem) == (1000 * 1e-11, 0.01)
+    assert ex.generation_time(GenTask(it.doc_ids[:2], 16, 100)) == 0.09
+    report, records = run(cfg, zipf_stream(50, 1.0, 20, seed=0, k=2, q_tokens=4, doc_tokens=8), CalibratedExecutor(costs))
+    assert len(records) == 20 and all(r.prefill == 0.03 for r in records)   # no generator: every query misses
