@@ -301,7 +301,8 @@ def kv_unpack(pool: KvPool, jobs: Sequence[tuple[torch.Tensor, int, int]], block
     _lib.check(_L().rdkv_kv_unpack(jobs_dev.data_ptr(), len(jobs), max(n for _, n, _ in jobs), block_table.data_ptr(),
                                    pool.block_size, pool.data.data_ptr(), s.layers, s.kv_heads, s.head_dim,
                                    pool.slots, elem_width, l0, l1, _stream_ptr(stream)))
-    pool._last_jobs = jobs_dev  # keep alive until the stream consumes it
+    # the job table may have been staged on another stream: keep its memory until this launch has read it
+    jobs_dev.record_stream(stream if stream is not None else torch.cuda.current_stream(pool.data.device))
 
 
 class LayerStreamer:
