@@ -31,6 +31,7 @@
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 #include <cstdint>
+#include <cstdlib>
 
 #include "attention.cuh"
 #include "common.cuh"
@@ -58,7 +59,8 @@ struct TcCfg {
   static constexpr uint32_t OFF_Q = 0;             // [2 Q tiles]
   static constexpr uint32_t OFF_K = OFF_Q + 2 * QB;
   static constexpr uint32_t OFF_V = OFF_K + STAGES * KB;
-  static constexpr uint32_t OFF_BAR = OFF_V + STAGES * KB;
+  static constexpr uint32_t OFF_RED = OFF_V + STAGES * KB;  // [2 parity][2 Q tiles][2 halves][128 rows] fp32
+  static constexpr uint32_t OFF_BAR = OFF_RED + 2 * 2 * 2 * ROWS * 4;
   static constexpr size_t SMEM = OFF_BAR + 8 * (1 + 3 * STAGES + 8) + 16;
   // TMEM columns
   static constexpr uint32_t COL_S = 0;                          // S_i at 128 i
@@ -67,7 +69,18 @@ struct TcCfg {
   static constexpr uint32_t P_STRIDE = ALIAS ? BKV : BKV / 2;
 };
 
-constexpr int THREADS = 384;  // warps 0-3 / 4-7: softmax of Q tile 0 / 1; 8: TMA; 9 / 10: MMA of tile 0 / 1; 11 idle
+// SPL softmax warps per query row (each takes BKV / SPL keys of a tile):
+//   warps [0, NS): softmax, NS = 8 * SPL (Q tile i, key half h, TMEM quadrant q);
+//   NS: TMA producer; NS+1 / NS+2: MMA issuers of Q tile 0 / 1; NS+3 idle.
+template <int SPL>
+struct Roles {
+  static constexpr int NS = 8 * SPL;
+  static constexpr int THREADS = 32 * (NS + 4);
+  // setmaxnreg budgets: the CTA keeps its launch allocation (THREADS x launch-bound registers),
+  // so NS x 32 x REG_SOFTMAX + 4 x 32 x REG_AUX must not exceed it (SPL=1: 384 x 168, SPL=2: 640 x 96)
+  static constexpr int REG_SOFTMAX = SPL == 1 ? 224 : 104;
+  static constexpr int REG_AUX = SPL == 1 ? 56 : 40;
+};
 constexpr float RESCALE_LOG2 = 8.f;   // lazy O rescale: keep a stale row max until it is 2^8 too small
 #ifndef RDKV_ATTN_TRACE
 #define RDKV_ATTN_TRACE 0  // 1: per-tile clock64 timeline of CTA 0 (debug builds only)
@@ -109,10 +122,13 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
-template <int DH>
-__global__ void __launch_bounds__(THREADS, 1)
+template <int DH, int SPL>
+__global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnParams p) {
   using C = TcCfg<DH>;
+  using R = Roles<SPL>;
+  constexpr int NS = R::NS;
+  constexpr int KH = BKV / SPL;  // keys of a tile per softmax thread
   constexpr int ST = C::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
@@ -150,10 +166,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int* bt = p.block_table + (long long)s * p.bt_stride;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  if (warp == 8 && lane == 0) {
+  if (warp == NS && lane == 0) {
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
-    mbar_init(q_full, 8);
+    mbar_init(q_full, NS);
     for (int i = 0; i < ST; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&v_full[i], 1);
@@ -161,13 +177,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 4);
-      mbar_init(&p_full[i], 4);
+      mbar_init(&s_empty[i], 4 * SPL);
+      mbar_init(&p_full[i], 4 * SPL);
       mbar_init(&o_done[i], 1);
     }
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  if (warp == NS + 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -177,8 +193,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   // register budget: the softmax warpgroups hold a 128-score row per thread,
   // the TMA / MMA warpgroup gives its registers up
-  if (warp >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
-  if (warp == 8) {
+  if (warp >= NS) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R::REG_AUX) : "memory");
+  if (warp == NS) {
     // ------------------------------------------------------------ TMA producer
     // The whole warp walks the tiles: every 32 tiles each lane resolves one
     // tile's two block-table rows (32 global loads in parallel instead of a
@@ -215,11 +231,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       __syncwarp();
     }
-  } else if (warp == 9 || warp == 10) {
+  } else if (warp == NS + 1 || warp == NS + 2) {
     // ------------------------------------------------------------ MMA issuers
     // one issuing thread per Q tile, so neither softmax warpgroup ever waits on
     // the other's progress (their exp2 phases drift apart and overlap)
-    const int i = warp - 9;
+    const int i = warp - NS - 1;
     if (lane == 0 && n_tiles > 0 && i < n_q) {
       constexpr uint32_t idesc_qk = idesc_bf16_f32(ROWS, BKV);
       constexpr uint32_t idesc_pv = idesc_bf16_f32(ROWS, DH) | (1u << 16);  // B (V) is MN-major
@@ -255,8 +271,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc_fence_after();
         const uint32_t va = sb + C::OFF_V + st * C::KB;
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)  // O_i (+)= P_i . V(j), P_i from TMEM
-          umma_bf16_ts(tO, tP + kk * 8, desc_mn(va + kk * 2048, BKV * 128), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+        for (int kk = 0; kk < BKV / 16; ++kk) {  // O_i (+)= P_i . V(j), P_i from TMEM
+          // P of keys [16kk, 16kk+16): with P over S each half writes inside its own S columns
+          const uint32_t pcol = C::ALIAS ? (kk / (KH / 16)) * KH + (kk % (KH / 16)) * 8 : kk * 8;
+          umma_bf16_ts(tO, tP + pcol, desc_mn(va + kk * 2048, BKV * 128), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+        }
         umma_commit(&o_done[i]);
         TRACE(2 + i, j, 1);
         umma_commit(&kv_empty[st]);
@@ -267,23 +286,40 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     }
-  } else if (warp < 8) {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
-    // ------------------------------------------------------------ softmax warpgroups
-    // warp w < 8: Q tile i = w / 4, TMEM lanes [32 (w % 4), +32) = query rows;
-    // each thread owns one full row of S (128 keys) and of O.
-    const int i = warp >> 2, quad = warp & 3;
+  } else if (warp < NS) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(R::REG_SOFTMAX) : "memory");
+    // ------------------------------------------------------------ softmax warps
+    // warp w < NS: Q tile i, key half h (SPL = 2: keys [64h, 64h+64) of every tile,
+    // O columns [h dh/2, (h+1) dh/2)), TMEM lanes [32 (w % 4), +32) = query rows.
+    // With SPL = 2 the two halves of a row exchange their row max per tile (and
+    // the row sum at the end) through smem under a 64-thread named barrier.
+    const int i = warp / (4 * SPL), h = (warp / 4) % SPL, quad = warp & 3;
     const int r = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const int nrows = max(0, min(TPT, ntok - i * TPT)) * G;
-    // Q row -> smem (K-major SW128, DH/64 column blocks of [128 rows][128 B])
+    float* red = reinterpret_cast<float*>(smem + C::OFF_RED);  // [parity][tile][half][row]
+    auto pair_sync = [&]() {
+      if constexpr (SPL == 2) asm volatile("bar.sync %0, 64;" ::"r"(1 + i * 4 + quad) : "memory");
+    };
+    auto exchange = [&](float v, int parity, bool use_max) {  // combine with the partner half of this row
+      if constexpr (SPL == 1) {
+        return v;
+      } else {
+        red[((parity * 2 + i) * 2 + h) * ROWS + r] = v;
+        pair_sync();
+        const float o = red[((parity * 2 + i) * 2 + (h ^ 1)) * ROWS + r];
+        return use_max ? fmaxf(v, o) : v + o;
+      }
+    };
+    // Q row (this half's 16-B chunks) -> smem (K-major SW128, DH/64 column blocks of [128 rows][128 B])
     {
       const bool ok = r < nrows;
       const int rr = ok ? r : 0;
       const uint4* src = reinterpret_cast<const uint4*>(
           p.q + (long long)(row_base + i * TPT + rr / G) * p.ldq + (long long)(kvh * G + rr % G) * DH);
 #pragma unroll
-      for (int c = 0; c < DH / 8; ++c) {
+      for (int cc = 0; cc < DH / 8 / SPL; ++cc) {
+        const int c = h * (DH / 8 / SPL) + cc;
         const uint4 v = ok ? src[c] : make_uint4(0, 0, 0, 0);
         const uint32_t a = sb + C::OFF_Q + i * C::QB + (c >> 3) * (ROWS * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4);
         st_shared_v4(a, v.x, v.y, v.z, v.w);
@@ -296,37 +332,36 @@ __global__ void __launch_bounds__(THREADS, 1)
       // padded rows pretend to be the last valid position so no row is fully masked
       const int qpos = (r < nrows) ? pos0 + i * TPT + r / G : kv_len - 1;
       const float sl2 = p.scale_log2;
-      const uint32_t tS = tmem + C::COL_S + i * BKV + lane_off;
-      const uint32_t tO = tmem + C::COL_O + i * DH + lane_off;
-      const uint32_t tP = tmem + C::COL_P + i * C::P_STRIDE + lane_off;
+      constexpr int OH = DH / SPL;  // O columns of this half
+      const uint32_t tS = tmem + C::COL_S + i * BKV + h * KH + lane_off;
+      const uint32_t tO = tmem + C::COL_O + i * DH + h * OH + lane_off;
+      // P columns of this half: inside its own S columns when P is written over S
+      const uint32_t tP = tmem + C::COL_P + i * C::P_STRIDE + h * (C::ALIAS ? KH : KH / 2) + lane_off;
       float m_used = -INFINITY;  // row max the P values and O are scaled to (log2 domain)
-      float l = 0.f;             // row sum at scale m_used
+      float l = 0.f;             // this half's row sum at scale m_used
       for (int j = 0; j < n_tiles; ++j) {
-        if (quad == 0 && lane == 0) TRACE(i, j, 0);
         mbar_wait(&s_full[i], j & 1);
-        if (quad == 0 && lane == 0) TRACE(i, j, 1);
         tc_fence_after();
-        uint32_t sv[BKV];
+        uint32_t sv[KH];
 #pragma unroll
-        for (int c = 0; c < BKV / 32; ++c) tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[c * 32]));
+        for (int c = 0; c < KH / 32; ++c) tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[c * 32]));
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[i]);
-        const int lim = qpos - (t_begin + j) * BKV;  // key e of the tile visible iff e <= lim
-        if (lim < BKV - 1) {
+        const int lim = qpos - (t_begin + j) * BKV - h * KH;  // key e of this half visible iff e <= lim
+        if (lim < KH - 1) {
 #pragma unroll
-          for (int e = 0; e < BKV; ++e)
+          for (int e = 0; e < KH; ++e)
             if (e > lim) sv[e] = __float_as_uint(-INFINITY);
         }
         float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-        for (int e = 0; e < BKV; e += 8)
+        for (int e = 0; e < KH; e += 8)
 #pragma unroll
           for (int u = 0; u < 4; ++u)
             mx4[u] = fmax3(mx4[u], __uint_as_float(sv[e + 2 * u]), __uint_as_float(sv[e + 2 * u + 1]));
-        const float mt = fmax3(fmaxf(mx4[0], mx4[1]), mx4[2], mx4[3]) * sl2;
-        if (quad == 0 && lane == 0) TRACE(i, j, 2);
+        const float mt = exchange(fmax3(fmaxf(mx4[0], mx4[1]), mx4[2], mx4[3]), j & 1, true) * sl2;
         // lazy rescale: move the reference max only when it grew by more than 2^8
         const bool need = mt > m_used + RESCALE_LOG2;
         const bool rescale = __any_sync(0xffffffffu, need) && j > 0;
@@ -340,9 +375,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         // overlaps P_i.V(j-1), which still reads the P_i buffer
         const float nb = m_used == -INFINITY ? 0.f : -m_used;
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-        uint32_t pk[BKV / 2];
+        uint32_t pk[KH / 2];
 #pragma unroll
-        for (int k = 0; k < BKV; k += 4) {
+        for (int k = 0; k < KH; k += 4) {
           float x0, x1, x2, x3;
           ffma2(x0, x1, __uint_as_float(sv[k]), __uint_as_float(sv[k + 1]), sl2, sl2, nb, nb);
           ffma2(x2, x3, __uint_as_float(sv[k + 2]), __uint_as_float(sv[k + 3]), sl2, sl2, nb, nb);
@@ -360,18 +395,17 @@ __global__ void __launch_bounds__(THREADS, 1)
           pk[k / 2] = pack_bf16(x0, x1);
           pk[k / 2 + 1] = pack_bf16(x2, x3);
         }
-        if (quad == 0 && lane == 0) TRACE(i, j, 3);
         // P_i (and O_i) are free once P_i.V(j-1) has retired (implied by s_full when P aliases S)
         if (j > 0) {
           mbar_wait(&o_done[i], (j - 1) & 1);
           tc_fence_after();
         }
 #pragma unroll
-        for (int c = 0; c < BKV / 64; ++c) tmem_st32(tP + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[c * 32]));
+        for (int c = 0; c < KH / 64; ++c) tmem_st32(tP + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[c * 32]));
         l += (s0 + s1) + (s2 + s3);
-        if (rescale) {  // O_i row *= f before P_i.V(j) accumulates into it
+        if (rescale) {  // this half of the O_i row *= f before P_i.V(j) accumulates into it
 #pragma unroll
-          for (int c = 0; c < DH / 32; ++c) {
+          for (int c = 0; c < OH / 32; ++c) {
             uint32_t ov[32];
             tmem_ld32(tO + c * 32, ov);
             tmem_ld_wait();
@@ -389,31 +423,32 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[i]);
-        if (quad == 0 && lane == 0) TRACE(i, j, 4);
       }
-      // final O row: wait for the last P.V, normalise, store
+      // final O row: wait for the last P.V, normalise, store (each half its O columns)
+      const float lt = exchange(l, n_tiles & 1, false);  // the parity the last tile did NOT use
       mbar_wait(&o_done[i], (n_tiles - 1) & 1);
       tc_fence_after();
       const bool ok = r < nrows;  // every lane joins the .sync.aligned TMEM loads; valid rows store
       const long long trow = row_base + i * TPT + (ok ? r : 0) / G;  // token row in [0, T)
       const int head = kvh * G + (ok ? r : 0) % G;
-      const float inv = l > 0.f ? 1.f / l : 0.f;
+      const float inv = lt > 0.f ? 1.f / lt : 0.f;
 #pragma unroll
-      for (int c = 0; c < DH / 32; ++c) {
+      for (int c = 0; c < OH / 32; ++c) {
         uint32_t ov[32];
         tmem_ld32(tO + c * 32, ov);
         tmem_ld_wait();
         if (!ok) continue;
+        const int col = h * OH + c * 32;
         if (p.kv_splits > 1) {
           // unnormalised partial at scale m_used; combined by attn_split_combine_kernel
           float4* dst =
-              reinterpret_cast<float4*>(p.split_o + (((long long)ks * p.n_tokens + trow) * p.hq + head) * DH + c * 32);
+              reinterpret_cast<float4*>(p.split_o + (((long long)ks * p.n_tokens + trow) * p.hq + head) * DH + col);
 #pragma unroll
           for (int e = 0; e < 8; ++e)
             dst[e] = make_float4(__uint_as_float(ov[4 * e]), __uint_as_float(ov[4 * e + 1]),
                                  __uint_as_float(ov[4 * e + 2]), __uint_as_float(ov[4 * e + 3]));
         } else {
-          uint4* dst = reinterpret_cast<uint4*>(p.o + trow * p.ldo + (long long)head * DH + c * 32);
+          uint4* dst = reinterpret_cast<uint4*>(p.o + trow * p.ldo + (long long)head * DH + col);
 #pragma unroll
           for (int e = 0; e < 4; ++e)
             dst[e] = make_uint4(pack_bf16(__uint_as_float(ov[8 * e]) * inv, __uint_as_float(ov[8 * e + 1]) * inv),
@@ -422,8 +457,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                                 pack_bf16(__uint_as_float(ov[8 * e + 6]) * inv, __uint_as_float(ov[8 * e + 7]) * inv));
         }
       }
-      if (ok && p.kv_splits > 1) p.split_ml[((long long)ks * p.n_tokens + trow) * p.hq + head] = make_float2(m_used, l);
-    } else if (p.kv_splits > 1 && n_tiles == 0 && r < nrows) {
+      if (ok && h == 0 && p.kv_splits > 1)
+        p.split_ml[((long long)ks * p.n_tokens + trow) * p.hq + head] = make_float2(m_used, lt);
+    } else if (p.kv_splits > 1 && n_tiles == 0 && r < nrows && h == 0) {
       // empty split: mark the partial as absent
       const long long trow = row_base + i * TPT + r / G;
       p.split_ml[((long long)ks * p.n_tokens + trow) * p.hq + kvh * G + r % G] = make_float2(-INFINITY, 0.f);
@@ -431,7 +467,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (warp == NS + 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
@@ -464,12 +500,12 @@ __global__ void __launch_bounds__(256) attn_split_combine_kernel(AttnParams p) {
   for (int e = 0; e < PER; ++e) dst[lane + 32 * e] = __float2bfloat16(acc[e] * inv);
 }
 
-template <int DH>
+template <int DH, int SPL>
 int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
   using C = TcCfg<DH>;
   static bool attr = false;
   if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(attn_tc_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    CUDA_TRY(cudaFuncSetAttribute(attn_tc_kernel<DH, SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     attr = true;
   }
   // plane view: rows = hkv * slots, cols = dh
@@ -492,7 +528,7 @@ int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
     if (k >= 2 && (size_t)k * p.n_tokens * p.hq * (DH * 4 + 8) <= p.split_bytes) q.kv_splits = k;
   }
   dim3 grid(qblocks * q.kv_splits, p.hkv, n_seqs);
-  CUDA_TRY(launch_k(attn_tc_kernel<DH>, grid, dim3(THREADS), C::SMEM, st, tk, tv, q));
+  CUDA_TRY(launch_k(attn_tc_kernel<DH, SPL>, grid, dim3(Roles<SPL>::THREADS), C::SMEM, st, tk, tv, q));
   CUDA_TRY(cudaGetLastError());
   if (q.kv_splits > 1) {
     CUDA_TRY(launch_k(attn_split_combine_kernel<DH>, dim3(p.n_tokens, (p.hq + 7) / 8), dim3(256), 0, st, q));
@@ -519,8 +555,12 @@ int launch_attention_tc(const AttnParams& p, int head_dim, int n_seqs, int max_n
   if (!attention_tc_supported(p, head_dim))
     return set_error(RDKV_ERR_ARG, "attention_tc: unsupported shape (dh %d, group %d, block %d)", head_dim,
                      p.hq / p.hkv, p.block_size);
-  if (head_dim == 64) return launch_tc<64>(p, n_seqs, max_new, st);
-  return launch_tc<128>(p, n_seqs, max_new, st);
+  static const int spl = [] {  // softmax warps per query row (RDKV_ATTN_SPL=2: two, 640 threads; measured slower)
+    const char* e = std::getenv("RDKV_ATTN_SPL");
+    return e && e[0] == '2' ? 2 : 1;
+  }();
+  if (head_dim == 64) return spl == 2 ? launch_tc<64, 2>(p, n_seqs, max_new, st) : launch_tc<64, 1>(p, n_seqs, max_new, st);
+  return spl == 2 ? launch_tc<128, 2>(p, n_seqs, max_new, st) : launch_tc<128, 1>(p, n_seqs, max_new, st);
 }
 
 }  // namespace rdkv
