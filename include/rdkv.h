@@ -168,6 +168,16 @@ RDKV_API int rdkv_kv_unpack(const rdkv_unpack_job* jobs_dev, int n_jobs, int max
                             int layers, int kv_heads, int head_dim, int64_t pool_slots,
                             int elem_width, int layer_begin, int layer_end, void* stream);
 
+/* rdkv_kv_unpack for one tensor-parallel rank: the payloads hold src_kv_heads
+ * heads (the full model's .rdkv layout) and heads [head_begin, head_begin +
+ * kv_heads) are unpacked into a pool of kv_heads heads.  Each head is a
+ * contiguous [n][dh] run per (layer, K|V) of the head-major payload, so a rank
+ * moves exactly its share. */
+RDKV_API int rdkv_kv_unpack_heads(const rdkv_unpack_job* jobs_dev, int n_jobs, int max_tokens,
+                                  const int32_t* block_table_dev, int block_size, void* pool_base, int layers,
+                                  int kv_heads, int head_dim, int64_t pool_slots, int elem_width, int layer_begin,
+                                  int layer_end, int head_begin, int src_kv_heads, void* stream);
+
 /* Copy the first n_tokens slots of pool block src_block into dst_block, in every
  * (layer, K|V, head) plane: one strided DMA (cudaMemcpy2DAsync, L*2*Hkv rows).
  * Copy-on-write of a resident prefix's partial last block, so a query can append

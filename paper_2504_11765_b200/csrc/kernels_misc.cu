@@ -25,10 +25,14 @@ __device__ __forceinline__ uint4 ld_stream(const void* p) {
 // One warp moves one segment = (job, layer, k|v, head, block): a contiguous
 // run of up to block_size*dh elements in the blob and in the pool plane.
 // 16-byte loads, UNROLL of them in flight per lane.
+// Heads [h0, h0 + hkv) of a payload holding src_hkv heads land in a pool of hkv
+// heads (a tensor-parallel rank reads its own heads of a full-model blob: each
+// is a contiguous [n][dh] run of the head-major payload).
 template <int SRC_W>
 __global__ void __launch_bounds__(256) kv_unpack_kernel(const UnpackJob* __restrict__ jobs, const int* __restrict__ bt,
                                                         int block_size, __nv_bfloat16* __restrict__ pool, int layer0,
-                                                        int layers, int hkv, int dh, long long slots) {
+                                                        int layers, int hkv, int dh, long long slots, int h0,
+                                                        int src_hkv) {
   pdl_trigger();
   pdl_wait();
   const UnpackJob jb = jobs[blockIdx.y];
@@ -39,10 +43,12 @@ __global__ void __launch_bounds__(256) kv_unpack_kernel(const UnpackJob* __restr
   for (long long seg = (long long)blockIdx.x * 8 + warp; seg < nseg; seg += (long long)gridDim.x * 8) {
     const int b = (int)(seg % nblk);
     const long long plane = (long long)layer0 * 2 * hkv + seg / nblk;  // (l*2 + kv)*hkv + h
+    const long long lkv = plane / hkv;                                 // l*2 + kv
+    const long long src_plane = lkv * src_hkv + h0 + plane % hkv;
     const int t0 = b * block_size;
     const int ntok = min(block_size, jb.n_tokens - t0);
     const long long n_el = (long long)ntok * dh;
-    const long long src_off = plane * (long long)jb.n_tokens * dh + (long long)t0 * dh;
+    const long long src_off = src_plane * (long long)jb.n_tokens * dh + (long long)t0 * dh;
     const long long dst_off = plane * slots * dh + (long long)bt[jb.first_block + b] * block_size * dh;
     __nv_bfloat16* dst = pool + dst_off;
     if constexpr (SRC_W == 2) {
@@ -196,11 +202,15 @@ __global__ void argmax_final_kernel(const float2* __restrict__ part, int* __rest
 
 int launch_kv_unpack(const UnpackJob* jobs_dev, int n_jobs, int max_tokens, const int* bt, int block_size,
                      void* pool, int layer_begin, int layer_end, int hkv, int dh, long long slots, int elem_width,
-                     cudaStream_t st) {
+                     cudaStream_t st, int head_begin, int src_kv_heads) {
   const int layers = layer_end - layer_begin;
   if (n_jobs <= 0 || max_tokens <= 0 || layers <= 0) return 0;
   if (dh % 8 != 0) return set_error(RDKV_ERR_ARG, "unpack: head_dim must be a multiple of 8");
   if (elem_width != 2 && elem_width != 4) return set_error(RDKV_ERR_ARG, "unpack: elem_width must be 2 or 4");
+  if (src_kv_heads <= 0) src_kv_heads = hkv;
+  if (head_begin < 0 || head_begin + hkv > src_kv_heads)
+    return set_error(RDKV_ERR_ARG, "unpack: heads [%d, %d) outside the payload's %d", head_begin, head_begin + hkv,
+                     src_kv_heads);
   const long long segs = (long long)layers * 2 * hkv * ((max_tokens + block_size - 1) / block_size);
   long long gx = (segs + 7) / 8;
   const long long cap = 4LL * num_sms() * 4;  // ~4 CTAs/SM resident, a few waves
@@ -208,9 +218,11 @@ int launch_kv_unpack(const UnpackJob* jobs_dev, int n_jobs, int max_tokens, cons
   dim3 grid((unsigned)gx, (unsigned)n_jobs);
   auto* dst = static_cast<__nv_bfloat16*>(pool);
   if (elem_width == 2)
-    CUDA_TRY(launch_k(kv_unpack_kernel<2>, grid, dim3(256), 0, st, jobs_dev, bt, block_size, dst, layer_begin, layers, hkv, dh, slots));
+    CUDA_TRY(launch_k(kv_unpack_kernel<2>, grid, dim3(256), 0, st, jobs_dev, bt, block_size, dst, layer_begin, layers,
+                      hkv, dh, slots, head_begin, src_kv_heads));
   else
-    CUDA_TRY(launch_k(kv_unpack_kernel<4>, grid, dim3(256), 0, st, jobs_dev, bt, block_size, dst, layer_begin, layers, hkv, dh, slots));
+    CUDA_TRY(launch_k(kv_unpack_kernel<4>, grid, dim3(256), 0, st, jobs_dev, bt, block_size, dst, layer_begin, layers,
+                      hkv, dh, slots, head_begin, src_kv_heads));
   CUDA_TRY(cudaGetLastError());
   return 0;
 }

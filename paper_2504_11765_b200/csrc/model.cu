@@ -401,11 +401,20 @@ int rdkv_kv_copy_block(void* pool_base, int layers, int kv_heads, int head_dim, 
 int rdkv_kv_unpack(const rdkv_unpack_job* jobs_dev, int n_jobs, int max_tokens, const int32_t* block_table_dev,
                    int block_size, void* pool_base, int layers, int kv_heads, int head_dim, int64_t pool_slots,
                    int elem_width, int layer_begin, int layer_end, void* stream) {
+  return rdkv_kv_unpack_heads(jobs_dev, n_jobs, max_tokens, block_table_dev, block_size, pool_base, layers, kv_heads,
+                              head_dim, pool_slots, elem_width, layer_begin, layer_end, 0, kv_heads, stream);
+}
+
+int rdkv_kv_unpack_heads(const rdkv_unpack_job* jobs_dev, int n_jobs, int max_tokens, const int32_t* block_table_dev,
+                         int block_size, void* pool_base, int layers, int kv_heads, int head_dim, int64_t pool_slots,
+                         int elem_width, int layer_begin, int layer_end, int head_begin, int src_kv_heads,
+                         void* stream) {
   if (block_size <= 0 || !pool_base || !jobs_dev) return set_error(RDKV_ERR_ARG, "kv_unpack: bad arguments");
   if (layer_begin < 0 || layer_end > layers || layer_begin > layer_end)
     return set_error(RDKV_ERR_ARG, "kv_unpack: bad layer range [%d, %d) of %d", layer_begin, layer_end, layers);
   return launch_kv_unpack(jobs_dev, n_jobs, max_tokens, block_table_dev, block_size, pool_base, layer_begin,
-                          layer_end, kv_heads, head_dim, pool_slots, elem_width, static_cast<cudaStream_t>(stream));
+                          layer_end, kv_heads, head_dim, pool_slots, elem_width, static_cast<cudaStream_t>(stream),
+                          head_begin, src_kv_heads);
 }
 
 }  // extern "C"

@@ -65,6 +65,9 @@ _N_SIG = {
     "rdkv_forward": (C.c_int, [C.c_void_p, C.POINTER(RdkvBatch), C.c_void_p, C.c_size_t, C.c_void_p]),
     "rdkv_kv_unpack": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int,
                                  C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_void_p]),
+    "rdkv_kv_unpack_heads": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int,
+                                       C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       C.c_void_p]),
     "rdkv_kv_copy_block": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int,
                                      C.c_int, C.c_void_p]),
     "rdkv_ipc_handle": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),
@@ -287,20 +290,24 @@ class DeviceModel:
 
 def kv_unpack(pool: KvPool, jobs: Sequence[tuple[torch.Tensor, int, int]], block_table: torch.Tensor,
               elem_width: int = 2, stream: torch.cuda.Stream | None = None, layers: tuple[int, int] | None = None,
-              jobs_dev: torch.Tensor | None = None) -> None:
+              jobs_dev: torch.Tensor | None = None, heads: tuple[int, int] | None = None) -> None:
     """K3: unpack device-resident blob payloads into the pool.
 
     ``jobs`` = (payload device tensor, n_tokens, first_block index into the flat
-    ``block_table`` int32 device tensor)."""
+    ``block_table`` int32 device tensor).  ``heads`` = (first head, heads in the
+    payload) when the payloads hold more KV heads than the pool — a
+    tensor-parallel rank reading its share of full-model blobs."""
     if not jobs:
         return
     if jobs_dev is None:
         jobs_dev = pack_unpack_jobs(jobs).to(pool.data.device, non_blocking=True)
     s = pool.spec
     l0, l1 = layers if layers is not None else (0, s.layers)
-    _lib.check(_L().rdkv_kv_unpack(jobs_dev.data_ptr(), len(jobs), max(n for _, n, _ in jobs), block_table.data_ptr(),
-                                   pool.block_size, pool.data.data_ptr(), s.layers, s.kv_heads, s.head_dim,
-                                   pool.slots, elem_width, l0, l1, _stream_ptr(stream)))
+    h0, src_heads = heads if heads is not None else (0, s.kv_heads)
+    _lib.check(_L().rdkv_kv_unpack_heads(jobs_dev.data_ptr(), len(jobs), max(n for _, n, _ in jobs),
+                                         block_table.data_ptr(), pool.block_size, pool.data.data_ptr(), s.layers,
+                                         s.kv_heads, s.head_dim, pool.slots, elem_width, l0, l1, h0, src_heads,
+                                         _stream_ptr(stream)))
     # the job table may have been staged on another stream: keep its memory until this launch has read it
     jobs_dev.record_stream(stream if stream is not None else torch.cuda.current_stream(pool.data.device))
 
@@ -325,7 +332,8 @@ class LayerStreamer:
         self.handles = (C.c_void_p * L)()
 
     def launch(self, pool: KvPool, jobs, block_table: torch.Tensor, jobs_dev: torch.Tensor, main: torch.cuda.Stream,
-               first_event=None, last_event=None, h2d: Sequence[tuple[torch.Tensor, torch.Tensor]] = ()):
+               first_event=None, last_event=None, h2d: Sequence[tuple[torch.Tensor, torch.Tensor]] = (),
+               heads: tuple[int, int] | None = None):
         """Enqueue per-layer [H2D ->] unpack; returns the event-handle array for rdkv_forward.
         ``h2d`` = (pinned host payload, device staging buffer) pairs still to be copied."""
         L = len(self.events)
@@ -351,7 +359,8 @@ class LayerStreamer:
                     first_event.record(self.stream)
                 if h2d:
                     self.stream.wait_event(self.copied[l])
-                kv_unpack(pool, jobs, block_table, stream=self.stream, layers=(l, l + 1), jobs_dev=jobs_dev)
+                kv_unpack(pool, jobs, block_table, stream=self.stream, layers=(l, l + 1), jobs_dev=jobs_dev,
+                          heads=heads)
                 self.events[l].record(self.stream)
         if last_event is not None:
             last_event.record(self.stream)
@@ -558,6 +567,7 @@ class Engine:
         self.pool = KvPool(spec, work_blocks + tier_blocks, block_size, self.device)
         self.copy_stream = torch.cuda.Stream(device=self.device)
         self.resident = ResidentKvTier(self.pool, tier_blocks)
+        self.tp_rank = 0  # set by multi.TpGroup: which KV heads of full-model blobs this rank owns
         self.graphs = GraphRunner(self)
         self.streamer = LayerStreamer(self)
 

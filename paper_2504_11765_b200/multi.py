@@ -201,6 +201,7 @@ class TpGroup:
         lib = _L()
         self.engine = engine
         self.rank, self.size = dist.get_rank(group), dist.get_world_size(group)
+        engine.tp_rank = self.rank  # its KV heads of full-model blobs: [rank * kv_heads, (rank + 1) * kv_heads)
         self.max_elems = max_tokens * engine.spec.hidden
         nbytes = int(lib.rdkv_tp_comm_bytes(self.max_elems, self.size))
         self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=engine.device)

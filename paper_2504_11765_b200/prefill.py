@@ -103,12 +103,20 @@ def prefill_batch(engine: Engine, requests: Sequence[PrefillRequest], timed: boo
                     dev = engine.stage(host, stream=engine.copy_stream)
                 staged.append(dev)
                 jobs.append((dev, n_cached, i))
+        # full-model blobs on a tensor-parallel rank: unpack only this rank's KV heads
+        heads = None
+        src = {int(requests[i].lookup.blob.header.kv_heads) for _, _, i in jobs}
+        if len(src) > 1:
+            raise ValueError("one batch mixes payloads with different KV-head counts")
+        if src and src != {engine.spec.kv_heads}:
+            (n_src,) = src
+            heads = (engine.tp_rank * engine.spec.kv_heads, n_src)
         plan = BatchPlan(seqs, pool.block_size, engine.device)
         if staged:
             main.wait_stream(engine.copy_stream)
         ujobs = [(d, n, i * plan.bt_stride) for d, n, i in jobs]
         graphed = None
-        if use_graph and not timed and unpack_events is None and not pending_h2d:
+        if use_graph and not timed and unpack_events is None and not pending_h2d and heads is None:
             graphed = engine.graphs.run(plan, ujobs)  # [K3 unpack ->] forward as one CUDA-graph replay
         if graphed is not None:
             logits, nxt = graphed
@@ -122,12 +130,13 @@ def prefill_batch(engine: Engine, requests: Sequence[PrefillRequest], timed: boo
                     ua, ub = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     unpack_events.append((ua, ub))
                 jobs_dev = pack_unpack_jobs(ujobs).to(engine.device, non_blocking=True)
-                handles = engine.streamer.launch(pool, ujobs, _bt_view(plan), jobs_dev, main, ua, ub, h2d=pending_h2d)
+                handles = engine.streamer.launch(pool, ujobs, _bt_view(plan), jobs_dev, main, ua, ub, h2d=pending_h2d,
+                                                 heads=heads)
             elif ujobs:
                 if unpack_events is not None:
                     ua, ub = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     ua.record(main)
-                kv_unpack(pool, ujobs, _bt_view(plan), elem_width=2, stream=main)
+                kv_unpack(pool, ujobs, _bt_view(plan), elem_width=2, stream=main, heads=heads)
                 if unpack_events is not None:
                     ub.record(main)
                     unpack_events.append((ua, ub))

@@ -102,13 +102,17 @@ def _fw_worker(rank, world, port, q, model, layers):
         full = init_weights(spec, seed=4)
         prefix = combo_tokens([3, 9], [256, 200], spec.vocab)
         new = query_tokens(2, 48, spec.vocab)
-        ref_logits = None
+        ref_logits, blob_parts = None, [None]
         if rank == 0:  # the same weights on one GPU, no TP
+            from paper_2504_11765_b200.codec import make_header
             e1 = Engine(spec, weights=full, pool_tokens=2048)
             kv = e1.generate_doc_kv(prefix)
             ref_logits, _ = e1.prefill([QueryRequest(new, kv, len(prefix))])
             ref_logits = ref_logits[0].float().cpu()
+            # the full-model .rdkv payload of the prefix (all KV heads), as the shared store holds it
+            blob_parts = [(make_header(spec.profile(), (3, 9), len(prefix), 0), kv.view(torch.uint8).cpu())]
             del e1, kv
+        dist.broadcast_object_list(blob_parts, src=0)
         eng = Engine(tp_spec(spec, world), weights=shard_weights(full, rank, world), pool_tokens=2048)
         del full
         tp = TpGroup(eng, max_tokens=1024)
@@ -116,11 +120,22 @@ def _fw_worker(rank, world, port, q, model, layers):
         logits, nxt = eng.prefill([QueryRequest(new, kv, len(prefix))])
         torch.cuda.synchronize()
         got = logits[0].float().cpu()
+        # the same query over the FULL-model blob from the host tier: this rank unpacks only its KV heads
+        from paper_2504_11765_b200.codec import KvBlob
+        from paper_2504_11765_b200.prefill import PrefillRequest, prefill_batch
+        from paper_2504_11765_b200.store import LookupResult, Outcome
+        hdr, payload = blob_parts[0]
+        fb = KvBlob.trusted(hdr, payload.pin_memory())
+        r2 = prefill_batch(eng, [PrefillRequest(LookupResult(Outcome.MEMORY_HIT, fb, 0), None, new)], timed=False)
+        torch.cuda.synchronize()
+        got_full_blob = r2.logits[0].float().cpu()
         out = [None] * world
         dist.all_gather_object(out, got)
         res = {"rank": rank, "same_on_all_ranks": all(torch.equal(o, got) for o in out), "first": int(nxt[0])}
+        res["full_blob_vs_own_kv"] = rel_err(got_full_blob, got)
         if rank == 0:
             res["rel_err"] = rel_err(got, ref_logits)
+            res["full_blob_rel_err"] = rel_err(got_full_blob, ref_logits)
             res["ref_first"] = int(torch.argmax(ref_logits))
             top2 = torch.topk(ref_logits, 2).values
             res["margin"] = float(top2[0] - top2[1])
@@ -137,6 +152,10 @@ def test_tp_forward_matches_single_gpu(world):
     res = dict(_spawn(_fw_worker, world, "gqa-tp", None))
     r0 = res[0]
     assert all(r["same_on_all_ranks"] for r in res.values())   # replicated residual stream after every all-reduce
+    # head-range unpack of the full-model blob (its KV comes from the unsharded forward,
+    # so it differs from the rank's own KV by the bf16 rounding of the TP partials)
+    assert all(r["full_blob_vs_own_kv"] <= 1e-2 for r in res.values()), res
+    assert r0["full_blob_rel_err"] <= 2e-2, r0
     assert r0["rel_err"] <= 2e-2, r0
     if r0["margin"] > 4 * r0["abs_err"]:
         assert r0["first"] == r0["ref_first"]
