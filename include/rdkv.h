@@ -196,6 +196,12 @@ RDKV_API int rdkv_ipc_handle(const void* dev_ptr, void* handle_out, int64_t* off
 RDKV_API int rdkv_ipc_open(const void* handle, void** base_out);
 RDKV_API int rdkv_ipc_close(void* base);
 
+/* Strided device copy (cudaMemcpy2DAsync, any device to any device through UVA
+ * / IPC mappings): one TP rank's KV heads into the gathered full-model payload
+ * on the root rank ([L][2] rows of Hkv/T heads at a pitch of Hkv heads). */
+RDKV_API int rdkv_memcpy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                            void* stream);
+
 /* K3p: copy n_blocks KV blocks src_blocks[i] of pool src (possibly a peer's,
  * through rdkv_ipc_open) into dst_blocks[i] of the local pool dst, every
  * (layer, K|V, head) plane.  Pools are [L][2][Hkv][slots][dh] bf16; block

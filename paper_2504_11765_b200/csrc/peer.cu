@@ -127,3 +127,11 @@ extern "C" int rdkv_kv_peer_gather(const void* src_pool, int64_t src_slots, cons
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
+
+extern "C" int rdkv_memcpy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                              void* stream) {
+  if (!dst || !src || width > dpitch || width > spitch) return set_error(RDKV_ERR_ARG, "memcpy_2d: bad arguments");
+  CUDA_TRY(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDefault,
+                             static_cast<cudaStream_t>(stream)));
+  return 0;
+}

@@ -73,6 +73,7 @@ _N_SIG = {
     "rdkv_ipc_handle": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),
     "rdkv_ipc_open": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "rdkv_ipc_close": (C.c_int, [C.c_void_p]),
+    "rdkv_memcpy_2d": (C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_void_p]),
     "rdkv_kv_peer_gather": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int,
                                       C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]),
     "rdkv_tp_comm_bytes": (C.c_size_t, [C.c_size_t, C.c_int]),

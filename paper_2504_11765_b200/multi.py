@@ -245,9 +245,83 @@ class TpGroup:
         _lib.check(_L().rdkv_tp_reduce_resid(self.comm, x.data_ptr(), x.stride(0), rows, cols, buf,
                                              _stream_ptr(stream)))
 
+    def gather_payload(self, local: torch.Tensor, n_tokens: int, root: int = 0) -> torch.Tensor | None:
+        """Assemble the full-model payload [L][2][Hkv][n][dh] from every rank's share
+        [L][2][Hkv/T][n][dh] (document prefill on a TP instance) into HBM on ``root``:
+        each rank writes its heads with one strided copy straight into the root's
+        gather buffer over NVLink (CUDA-IPC mapping), then the group synchronises.
+        Returns the full payload (bf16, flat) on ``root``, None elsewhere."""
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        from . import _lib
+        from .engine import _L
+
+        s = self.engine.spec
+        part = s.layers * 2 * s.kv_heads * n_tokens * s.head_dim  # elements of one rank's share
+        full = part * self.size
+        if not hasattr(self, "_gather") or self._gather_elems < full:
+            # (re)size the root's gather buffer and (re)map it everywhere
+            if hasattr(self, "_gather") and self._gather_peer:
+                _L().rdkv_ipc_close(self._gather_peer)
+            info = [None]
+            if self.rank == root:
+                self._gather_buf = torch.empty(full, dtype=torch.bfloat16, device=self.engine.device)
+                h = (C.c_ubyte * 64)()
+                off = C.c_int64()
+                _lib.check(_L().rdkv_ipc_handle(C.c_void_p(self._gather_buf.data_ptr()), h, C.byref(off)))
+                info = [(bytes(h), int(off.value))]
+            dist.broadcast_object_list(info, src=root)
+            self._gather_peer = None
+            if self.rank == root:
+                self._gather = self._gather_buf.data_ptr()
+            else:
+                base = C.c_void_p()
+                _lib.check(_L().rdkv_ipc_open((C.c_ubyte * 64).from_buffer_copy(info[0][0]), C.byref(base)))
+                self._gather_peer = base.value
+                self._gather = base.value + info[0][1]
+            self._gather_elems = full
+        width = s.kv_heads * n_tokens * s.head_dim * 2          # bytes of this rank's heads per (layer, K|V)
+        pitch = width * self.size                               # bytes of all heads per (layer, K|V)
+        dst = self._gather + self.rank * width
+        st = torch.cuda.current_stream(self.engine.device)
+        _lib.check(_L().rdkv_memcpy_2d(dst, pitch, local.data_ptr(), width, width, s.layers * 2, st.cuda_stream))
+        st.synchronize()
+        dist.barrier()
+        return self._gather_buf[:full] if self.rank == root else None
+
+    def generate_blob(self, tokens, doc_ids, root: int = 0):
+        """Document-KV generation on a TP instance (the ``generate()`` plugin body for
+        C5): every rank prefills the combination for its KV heads, the shares are
+        gathered over NVLink on ``root``, hashed there on the GPU and copied once
+        into pinned host memory.  Returns the full-model ``KvBlob`` on ``root``."""
+        from dataclasses import replace
+
+        import numpy as np
+
+        from .codec import KvBlob, fnv1a64_device, make_header
+
+        eng = self.engine
+        n = len(tokens)
+        local = eng.generate_doc_kv(np.asarray(tokens, np.int32))
+        full = self.gather_payload(local, n, root)
+        if self.rank != root:
+            return None
+        s = eng.spec
+        full_spec = replace(s, n_heads=s.n_heads * self.size, kv_heads=s.kv_heads * self.size, ffn=s.ffn * self.size)
+        raw = full.view(torch.uint8)
+        checksum = fnv1a64_device(raw)
+        host = torch.empty(raw.numel(), dtype=torch.uint8, pin_memory=True)
+        host.copy_(raw)
+        return KvBlob.trusted(make_header(full_spec.profile(), tuple(doc_ids), n, checksum), host)
+
     def close(self) -> None:
         from .engine import _L
 
+        if getattr(self, "_gather_peer", None):
+            _L().rdkv_ipc_close(self._gather_peer)
+            self._gather_peer = None
         if self.comm:
             _L().rdkv_model_set_tp(self.engine.model._h, None)
             _L().rdkv_tp_comm_destroy(self.comm)

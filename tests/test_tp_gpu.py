@@ -111,11 +111,19 @@ def _fw_worker(rank, world, port, q, model, layers):
             ref_logits = ref_logits[0].float().cpu()
             # the full-model .rdkv payload of the prefix (all KV heads), as the shared store holds it
             blob_parts = [(make_header(spec.profile(), (3, 9), len(prefix), 0), kv.view(torch.uint8).cpu())]
+            single_kv = kv.float().cpu()
             del e1, kv
         dist.broadcast_object_list(blob_parts, src=0)
         eng = Engine(tp_spec(spec, world), weights=shard_weights(full, rank, world), pool_tokens=2048)
         del full
         tp = TpGroup(eng, max_tokens=1024)
+        # document-KV generation on the TP instance: shares gathered over NVLink into the full blob
+        gblob = tp.generate_blob(prefix, (3, 9))
+        if rank == 0:
+            from paper_2504_11765_b200.codec import fnv1a64
+            gathered = gblob.payload.view(torch.bfloat16).float()
+            gen_ok = (gblob.header.kv_heads == spec.kv_heads and gblob.header.checksum == fnv1a64(gblob.payload)
+                      and rel_err(gathered, single_kv) <= 2e-2)
         kv = eng.generate_doc_kv(prefix)                          # this rank's KV heads only
         logits, nxt = eng.prefill([QueryRequest(new, kv, len(prefix))])
         torch.cuda.synchronize()
@@ -134,6 +142,7 @@ def _fw_worker(rank, world, port, q, model, layers):
         res = {"rank": rank, "same_on_all_ranks": all(torch.equal(o, got) for o in out), "first": int(nxt[0])}
         res["full_blob_vs_own_kv"] = rel_err(got_full_blob, got)
         if rank == 0:
+            res["gathered_blob_ok"] = gen_ok
             res["rel_err"] = rel_err(got, ref_logits)
             res["full_blob_rel_err"] = rel_err(got_full_blob, ref_logits)
             res["ref_first"] = int(torch.argmax(ref_logits))
@@ -156,6 +165,7 @@ def test_tp_forward_matches_single_gpu(world):
     # so it differs from the rank's own KV by the bf16 rounding of the TP partials)
     assert all(r["full_blob_vs_own_kv"] <= 1e-2 for r in res.values()), res
     assert r0["full_blob_rel_err"] <= 2e-2, r0
+    assert r0["gathered_blob_ok"], r0                            # TP generation -> full-model .rdkv blob
     assert r0["rel_err"] <= 2e-2, r0
     if r0["margin"] > 4 * r0["abs_err"]:
         assert r0["first"] == r0["ref_first"]
@@ -166,6 +176,7 @@ def test_tp4_llama70b_shape_two_layers():
     res = dict(_spawn(_fw_worker, 4, "llama-3-70b", 2))
     r0 = res[0]
     assert all(r["same_on_all_ranks"] for r in res.values())
+    assert r0["gathered_blob_ok"] and r0["full_blob_rel_err"] <= 2e-2, r0
     assert r0["rel_err"] <= 2e-2, r0
     if r0["margin"] > 4 * r0["abs_err"]:
         assert r0["first"] == r0["ref_first"]
