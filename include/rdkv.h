@@ -320,7 +320,13 @@ typedef struct rdkv_batch {
                                   enables split-KV attention for small batches)      */
   void* const* layer_ready;     /* optional [layers] cudaEvent_t: layer l's attention
                                   waits for event l (layer-wise KV streaming)        */
+  int32_t flags;               /* RDKV_BATCH_ROW_DETERMINISTIC: every row's arithmetic
+                                  independent of the batch shape (no split-K GEMMs,
+                                  no split-KV attention), so a prefix's KV is
+                                  bit-identical to the same rows of a longer prefill */
 } rdkv_batch;
+
+#define RDKV_BATCH_ROW_DETERMINISTIC 1
 
 /* Make the model one rank of a TP group: its descriptor / weights are this
  * rank's shard (n_heads, kv_heads, ffn divided by the group size; wqkv rows,

@@ -230,6 +230,12 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     return !(e && e[0] == 'm');
   }();
 
+  if (b->flags & RDKV_BATCH_ROW_DETERMINISTIC) {  // no shape-dependent reduction orders
+    ws.splitk = nullptr;
+    ws.splitk_bytes = 0;
+    ws.attn_split = nullptr;
+    ws.attn_split_bytes = 0;
+  }
   LAUNCH(RDKV_PROF_MISC, 0.0, launch_embed(b->tokens, W(m, 0), ws.x, T, d.hidden, d.vocab, st));
   // small batches run the residual GEMMs split-K; their finalize also applies the
   // following RMSNorm, saving a launch per norm

@@ -48,7 +48,7 @@ class RdkvBatch(C.Structure):
                 ("seq_new", C.c_void_p), ("seq_cached", C.c_void_p), ("block_table", C.c_void_p),
                 ("last_row", C.c_void_p), ("kv_base", C.c_void_p), ("kv_slots", C.c_int64),
                 ("logits", C.c_void_p), ("next_token", C.c_void_p), ("max_ctx", C.c_int32),
-                ("layer_ready", C.c_void_p)]
+                ("layer_ready", C.c_void_p), ("flags", C.c_int32)]
 
 
 class RdkvUnpackJob(C.Structure):
@@ -207,6 +207,7 @@ class BatchPlan:
         self.bt_stride, self.block_size = bt_stride, block_size
         self.n_new, self.n_cached = n_new, cached
         self.max_ctx = int((n_new + cached).max())
+        self.flags = 0
         self.rebase(host.to(device, non_blocking=True))
 
     _FIELDS = ("tokens", "pos", "slot", "seq_start", "seq_new", "seq_cached", "block_table", "last_row")
@@ -231,7 +232,8 @@ class BatchPlan:
             kv_base=kv_base, kv_slots=kv_slots,
             logits=logits.data_ptr() if logits is not None else None,
             next_token=next_token.data_ptr() if next_token is not None else None, max_ctx=self.max_ctx,
-            layer_ready=C.cast(layer_ready, C.c_void_p).value if layer_ready is not None else None)
+            layer_ready=C.cast(layer_ready, C.c_void_p).value if layer_ready is not None else None,
+            flags=self.flags)
 
 
 # ----------------------------------------------------------------- the model handle
@@ -605,14 +607,19 @@ class Engine:
 
     # -------------------------------------------------------------- generation
     def generate_doc_kv(self, tokens: np.ndarray, out: torch.Tensor | None = None,
-                        stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+                        stream: torch.cuda.Stream | None = None, row_deterministic: bool = True) -> torch.Tensor:
         """Document KV of ``tokens`` (positions 0..n-1) in the blob payload layout
-        [L][2][Hkv][n][dh] bf16, as a flat device tensor."""
+        [L][2][Hkv][n][dh] bf16, as a flat device tensor.  ``row_deterministic``
+        keeps every row's arithmetic independent of n (no split-KV attention for
+        short documents), so the KV of a prefix is bit-identical to the same rows
+        of a longer combination's KV (SURVEY H-e)."""
         s, n = self.spec, len(tokens)
         numel = s.layers * 2 * s.kv_heads * n * s.head_dim
         if out is None:
             out = torch.empty(numel, dtype=torch.bfloat16, device=self.device)
         plan = BatchPlan([SeqPlan(np.asarray(tokens, np.int32), 0, [0])], block_size=n, device=self.device)
+        if row_deterministic:
+            plan.flags |= 1  # RDKV_BATCH_ROW_DETERMINISTIC
         self.model.forward(plan, out.data_ptr(), n, stream=stream)
         out._plan = plan  # metadata lifetime follows the output
         return out

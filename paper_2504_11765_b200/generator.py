@@ -46,22 +46,66 @@ class KvGenerator:
             raise ValueError("token_count must be >= 1")
         eng = self.engine
         with torch.cuda.device(eng.device):
-            kv = eng.generate_doc_kv(toks)
-            raw = kv.view(torch.uint8)
-            main = torch.cuda.current_stream()
             # D2H into the host tier on the copy stream while the GPU hashes the payload
-            eng.copy_stream.wait_stream(main)
-            host = torch.empty(raw.numel(), dtype=torch.uint8, pin_memory=True)
-            with torch.cuda.stream(eng.copy_stream):
-                host.copy_(raw, non_blocking=True)
-            raw.record_stream(eng.copy_stream)
-            checksum = fnv1a64_device(raw)
-            eng.copy_stream.synchronize()
-        header = make_header(self.profile, ids, len(toks), checksum)
+            return self._blob_from_device(ids, len(toks), eng.generate_doc_kv(toks))
+
+    def _blob_from_device(self, ids: tuple[int, ...], n: int, kv: torch.Tensor) -> KvBlob:
+        """Header + pinned host copy of a device payload, checksum on the GPU."""
+        eng = self.engine
+        raw = kv.view(torch.uint8)
+        main = torch.cuda.current_stream(eng.device)
+        eng.copy_stream.wait_stream(main)
+        host = torch.empty(raw.numel(), dtype=torch.uint8, pin_memory=True)
+        with torch.cuda.stream(eng.copy_stream):
+            host.copy_(raw, non_blocking=True)
+        raw.record_stream(eng.copy_stream)
+        checksum = fnv1a64_device(raw)
+        eng.copy_stream.synchronize()
         if self.keep_on_device:
-            with torch.cuda.device(eng.device):
-                eng.make_resident(KvKey(self.profile.model_hash, ids), kv, len(toks))
-        return KvBlob.trusted(header, host)
+            eng.make_resident(KvKey(self.profile.model_hash, ids), kv, n)
+        return KvBlob.trusted(make_header(self.profile, ids, n, checksum), host)
+
+    def slice_prefix(self, full: torch.Tensor, n_full: int, n: int) -> torch.Tensor:
+        """Payload of the first n tokens of a combination's payload [L][2][Hkv][n_full][dh]
+        (one strided device copy)."""
+        from . import _lib
+        from .engine import _L
+
+        s = self.engine.spec
+        if n == n_full:
+            return full
+        out = torch.empty(s.layers * 2 * s.kv_heads * n * s.head_dim, dtype=torch.bfloat16, device=full.device)
+        row = s.head_dim * 2
+        _lib.check(_L().rdkv_memcpy_2d(out.data_ptr(), n * row, full.data_ptr(), n_full * row, n * row,
+                                       s.layers * 2 * s.kv_heads,
+                                       torch.cuda.current_stream(full.device).cuda_stream))
+        return out
+
+    def for_combination(self, doc_ids: Sequence[int], doc_token_counts: Sequence[int]):
+        """Generator factory for every prefix of one ordered combination: the first
+        ``generate()`` runs the combination's prefill once (row-deterministic), each
+        prefix is then a slice of it — bit-identical to generating that prefix from
+        scratch (prefetch.py:6-8), with one forward instead of k."""
+        full_ids, full_counts = tuple(int(d) for d in doc_ids), tuple(int(c) for c in doc_token_counts)
+        state: dict = {}
+
+        def factory(prefix_ids, prefix_counts):
+            ids, counts = tuple(int(d) for d in prefix_ids), tuple(int(c) for c in prefix_counts)
+            if ids != full_ids[: len(ids)] or counts != full_counts[: len(ids)]:
+                return self.for_prefix(ids, counts)  # not a prefix of this combination
+
+            def generate() -> KvBlob:
+                eng = self.engine
+                with torch.cuda.device(eng.device):
+                    if "kv" not in state:
+                        state["kv"] = eng.generate_doc_kv(self.tokens(full_ids, full_counts))
+                        state["n"] = sum(full_counts)
+                    n = sum(counts)
+                    return self._blob_from_device(ids, n, self.slice_prefix(state["kv"], state["n"], n))
+
+            return generate
+
+        return factory
 
     def for_prefix(self, doc_ids: Sequence[int], doc_token_counts: Sequence[int]) -> Callable[[], KvBlob]:
         """The ``generate`` callable for one key (prefetch.prepare / get_or_generate)."""

@@ -62,6 +62,10 @@ class MeasuredExecutor:
     token_seed: int = 0
     access_log: list[AccessRecord] = field(default_factory=list)
     generations: list[tuple[tuple[int, ...], float]] = field(default_factory=list)
+    # query_id -> WorkItem: lets a generation task find its waiting query's whole
+    # combination and run one prefill for all of that combination's prefixes
+    workload: dict | None = None
+    _combos: "OrderedDict" = field(default_factory=lambda: __import__("collections").OrderedDict())
 
     def bind(self, config: SimConfig, cache: TierMirror) -> None:
         self.cfg = config
@@ -100,12 +104,33 @@ class MeasuredExecutor:
                                             r.breakdown.prefill, first))
         return kv_load, r.breakdown.prefill
 
+    def _factory(self, ids, counts):
+        """Per-prefix generate factory; shares one combination prefill when a waiting
+        query's combination extends this prefix (KvGenerator.for_combination)."""
+        if self.workload:
+            for combo, fac in self._combos.items():
+                if combo[: len(ids)] == ids:
+                    return fac
+            return None
+        return None
+
     def generation_time(self, task: GenTask) -> float:
         ids = task.prefix
         counts = self._doc_counts(ids, task.span_tokens)
         key = KvKey(self.profile.model_hash, ids)
         t0 = time.perf_counter()
-        self.service.get_or_generate(key, self.gen.for_prefix(ids, counts))
+        fac = self._factory(ids, counts)
+        if fac is None and self.workload:
+            for q in sorted(task.waiters):
+                it = self.workload.get(q)
+                if it is not None and tuple(it.doc_ids[: self.cfg.k])[: len(ids)] == ids:
+                    combo = tuple(it.doc_ids[: self.cfg.k])
+                    fac = self.gen.for_combination(combo, tuple(it.doc_tokens[: self.cfg.k]))
+                    self._combos[combo] = fac
+                    while len(self._combos) > 4:  # each holds one combination's KV in HBM
+                        self._combos.popitem(last=False)
+                    break
+        self.service.get_or_generate(key, (fac or self.gen.for_prefix)(ids, counts))
         dt = time.perf_counter() - t0
         self.generations.append((ids, dt))
         return dt

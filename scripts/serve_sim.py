@@ -55,7 +55,7 @@ def main():
                     arrival=ArrivalSpec(rate=a.rate), k=a.k, tries=a.tries, seed=1, threshold=a.threshold,
                     memory_capacity_bytes=0)
     items = zipf_stream(a.docs, 1.0, a.queries, seed=1, k=a.k, q_tokens=a.q_tokens, doc_tokens=a.doc_tokens)
-    ex = MeasuredExecutor(eng, svc)
+    ex = MeasuredExecutor(eng, svc, workload={it.query_id: it for it in items})
     t0 = time.perf_counter()
     report, records = run(cfg, items, ex)
     wall = time.perf_counter() - t0

@@ -228,3 +228,47 @@ def test_c2_full_shape_bench_path_matches_oracle():
     got = eng.pool.gather(eng.resident.acquire(key).blocks, 2560).float().cpu()
     eng.resident.unpin(key)
     assert rel_err(got, kref[:, :, :, :2560]) <= TOL
+
+
+@pytest.mark.parametrize("name,counts", [("tiny", (100, 40, 128)), ("gqa-small-128", (256, 64, 200)),
+                                         ("llama-3.2-1b", (512, 512, 512))])
+def test_combination_prefix_slices_equal_from_scratch_prefixes(name, counts):
+    """SURVEY H-e: one prefill of the ordered combination + slicing gives every prefix
+    blob bit-identical (payload, checksum) to generating the prefix from scratch —
+    the kernels are row-deterministic in generation mode (no split-K / split-KV)."""
+    from paper_2504_11765_b200.generator import KvGenerator
+
+    spec = get_spec(name)
+    eng = Engine(spec, seed=5, pool_tokens=4096)
+    gen = KvGenerator(eng, keep_on_device=False)
+    ids = (31, 7, 19)[: len(counts)]
+    factory = gen.for_combination(ids, counts)
+    for j in range(1, len(ids) + 1):
+        a = factory(ids[:j], counts[:j])()
+        b = gen.generate(ids[:j], counts[:j])
+        assert a.header == b.header                      # incl. the FNV-1a checksum
+        assert torch.equal(a.payload_tensor(), b.payload_tensor())
+
+
+def test_prepare_uses_one_prefill_per_combination(tmp_path):
+    from paper_2504_11765_b200.generator import KvGenerator
+    from paper_2504_11765_b200.prefetch import PendingQuery, prepare
+    from paper_2504_11765_b200.service import SharedCacheService
+    from paper_2504_11765_b200.store import KvKey, KvStore, Outcome
+
+    spec = get_spec("gqa-small-64")
+    eng = Engine(spec, seed=5, pool_tokens=4096)
+    gen = KvGenerator(eng, keep_on_device=False)
+    svc = SharedCacheService(KvStore(tmp_path, 0))
+    calls = []
+    orig = eng.generate_doc_kv
+    eng.generate_doc_kv = lambda toks, *a, **k: (calls.append(len(toks)), orig(toks, *a, **k))[1]
+    q = PendingQuery(query_id=1, arrival_time=0.0, k=4, q_tokens=8, doc_ids=(4, 8, 15, 16), doc_tokens=(64, 64, 64, 64))
+    q.flagged = True
+    prepare(q, None, svc, None, spec.profile(), generator=gen)
+    assert calls == [256]                                 # one prefill for the four prefixes
+    for j in range(1, 5):
+        look = svc.store.get(KvKey(spec.profile().model_hash, q.doc_ids[:j]))
+        assert look.outcome is Outcome.DISK_HIT
+        ref = gen.generate(q.doc_ids[:j], q.doc_tokens[:j])
+        assert look.blob == ref
