@@ -9,8 +9,10 @@ Locality analysis and traces (workload.py:50-98, 157-250) are out of scope
 
 from __future__ import annotations
 
+import json
 from dataclasses import dataclass
-from typing import Sequence
+from pathlib import Path
+from typing import Iterable, Sequence
 
 import numpy as np
 
@@ -88,3 +90,49 @@ def uniform_arrivals(items: Sequence[WorkItem], rate: float) -> list[tuple[float
         raise ValueError("rate must be positive")
     dt = 1.0 / rate
     return [(dt * (i + 1), it) for i, it in enumerate(items)]
+
+
+class TraceError(ValueError):
+    """A malformed work trace (workload.py:190-231)."""
+
+
+def save_trace(items: Iterable[WorkItem], path: str | Path) -> None:
+    """One JSON object per line, keys sorted (workload.py:234-250)."""
+    lines = []
+    for it in items:
+        if it.doc_ids is None:
+            raise ValueError("only doc-id items can be saved to a trace")
+        lines.append(json.dumps({"query_id": it.query_id, "doc_ids": list(it.doc_ids), "q_tokens": it.q_tokens,
+                                 "doc_tokens": list(it.doc_tokens)}, sort_keys=True))
+    Path(path).write_text("".join(line + "\n" for line in lines), encoding="utf-8")
+
+
+def load_trace(path: str | Path) -> list[WorkItem]:
+    """Inverse of save_trace; missing token counts take the module defaults and
+    a missing query_id the 0-based line number (workload.py:190-231)."""
+    items = []
+    for lineno, line in enumerate(Path(path).read_text(encoding="utf-8").splitlines(), start=1):
+        if not line.strip():
+            continue
+        try:
+            obj = json.loads(line)
+        except json.JSONDecodeError as exc:
+            raise TraceError(f"{path}:{lineno}: invalid JSON: {exc}") from exc
+        try:
+            doc_ids = tuple(int(d) for d in obj["doc_ids"])
+        except (KeyError, TypeError, ValueError) as exc:
+            raise TraceError(f"{path}:{lineno}: field 'doc_ids': {exc}") from exc
+        raw = obj.get("doc_tokens")
+        doc_tokens = (DEFAULT_DOC_TOKENS,) * len(doc_ids) if raw is None else tuple(int(t) for t in raw)
+        if len(doc_tokens) != len(doc_ids):
+            raise TraceError(f"{path}:{lineno}: field 'doc_tokens': length {len(doc_tokens)} does not match "
+                             f"{len(doc_ids)} doc_ids")
+        try:
+            items.append(WorkItem(query_id=int(obj.get("query_id", lineno - 1)),
+                                  q_tokens=int(obj.get("q_tokens", DEFAULT_Q_TOKENS)), doc_ids=doc_ids,
+                                  doc_tokens=doc_tokens))
+        except ValueError as exc:
+            raise TraceError(f"{path}:{lineno}: {exc}") from exc
+    if not items:
+        raise TraceError(f"{path}: no work items")
+    return items
