@@ -154,18 +154,29 @@ __global__ void __launch_bounds__(128) fnv_affine_kernel(const uint8_t* __restri
   cterm[c] = C;
 }
 
+// h = ((seed * A_0 + C_0) * A_1 + C_1) ...: each lane folds a contiguous run of
+// chunks into one affine map (A, C), then lane 0 folds the 32 maps in order.
 __global__ void fnv_combine_kernel(const uint64_t* __restrict__ cterm, int chunks, size_t n, uint64_t seed,
                                    uint64_t* __restrict__ out) {
   pdl_trigger();
   pdl_wait();
-  if (threadIdx.x != 0) return;
+  const int lane = threadIdx.x;
   const uint64_t a_full = pow_p(kChunk);
-  uint64_t h = seed;
-  for (int c = 0; c < chunks; ++c) {
+  const int per = (chunks + 31) / 32;
+  const int c0 = min(chunks, lane * per), c1 = min(chunks, c0 + per);
+  uint64_t A = 1, C = 0;
+  for (int c = c0; c < c1; ++c) {
     const size_t len = min((size_t)kChunk, n - (size_t)c * kChunk);
-    h = h * (len == (size_t)kChunk ? a_full : pow_p(len)) + cterm[c];
+    const uint64_t a = len == (size_t)kChunk ? a_full : pow_p(len);
+    A *= a;
+    C = C * a + cterm[c];
   }
-  *out = h;
+  uint64_t h = seed;
+  for (int l = 0; l < 32; ++l) {
+    const uint64_t Al = __shfl_sync(0xffffffffu, A, l), Cl = __shfl_sync(0xffffffffu, C, l);
+    h = h * Al + Cl;
+  }
+  if (lane == 0) *out = h;
 }
 
 }  // namespace
