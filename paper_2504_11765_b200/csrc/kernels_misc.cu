@@ -42,14 +42,13 @@ __global__ void __launch_bounds__(256) kv_unpack_kernel(const UnpackJob* __restr
   constexpr int UNROLL = 4;
   for (long long seg = (long long)blockIdx.x * 8 + warp; seg < nseg; seg += (long long)gridDim.x * 8) {
     const int b = (int)(seg % nblk);
-    const long long plane = (long long)layer0 * 2 * hkv + seg / nblk;  // (l*2 + kv)*hkv + h
-    const long long lkv = plane / hkv;                                 // l*2 + kv
-    const long long src_plane = lkv * src_hkv + h0 + plane % hkv;
+    const int plane = layer0 * 2 * hkv + (int)(seg / nblk);  // (l*2 + kv)*hkv + h  (< 2^31)
+    const int src_plane = src_hkv == hkv ? plane : (plane / hkv) * src_hkv + h0 + plane % hkv;
     const int t0 = b * block_size;
     const int ntok = min(block_size, jb.n_tokens - t0);
     const long long n_el = (long long)ntok * dh;
-    const long long src_off = src_plane * (long long)jb.n_tokens * dh + (long long)t0 * dh;
-    const long long dst_off = plane * slots * dh + (long long)bt[jb.first_block + b] * block_size * dh;
+    const long long src_off = (long long)src_plane * jb.n_tokens * dh + (long long)t0 * dh;
+    const long long dst_off = (long long)plane * slots * dh + (long long)bt[jb.first_block + b] * block_size * dh;
     __nv_bfloat16* dst = pool + dst_off;
     if constexpr (SRC_W == 2) {
       const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(jb.src) + src_off;
