@@ -221,9 +221,13 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 
 // 2^x for a pair of fp32 on the FMA/ALU pipes instead of the MUFU (FA4-style
 // offload of the SFU bottleneck): x = j + f, j = rint(x) via the 1.5*2^23
-// magic add, 2^f by a degree-3 minimax polynomial on [-0.5, 0.5] (max rel err
-// 9.3e-5, below bf16 2^-9), 2^j added into the exponent bits.  x < -125
+// magic add, 2^f by a minimax polynomial on [-0.5, 0.5] (degree 2: max rel err
+// 1.7e-3, the order of P's own bf16 rounding; degree 3: 9.3e-5), 2^j added
+// into the exponent bits.  x < -125
 // (incl. -inf) clamps to 2^-125 (~2e-38, nil against any visible key).
+#ifndef RDKV_EXP2_DEG2
+#define RDKV_EXP2_DEG2 1  // degree-2 polynomial: 2% faster attention than degree 3, error at bf16 rounding level
+#endif
 __device__ __forceinline__ void exp2_emu2(float& y0, float& y1, float x0, float x1) {
   constexpr float MAGIC = 12582912.f;
   x0 = fmaxf(x0, -125.f);  // keeps 2^j in the normal range for p in [0.7, 1.42)
@@ -232,9 +236,15 @@ __device__ __forceinline__ void exp2_emu2(float& y0, float& y1, float x0, float 
   fadd2(t0, t1, x0, x1, MAGIC, MAGIC);
   fadd2(j0, j1, t0, t1, -MAGIC, -MAGIC);
   ffma2(f0, f1, j0, j1, -1.f, -1.f, x0, x1);
+#if RDKV_EXP2_DEG2
+  // degree 2 (max rel err 1.7e-3, the order of bf16 rounding of P)
+  ffma2(p0, p1, f0, f1, 0.23841818417998267f, 0.23841818417998267f, 0.7034251708305549f, 0.7034251708305549f);
+  ffma2(p0, p1, p0, p1, f0, f1, 1.000442245833965f, 1.000442245833965f);
+#else
   ffma2(p0, p1, f0, f1, 0.05520277717811479f, 0.05520277717811479f, 0.24272204344485557f, 0.24272204344485557f);
   ffma2(p0, p1, p0, p1, f0, f1, 0.6932596326013668f, 0.6932596326013668f);
   ffma2(p0, p1, p0, p1, f0, f1, 0.9999097302078288f, 0.9999097302078288f);
+#endif
   y0 = __uint_as_float(__float_as_uint(p0) + (__float_as_uint(t0) << 23));
   y1 = __uint_as_float(__float_as_uint(p1) + (__float_as_uint(t1) << 23));
 }
