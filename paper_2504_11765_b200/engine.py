@@ -22,6 +22,7 @@ All GPU work goes through librdkv's C ABI; there is no PyTorch compute path.
 from __future__ import annotations
 
 import contextlib
+import os
 import ctypes as C
 import threading
 from collections import OrderedDict, deque
@@ -332,6 +333,9 @@ class LayerStreamer:
         self.h2d = torch.cuda.Stream(device=engine.device)          # host -> HBM copies
         self.events = [torch.cuda.Event() for _ in range(L)]
         self.copied = [torch.cuda.Event() for _ in range(L)]
+        # layers per H2D copy: 2 measured best (C2: 94% of the pinned-copy peak vs 92% at 1,
+        # 88% at 16 — fewer, larger DMAs, still early enough for the first attention)
+        self.copy_layers = max(1, int(os.environ.get("RDKV_H2D_LAYERS", "2")))
         self.handles = (C.c_void_p * L)()
 
     def launch(self, pool: KvPool, jobs, block_table: torch.Tensor, jobs_dev: torch.Tensor, main: torch.cuda.Stream,
@@ -350,13 +354,16 @@ class LayerStreamer:
             self.h2d.wait_stream(main)
             for _, dev in h2d:
                 dev.record_stream(self.h2d)
+        g = self.copy_layers
         for l in range(L):
-            if h2d:
+            if h2d and l % g == 0:
+                l1 = min(L, l + g)
                 with torch.cuda.stream(self.h2d):
                     for host, dev in h2d:
                         per = host.numel() // L
-                        dev[l * per:(l + 1) * per].copy_(host[l * per:(l + 1) * per], non_blocking=True)
-                    self.copied[l].record(self.h2d)
+                        dev[l * per:l1 * per].copy_(host[l * per:l1 * per], non_blocking=True)
+                    for ll in range(l, l1):
+                        self.copied[ll].record(self.h2d)
             with torch.cuda.stream(self.stream):
                 if l == 0 and first_event is not None:
                     first_event.record(self.stream)
