@@ -628,7 +628,7 @@ class Engine:
         if row_deterministic:
             plan.flags |= 1  # RDKV_BATCH_ROW_DETERMINISTIC
         self.model.forward(plan, out.data_ptr(), n, stream=stream)
-        out._plan = plan  # metadata lifetime follows the output
+        plan.meta.record_stream(stream if stream is not None else torch.cuda.current_stream(self.device))
         return out
 
     # -------------------------------------------------------------- query prefill
