@@ -246,9 +246,11 @@ RDKV_API int rdkv_tp_reduce_resid(rdkv_tp_comm* comm, void* x, int64_t ldx, int 
  *             position p of sequence s at slot block_table[s*bt_stride + p/block_size]
  *             * block_size + p % block_size
  * impl 0 = tcgen05 kernel (block_size % 64 == 0 or bt_stride == 1), 1 = mma.sync
- * kernel (any block size).  `scratch` (rdkv_attention_scratch_bytes) enables
- * split-KV for grids too small to fill the GPU.  The building block rdkv_forward
- * calls per layer; exposed for tests. */
+ * kernel (any block size), 2 = tcgen05 kernel on a stream-K schedule (148
+ * persistent CTAs with equal KV-tile shares; grids of more than half a wave).
+ * `scratch` (rdkv_attention_scratch_bytes) enables split-KV for grids too small
+ * to fill the GPU and holds the stream-K partials.  The building block
+ * rdkv_forward calls per layer; exposed for tests. */
 RDKV_API int rdkv_attention(const void* q, int64_t ldq, void* o, int64_t ldo, const void* kplane,
                             const void* vplane, int64_t kv_slots, const int32_t* seq_start,
                             const int32_t* seq_new, const int32_t* seq_cached, const int32_t* block_table,

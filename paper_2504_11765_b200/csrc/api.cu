@@ -92,6 +92,15 @@ extern "C" int rdkv_attention(const void* q, int64_t ldq, void* o, int64_t ldo, 
     ap.split_bytes = need;
   }
   auto st = static_cast<cudaStream_t>(stream);
+  const size_t sk = attention_sk_scratch_bytes(num_sms(), head_dim);
+  if (scratch && scratch_bytes >= need + sk) {
+    attention_sk_carve(ap, static_cast<uint8_t*>(scratch) + need, num_sms(), head_dim);
+    RDKV_TRY(attention_sk_zero_flags(ap, st));
+  }
+  if (impl == 2) {  // tcgen05 kernel, stream-K schedule where it applies
+    ap.sk_mode = 1;
+    impl = 0;
+  }
   if (impl == 0) {
     if (!attention_tc_supported(ap, head_dim))
       return set_error(RDKV_ERR_ARG, "rdkv_attention: shape not supported by the tcgen05 kernel");
@@ -101,5 +110,5 @@ extern "C" int rdkv_attention(const void* q, int64_t ldq, void* o, int64_t ldo, 
 }
 
 extern "C" size_t rdkv_attention_scratch_bytes(int n_tokens, int n_heads, int head_dim) {
-  return attention_split_scratch_bytes(n_tokens, n_heads, head_dim);
+  return attention_split_scratch_bytes(n_tokens, n_heads, head_dim) + attention_sk_scratch_bytes(num_sms(), head_dim);
 }

@@ -28,7 +28,21 @@ struct AttnParams {
   float* split_o;               // [splits][T][hq][dh] fp32
   float2* split_ml;             // [splits][T][hq] (max, sum)
   size_t split_bytes;
+  // stream-K (tensor-core kernel, chosen at launch): per-CTA partial of the unit it
+  // shares with its predecessor CTA, and the publish flags (zero between launches)
+  int n_seqs;
+  int sk_qblocks;               // query blocks per sequence (set by the launcher)
+  float* sk_o;                  // [ctas][2 Q tiles x 128 rows][dh] fp32
+  float2* sk_ml;                // [ctas][256] (max, sum)
+  int* sk_flag;                 // [ctas]
+  int sk_ctas;                  // CTAs the scratch was sized for (0 = no stream-K)
+  int sk_mode;                  // 1: use stream-K where it applies (rdkv_attention impl 2, RDKV_ATTN_SK=1)
 };
+
+// stream-K scratch: partials + flags for `ctas` CTAs; carve() points p's sk_* into it
+size_t attention_sk_scratch_bytes(int ctas, int dh);
+void attention_sk_carve(AttnParams& p, void* base, int ctas, int dh);
+int attention_sk_zero_flags(const AttnParams& p, cudaStream_t st);
 
 // split-KV scratch bytes for T tokens (0 when T is too large to ever split)
 size_t attention_split_scratch_bytes(int T, int hq, int dh);

@@ -25,6 +25,9 @@
 //               O_i += P_i.V with P_i read from TMEM (tcgen05.mma A-from-TMEM,
 //               V as the MN-major B).  Separate issuers keep the two Q tiles'
 //               pipelines independent.
+//   warp 11     Q loader: TMA of each segment's Q tiles (3-D map: dh x heads x
+//               tokens, so the G heads of one kv head land as consecutive rows)
+//               as soon as the previous segment's last Q.K^T has retired.
 // TMEM (512 columns): S_0 S_1 (128 each), O_0 O_1 (dh each), P_0 P_1 (64 each,
 // dh=64) or P_i over S_i (dh=128, after S_i is in registers).
 #include <cuda.h>
@@ -41,6 +44,22 @@
 namespace rdkv {
 
 int make_tmap(CUtensorMap* m, const void* base, long long rows, long long K, long long ld, int box_rows);
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn();
+
+// Q as a 3-D bf16 map {dh, heads, tokens} (token stride ldq elements), box {64, G, TPT}, 128-B swizzle
+static int make_tmap_q(CUtensorMap* m, const void* q, long long tokens, int hq, int dh, long long ldq, int G, int tpt) {
+  auto fn = encode_fn();
+  if (!fn) return set_error(RDKV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)dh, (cuuint64_t)hq, (cuuint64_t)tokens};
+  cuuint64_t strides[2] = {(cuuint64_t)dh * 2, (cuuint64_t)ldq * 2};
+  cuuint32_t box[3] = {64, (cuuint32_t)G, (cuuint32_t)tpt};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(q), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(RDKV_ERR_CUDA, "cuTensorMapEncodeTiled (q) failed (%d)", (int)r);
+  return 0;
+}
 
 namespace {
 
@@ -61,7 +80,10 @@ struct TcCfg {
   static constexpr uint32_t OFF_V = OFF_K + STAGES * KB;
   static constexpr uint32_t OFF_RED = OFF_V + STAGES * KB;  // [2 parity][2 Q tiles][2 halves][128 rows] fp32
   static constexpr uint32_t OFF_BAR = OFF_RED + 2 * 2 * 2 * ROWS * 4;
-  static constexpr size_t SMEM = OFF_BAR + 8 * (1 + 3 * STAGES + 8) + 16;
+  static constexpr uint32_t OFF_MISC = (OFF_BAR + 8 * (4 + 3 * STAGES + 8) + 15) / 16 * 16;  // TMEM base, segment count, W
+  static constexpr uint32_t OFF_SEG = OFF_MISC + 16;                        // stream-K segments (int4)
+  static constexpr uint32_t OFF_SEQ = OFF_SEG + 16 * 512;                   // stream-K: [3][512] seq start/new/cached
+  static constexpr size_t SMEM = OFF_SEQ + 3 * 4 * 512;
   // TMEM columns
   static constexpr uint32_t COL_S = 0;                          // S_i at 128 i
   static constexpr uint32_t COL_O = 2 * BKV;                    // O_i at 256 + DH i
@@ -71,7 +93,7 @@ struct TcCfg {
 
 // SPL softmax warps per query row (each takes BKV / SPL keys of a tile):
 //   warps [0, NS): softmax, NS = 8 * SPL (Q tile i, key half h, TMEM quadrant q);
-//   NS: TMA producer; NS+1 / NS+2: MMA issuers of Q tile 0 / 1; NS+3 idle.
+//   NS: TMA producer; NS+1 / NS+2: MMA issuers of Q tile 0 / 1; NS+3: Q loader.
 template <int SPL>
 struct Roles {
   static constexpr int NS = 8 * SPL;
@@ -86,7 +108,7 @@ constexpr float RESCALE_LOG2 = 8.f;   // lazy O rescale: keep a stale row max un
 #define RDKV_ATTN_TRACE 0  // 1: per-tile clock64 timeline of CTA 0 (debug builds only)
 #endif
 #if RDKV_ATTN_TRACE
-__device__ long long g_attn_trace[4][64][8];
+__device__ long long g_attn_trace[6][64][8];
 #define TRACE(who, j, ev) \
   do { if (blockIdx.x == gridDim.x - 1 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 64) g_attn_trace[who][j][ev] = clock64(); } while (0)
 #else
@@ -122,11 +144,59 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
-template <int DH, int SPL>
+// One unit of attention work: two Q tiles (query block qb) of sequence s against KV head kvh.
+struct Unit {
+  int s, kvh, tok0, ntok, n_q, pos0, kv_len, n_all, row_base;
+};
+__device__ __forceinline__ Unit unit_of(const int* seq_start, const int* seq_new, const int* seq_cached, int s, int qb,
+                                       int kvh, int TPT) {
+  Unit u;
+  u.s = s;
+  u.kvh = kvh;
+  const int n_new = seq_new[s];
+  u.tok0 = qb * 2 * TPT;
+  u.ntok = max(0, min(2 * TPT, n_new - u.tok0));
+  u.n_q = u.ntok > TPT ? 2 : (u.ntok > 0 ? 1 : 0);
+  u.pos0 = seq_cached[s] + u.tok0;
+  u.kv_len = u.pos0 + u.ntok;
+  u.n_all = u.ntok > 0 ? (u.kv_len + BKV - 1) / BKV : 0;
+  u.row_base = seq_start[s] + u.tok0;
+  return u;
+}
+
+// Segment kinds: a CTA's share [ta, tb) of one unit's KV tiles
+enum : int { SEG_WHOLE = 0, SEG_SPLIT = 1, SEG_PART = 2, SEG_HEAD = 3 };
+constexpr int SK_MAXSEG = 512;     // stream-K: segments per CTA (<= units, checked at launch)
+constexpr int SK_BAR = 9;          // named barrier of the softmax warps (stream-K hand-off)
+constexpr int SK_PUB = 10;         // softmax warps + the Q-loader warp: a part's rows are written
+
+// stream-K: first global tile of CTA b when W tiles are spread over G CTAs
+__device__ __forceinline__ long long sk_bound(int b, long long W, int G) { return (long long)b * W / G; }
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// SK = false: one CTA per (query block, kv head, sequence[, KV split]), as the grid says.
+// SK = true (stream-K, SPL = 1): a persistent grid of G CTAs; the W = sum of all units' KV
+// tiles are dealt out as G equal contiguous ranges of the (sequence, query block, kv head)
+// -major tile order, so every SM gets the same number of tile iterations whatever the
+// unit count.  A unit cut by a range boundary is finished by the CTA that holds its
+// first tiles (SEG_HEAD, always that CTA's last segment): it merges the (m, l, O)
+// partials that the following CTAs wrote as their FIRST segment (SEG_PART, published
+// with a release flag before they do anything else, so the waits cannot deadlock).
+template <int DH, int SPL, bool SK>
 __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
-    attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnParams p) {
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                   const __grid_constant__ CUtensorMap tmQ, AttnParams p) {
   using C = TcCfg<DH>;
   using R = Roles<SPL>;
+  static_assert(!SK || SPL == 1, "stream-K runs one softmax warp per row");
   constexpr int NS = R::NS;
   constexpr int KH = BKV / SPL;  // keys of a tile per softmax thread
   constexpr int ST = C::STAGES;
@@ -135,59 +205,132 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
   const uint32_t sb = smem_u32(smem);
   if (sb & 1023) __trap();  // SW128 operands need 1024-B alignment
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;             // [ST]
+  uint64_t* q_full = bars + 0;             // [2] per Q tile: Q_i staged
+  uint64_t* q_empty = bars + 2;            // [2] per Q tile: the segment's last Q_i.K^T retired
+  uint64_t* k_full = bars + 4;             // [ST]
   uint64_t* v_full = k_full + ST;          // [ST]
   uint64_t* kv_empty = v_full + ST;        // [ST]
   uint64_t* s_full = kv_empty + ST;        // [2] per Q tile: S_i = Q_i.K^T landed
   uint64_t* s_empty = s_full + 2;          // [2] S_i read into registers
   uint64_t* p_full = s_empty + 2;          // [2] P_i written (and O_i rescaled)
   uint64_t* o_done = p_full + 2;           // [2] O_i += P_i.V retired (P_i free)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_MISC);
+  int* nseg_s = reinterpret_cast<int*>(smem + C::OFF_MISC + 4);
+  long long* wtot_s = reinterpret_cast<long long*>(smem + C::OFF_MISC + 8);
+  int4* segs = reinterpret_cast<int4*>(smem + C::OFF_SEG);  // {unit code, ta, tb, kind}
 
   const int G = p.hq / p.hkv;
   const int TPT = ROWS / G;                 // tokens per Q tile
-  const int s = blockIdx.z, kvh = blockIdx.y;
-  const int xb = gridDim.x - 1 - blockIdx.x;  // longest causal rows first
-  const int qb = xb / p.kv_splits, ks = xb % p.kv_splits;  // query-tile pair, KV split
-  const int n_new = p.seq_new[s];
-  const int tok0 = qb * 2 * TPT;
-  if (tok0 >= n_new) return;
-  const int ntok = min(2 * TPT, n_new - tok0);
-  const int n_q = ntok > TPT ? 2 : 1;       // active Q tiles
-  const int pos0 = p.seq_cached[s] + tok0;
-  const int kv_len = pos0 + ntok;
-  // this CTA's share of the KV tiles (split-KV when the grid alone cannot fill the GPU)
-  const int n_all = (kv_len + BKV - 1) / BKV;
-  const int per_split = (n_all + p.kv_splits - 1) / p.kv_splits;
-  const int t_begin = ks * per_split;
-  const int n_tiles = max(0, min(n_all, t_begin + per_split) - t_begin);
-  const int row_base = p.seq_start[s] + tok0;
-  const int* bt = p.block_table + (long long)s * p.bt_stride;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int QBn = SK ? p.sk_qblocks : gridDim.x / p.kv_splits;
+  // the single segment of a non-stream-K CTA
+  int4 seg0 = make_int4(0, 0, 0, SEG_WHOLE);
+  if constexpr (!SK) {
+    const int s = blockIdx.z, kvh = blockIdx.y;
+    const int xb = gridDim.x - 1 - blockIdx.x;  // longest causal rows first
+    const int qb = xb / p.kv_splits, ks = xb % p.kv_splits;
+    const Unit u = unit_of(p.seq_start, p.seq_new, p.seq_cached, s, qb, kvh, TPT);
+    if (u.ntok == 0) return;
+    const int per_split = (u.n_all + p.kv_splits - 1) / p.kv_splits;
+    const int ta = min(u.n_all, ks * per_split), tb = min(u.n_all, ta + per_split);
+    seg0 = make_int4((s * QBn + qb) * p.hkv + kvh, ta, tb, p.kv_splits > 1 ? SEG_SPLIT : SEG_WHOLE);
+  }
 
-  if (warp == NS && lane == 0) {
-    tma_prefetch_desc(&tmK);
-    tma_prefetch_desc(&tmV);
-    mbar_init(q_full, NS);
-    for (int i = 0; i < ST; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&v_full[i], 1);
-      mbar_init(&kv_empty[i], n_q);  // released by both Q tiles' P.V
+  if (warp == NS) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+      tma_prefetch_desc(&tmQ);
+      for (int i = 0; i < 2; ++i) {
+        mbar_init(&q_full[i], 1);
+        mbar_init(&q_empty[i], 1);
+      }
+      for (int i = 0; i < ST; ++i) {
+        mbar_init(&k_full[i], 1);
+        mbar_init(&v_full[i], 1);
+        mbar_init(&kv_empty[i], 2);  // both Q tiles' issuers release every stage
+      }
+      for (int i = 0; i < 2; ++i) {
+        mbar_init(&s_full[i], 1);
+        mbar_init(&s_empty[i], 4 * SPL);
+        mbar_init(&p_full[i], 4 * SPL);
+        mbar_init(&o_done[i], 1);
+      }
+      fence_barrier_init();
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 4 * SPL);
-      mbar_init(&p_full[i], 4 * SPL);
-      mbar_init(&o_done[i], 1);
+    if constexpr (SK) {
+      // stream-K schedule (batch metadata only: valid before the predecessor finishes).
+      // Lane l walks a contiguous chunk of (sequence, query block) pairs; every pair
+      // holds hkv units of equal cost (KV tiles).
+      const int npair = p.n_seqs * QBn;
+      // the batch metadata the roles re-read per segment, cached in smem (n_seqs <= units <= 512)
+      int* seq_s = reinterpret_cast<int*>(smem + C::OFF_SEQ);
+      for (int q = lane; q < p.n_seqs; q += 32) {
+        seq_s[q] = p.seq_start[q];
+        seq_s[512 + q] = p.seq_new[q];
+        seq_s[1024 + q] = p.seq_cached[q];
+      }
+      auto cost = [&](int pr) { return unit_of(p.seq_start, p.seq_new, p.seq_cached, pr / QBn, pr % QBn, 0, TPT).n_all; };
+      const int chunk = (npair + 31) / 32;
+      const int c0 = min(npair, lane * chunk), c1 = min(npair, c0 + chunk);
+      long long mine = 0;
+      for (int pr = c0; pr < c1; ++pr) mine += (long long)cost(pr) * p.hkv;
+      long long incl = mine;
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const long long W = __shfl_sync(0xffffffffu, incl, 31);
+      const long long B0 = sk_bound(blockIdx.x, W, gridDim.x), B1 = sk_bound(blockIdx.x + 1, W, gridDim.x);
+      int base = 0;
+      for (int pass = 0; pass < 2; ++pass) {
+        long long g = incl - mine;
+        int cnt = 0;
+        for (int pr = c0; pr < c1 && g < B1; ++pr) {
+          const int c = cost(pr);
+          if (c == 0 || g + (long long)c * p.hkv <= B0) {
+            g += (long long)c * p.hkv;
+            continue;
+          }
+          for (int kvh = 0; kvh < p.hkv; ++kvh, g += c) {
+            const long long lo = max(g, B0), hi = min(g + c, B1);
+            if (lo >= hi) continue;
+            if (pass == 1) {
+              const int ta = (int)(lo - g), tb = (int)(hi - g);
+              segs[base + cnt] = make_int4(pr * p.hkv + kvh, ta, tb, ta > 0 ? SEG_PART : tb < c ? SEG_HEAD : SEG_WHOLE);
+            }
+            ++cnt;
+          }
+        }
+        if (pass == 0) {  // exclusive scan of the per-lane counts -> write offsets
+          int ic = cnt;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, ic, o);
+            if (lane >= o) ic += t;
+          }
+          base = ic - cnt;
+          if (lane == 31) {
+            *nseg_s = ic;
+            *wtot_s = W;
+          }
+        }
+      }
     }
-    fence_barrier_init();
   }
   if (warp == NS + 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int nseg = SK ? *nseg_s : 1;
+  const long long Wtot = SK ? *wtot_s : 0;  // stream-K: total KV tiles of the launch
+  auto seg_at = [&](int k) { return SK ? segs[k] : seg0; };
+  const int* seq_s = reinterpret_cast<const int*>(smem + C::OFF_SEQ);
+  auto unit_at = [&](int code) {
+    const int pr = code / p.hkv;
+    if constexpr (SK) return unit_of(seq_s, seq_s + 512, seq_s + 1024, pr / QBn, pr % QBn, code % p.hkv, TPT);
+    return unit_of(p.seq_start, p.seq_new, p.seq_cached, pr / QBn, pr % QBn, code % p.hkv, TPT);
+  };
   pdl_trigger();
   pdl_wait();  // q / KV planes written by the predecessor are visible from here
 
@@ -199,51 +342,60 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
     // The whole warp walks the tiles: every 32 tiles each lane resolves one
     // tile's two block-table rows (32 global loads in parallel instead of a
     // dependent load per tile on the issue path); lane 0 issues the TMA.
-    const long long row0 = (long long)kvh * (p.head_stride / DH);  // first row of this head in the plane view
-    int my_rows[2] = {0, 0};
-    for (int j = 0; j < n_tiles; ++j) {
-      if ((j & 31) == 0 && j + lane < n_tiles) {
+    int it = 0;  // stage counter over every tile of every segment
+    for (int k = 0; k < nseg; ++k) {
+      const int4 sg = seg_at(k);
+      const Unit u = unit_at(sg.x);
+      const long long row0 = (long long)u.kvh * (p.head_stride / DH);  // first row of this head in the plane view
+      const int* bt = p.block_table + (long long)u.s * p.bt_stride;
+      int my_rows[2] = {0, 0};
+      for (int j = sg.y; j < sg.z; ++j, ++it) {
+        if (((j - sg.y) & 31) == 0 && j + lane < sg.z) {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          int pos = (t_begin + j + lane) * BKV + h * HALF;
-          if (pos >= kv_len) pos = (t_begin + j + lane) * BKV;  // masked half: any valid, finite block
-          my_rows[h] = (int)(row0 + (long long)bt[pos / p.block_size] * p.block_size + pos % p.block_size);
+          for (int h = 0; h < 2; ++h) {
+            int pos = (j + lane) * BKV + h * HALF;
+            if (pos >= u.kv_len) pos = (j + lane) * BKV;  // masked half: any valid, finite block
+            my_rows[h] = (int)(row0 + (long long)bt[pos / p.block_size] * p.block_size + pos % p.block_size);
+          }
         }
+        const int rows[2] = {__shfl_sync(0xffffffffu, my_rows[0], (j - sg.y) & 31),
+                             __shfl_sync(0xffffffffu, my_rows[1], (j - sg.y) & 31)};
+        if (lane == 0) {
+          const int st = it % ST;
+          TRACE(4, it, 0);
+          mbar_wait_sleep(&kv_empty[st], ((it / ST) & 1) ^ 1);
+          TRACE(4, it, 1);
+          mbar_arrive_expect_tx(&k_full[st], C::KB);
+#pragma unroll
+          for (int c = 0; c < DH / 64; ++c)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              tma_load_2d_nohint(&tmK, &k_full[st], smem + C::OFF_K + st * C::KB + c * (BKV * 128) + h * (HALF * 128),
+                                 c * 64, rows[h]);
+          mbar_arrive_expect_tx(&v_full[st], C::KB);
+#pragma unroll
+          for (int c = 0; c < DH / 64; ++c)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              tma_load_2d_nohint(&tmV, &v_full[st], smem + C::OFF_V + st * C::KB + c * (BKV * 128) + h * (HALF * 128),
+                                 c * 64, rows[h]);
+        }
+        __syncwarp();
       }
-      const int rows[2] = {__shfl_sync(0xffffffffu, my_rows[0], j & 31), __shfl_sync(0xffffffffu, my_rows[1], j & 31)};
-      if (lane == 0) {
-        const int st = j % ST;
-        mbar_wait_sleep(&kv_empty[st], ((j / ST) & 1) ^ 1);
-        mbar_arrive_expect_tx(&k_full[st], C::KB);
-#pragma unroll
-        for (int c = 0; c < DH / 64; ++c)
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-            tma_load_2d_nohint(&tmK, &k_full[st], smem + C::OFF_K + st * C::KB + c * (BKV * 128) + h * (HALF * 128),
-                               c * 64, rows[h]);
-        mbar_arrive_expect_tx(&v_full[st], C::KB);
-#pragma unroll
-        for (int c = 0; c < DH / 64; ++c)
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-            tma_load_2d_nohint(&tmV, &v_full[st], smem + C::OFF_V + st * C::KB + c * (BKV * 128) + h * (HALF * 128),
-                               c * 64, rows[h]);
-      }
-      __syncwarp();
     }
   } else if (warp == NS + 1 || warp == NS + 2) {
     // ------------------------------------------------------------ MMA issuers
     // one issuing thread per Q tile, so neither softmax warpgroup ever waits on
     // the other's progress (their exp2 phases drift apart and overlap)
     const int i = warp - NS - 1;
-    if (lane == 0 && n_tiles > 0 && i < n_q) {
+    if (lane == 0) {
       constexpr uint32_t idesc_qk = idesc_bf16_f32(ROWS, BKV);
       constexpr uint32_t idesc_pv = idesc_bf16_f32(ROWS, DH) | (1u << 16);  // B (V) is MN-major
       const uint32_t qa = sb + C::OFF_Q + i * C::QB;
       const uint32_t tS = tmem + C::COL_S + i * BKV, tO = tmem + C::COL_O + i * DH;
       const uint32_t tP = tmem + C::COL_P + i * C::P_STRIDE;
-      auto issue_qk = [&](int j) {  // S_i = Q_i . K(j)^T
-        const uint32_t ka = sb + C::OFF_K + (j % ST) * C::KB;
+      auto issue_qk = [&](int stg, bool last) {  // S_i = Q_i . K^T of the tile in stage stg
+        const uint32_t ka = sb + C::OFF_K + stg * C::KB;
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
           const uint32_t sub = (kk & 3) * 32;
@@ -251,39 +403,92 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
                     idesc_qk, kk > 0 ? 1u : 0u);
         }
         umma_commit(&s_full[i]);
+        if (last) umma_commit(&q_empty[i]);  // Q_i may be overwritten by the next segment's
       };
-      issuer_wait(q_full, 0);
-      issuer_wait(&k_full[0], 0);
-      tc_fence_after();
-      issue_qk(0);
-      for (int j = 0; j < n_tiles; ++j) {
-        const int st = j % ST;
-        const bool more = j + 1 < n_tiles;
-        if (!C::ALIAS && more) {  // next S_i while the softmax still works on this tile
-          issuer_wait(&k_full[(j + 1) % ST], ((j + 1) / ST) & 1);
-          issuer_wait(&s_empty[i], j & 1);
-          tc_fence_after();
-          issue_qk(j + 1);
-          TRACE(2 + i, j, 0);
+      int it = 0, ti = 0, qi = 0;  // stage counter, this Q tile's tiles, this Q tile's segments
+      for (int k = 0; k < nseg; ++k) {
+        const int4 sg = seg_at(k);
+        const int nt = sg.z - sg.y;
+        if (nt == 0) continue;
+        if (i >= unit_at(sg.x).n_q) {  // no Q tile i in this unit: release its stages
+          for (int j = 0; j < nt; ++j, ++it) {
+            issuer_wait(&v_full[it % ST], (it / ST) & 1);
+            mbar_arrive(&kv_empty[it % ST]);
+          }
+          continue;
         }
-        issuer_wait(&v_full[st], (j / ST) & 1);
-        issuer_wait(&p_full[i], j & 1);
+        TRACE(2 + i, ti, 2);
+        issuer_wait(&q_full[i], qi & 1);
+        ++qi;
+        TRACE(2 + i, ti, 3);
+        issuer_wait(&k_full[it % ST], (it / ST) & 1);
+        TRACE(2 + i, ti, 4);
+        if (!C::ALIAS && ti > 0) issuer_wait(&s_empty[i], (ti - 1) & 1);
+        TRACE(2 + i, ti, 5);
         tc_fence_after();
-        const uint32_t va = sb + C::OFF_V + st * C::KB;
-#pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk) {  // O_i (+)= P_i . V(j), P_i from TMEM
-          // P of keys [16kk, 16kk+16): with P over S each half writes inside its own S columns
-          const uint32_t pcol = C::ALIAS ? (kk / (KH / 16)) * KH + (kk % (KH / 16)) * 8 : kk * 8;
-          umma_bf16_ts(tO, tP + pcol, desc_mn(va + kk * 2048, BKV * 128), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
-        }
-        umma_commit(&o_done[i]);
-        TRACE(2 + i, j, 1);
-        umma_commit(&kv_empty[st]);
-        if (C::ALIAS && more) {  // S_i overwrites P_i only after the P.V above (issue order)
-          issuer_wait(&k_full[(j + 1) % ST], ((j + 1) / ST) & 1);
+        issue_qk(it % ST, nt == 1);
+        for (int j = 0; j < nt; ++j, ++it, ++ti) {
+          const int st = it % ST;
+          const bool more = j + 1 < nt;
+          if (!C::ALIAS && more) {  // next S_i while the softmax still works on this tile
+            issuer_wait(&k_full[(it + 1) % ST], ((it + 1) / ST) & 1);
+            issuer_wait(&s_empty[i], ti & 1);
+            tc_fence_after();
+            issue_qk((it + 1) % ST, j + 2 == nt);
+            TRACE(2 + i, ti, 0);
+          }
+          issuer_wait(&v_full[st], (it / ST) & 1);
+          issuer_wait(&p_full[i], ti & 1);
           tc_fence_after();
-          issue_qk(j + 1);
+          const uint32_t va = sb + C::OFF_V + st * C::KB;
+#pragma unroll
+          for (int kk = 0; kk < BKV / 16; ++kk) {  // O_i (+)= P_i . V(j), P_i from TMEM
+            // P of keys [16kk, 16kk+16): with P over S each half writes inside its own S columns
+            const uint32_t pcol = C::ALIAS ? (kk / (KH / 16)) * KH + (kk % (KH / 16)) * 8 : kk * 8;
+            umma_bf16_ts(tO, tP + pcol, desc_mn(va + kk * 2048, BKV * 128), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&o_done[i]);
+          TRACE(2 + i, ti, 1);
+          umma_commit(&kv_empty[st]);
+          if (C::ALIAS && more) {  // S_i overwrites P_i only after the P.V above (issue order)
+            issuer_wait(&k_full[(it + 1) % ST], ((it + 1) / ST) & 1);
+            tc_fence_after();
+            issue_qk((it + 1) % ST, j + 2 == nt);
+          }
         }
+      }
+    }
+  } else if (warp == NS + 3) {
+    // ------------------------------------------------------------ Q loader
+    // rows of a Q tile = (token, head of this kv group) pairs, token-major: the
+    // box {64 dh, G heads, TPT tokens} lands exactly as [128 rows][128 B] SW128.
+    // Rows past the unit's tokens hold other tokens' queries (or TMA zero fill):
+    // finite, and their scores only reach their own (discarded) O rows.
+    // Stream-K: this warp also publishes the CTA's part (its first segment) once
+    // the softmax warps have written it, so they never wait for the release.
+    int qn[2] = {0, 0};
+    const bool part = SK && nseg > 0 && seg_at(0).w == SEG_PART;
+    const int k_pub = part ? min(2, nseg) : -1;  // publish after requesting this many segments' Q
+    for (int k = 0; k < nseg; ++k) {
+      const int4 sg = seg_at(k);
+      if (lane == 0 && sg.z > sg.y) {
+        const Unit u = unit_at(sg.x);
+        for (int i = 0; i < u.n_q; ++i) {
+          TRACE(5, 2 * k + i, 0);
+          if (qn[i] > 0) mbar_wait_sleep(&q_empty[i], (qn[i] - 1) & 1);
+          TRACE(5, 2 * k + i, 1);
+          ++qn[i];
+          mbar_arrive_expect_tx(&q_full[i], C::QB);
+#pragma unroll
+          for (int c = 0; c < DH / 64; ++c)
+            tma_load_3d_nohint(&tmQ, &q_full[i], smem + C::OFF_Q + i * C::QB + c * (ROWS * 128), c * 64, u.kvh * G,
+                               u.row_base + i * TPT);
+        }
+      }
+      if (k + 1 == k_pub) {
+        __syncwarp();
+        asm volatile("bar.sync %0, %1;" ::"n"(SK_PUB), "n"(NS * 32 + 32) : "memory");
+        if (lane == 0) st_release_gpu(p.sk_flag + blockIdx.x, 1);
       }
     }
   } else if (warp < NS) {
@@ -296,7 +501,6 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
     const int i = warp / (4 * SPL), h = (warp / 4) % SPL, quad = warp & 3;
     const int r = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    const int nrows = max(0, min(TPT, ntok - i * TPT)) * G;
     float* red = reinterpret_cast<float*>(smem + C::OFF_RED);  // [parity][tile][half][row]
     auto pair_sync = [&]() {
       if constexpr (SPL == 2) asm volatile("bar.sync %0, 64;" ::"r"(1 + i * 4 + quad) : "memory");
@@ -311,158 +515,235 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
         return use_max ? fmaxf(v, o) : v + o;
       }
     };
-    // Q row (this half's 16-B chunks) -> smem (K-major SW128, DH/64 column blocks of [128 rows][128 B])
-    {
+    auto softmax_bar = [&]() { asm volatile("bar.sync %0, %1;" ::"n"(SK_BAR), "n"(NS * 32) : "memory"); };
+    constexpr int OH = DH / SPL;  // O columns of this half
+    const uint32_t tS = tmem + C::COL_S + i * BKV + h * KH + lane_off;
+    const uint32_t tO = tmem + C::COL_O + i * DH + h * OH + lane_off;
+    // P columns of this half: inside its own S columns when P is written over S
+    const uint32_t tP = tmem + C::COL_P + i * C::P_STRIDE + h * (C::ALIAS ? KH : KH / 2) + lane_off;
+    const float sl2 = p.scale_log2;
+    int ti = 0;  // this Q tile's tiles so far (barrier parities)
+    for (int k = 0; k < nseg; ++k) {
+      const int4 sg = seg_at(k);
+      const Unit u = unit_at(sg.x);
+      const int nt = sg.z - sg.y;
+      const bool act = i < u.n_q && nt > 0;
+      const int nrows = max(0, min(TPT, u.ntok - i * TPT)) * G;
       const bool ok = r < nrows;
-      const int rr = ok ? r : 0;
-      const uint4* src = reinterpret_cast<const uint4*>(
-          p.q + (long long)(row_base + i * TPT + rr / G) * p.ldq + (long long)(kvh * G + rr % G) * DH);
-#pragma unroll
-      for (int cc = 0; cc < DH / 8 / SPL; ++cc) {
-        const int c = h * (DH / 8 / SPL) + cc;
-        const uint4 v = ok ? src[c] : make_uint4(0, 0, 0, 0);
-        const uint32_t a = sb + C::OFF_Q + i * C::QB + (c >> 3) * (ROWS * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4);
-        st_shared_v4(a, v.x, v.y, v.z, v.w);
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(q_full);
-    }
-    if (i < n_q && n_tiles > 0) {
-      // padded rows pretend to be the last valid position so no row is fully masked
-      const int qpos = (r < nrows) ? pos0 + i * TPT + r / G : kv_len - 1;
-      const float sl2 = p.scale_log2;
-      constexpr int OH = DH / SPL;  // O columns of this half
-      const uint32_t tS = tmem + C::COL_S + i * BKV + h * KH + lane_off;
-      const uint32_t tO = tmem + C::COL_O + i * DH + h * OH + lane_off;
-      // P columns of this half: inside its own S columns when P is written over S
-      const uint32_t tP = tmem + C::COL_P + i * C::P_STRIDE + h * (C::ALIAS ? KH : KH / 2) + lane_off;
+      const long long trow = u.row_base + i * TPT + (ok ? r : 0) / G;  // token row in [0, T)
+      const int head = u.kvh * G + (ok ? r : 0) % G;
       float m_used = -INFINITY;  // row max the P values and O are scaled to (log2 domain)
       float l = 0.f;             // this half's row sum at scale m_used
-      for (int j = 0; j < n_tiles; ++j) {
-        mbar_wait(&s_full[i], j & 1);
-        tc_fence_after();
-        uint32_t sv[KH];
-#pragma unroll
-        for (int c = 0; c < KH / 32; ++c) tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[c * 32]));
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_empty[i]);
-        const int lim = qpos - (t_begin + j) * BKV - h * KH;  // key e of this half visible iff e <= lim
-        if (lim < KH - 1) {
-#pragma unroll
-          for (int e = 0; e < KH; ++e)
-            if (e > lim) sv[e] = __float_as_uint(-INFINITY);
-        }
-        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-        for (int e = 0; e < KH; e += 8)
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            mx4[u] = fmax3(mx4[u], __uint_as_float(sv[e + 2 * u]), __uint_as_float(sv[e + 2 * u + 1]));
-        const float mt = exchange(fmax3(fmaxf(mx4[0], mx4[1]), mx4[2], mx4[3]), j & 1, true) * sl2;
-        // lazy rescale: move the reference max only when it grew by more than 2^8
-        const bool need = mt > m_used + RESCALE_LOG2;
-        const bool rescale = __any_sync(0xffffffffu, need) && j > 0;
-        float f = 1.f;
-        if (need) {
-          f = ex2_approx(m_used - mt);  // 0 when m_used = -inf
-          l *= f;
-          m_used = mt;
-        }
-        // P = 2^(S*scale - m_used) as bf16 pairs (registers), row sum in fp32; this
-        // overlaps P_i.V(j-1), which still reads the P_i buffer
-        const float nb = m_used == -INFINITY ? 0.f : -m_used;
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-        uint32_t pk[KH / 2];
-#pragma unroll
-        for (int k = 0; k < KH; k += 4) {
-          float x0, x1, x2, x3;
-          ffma2(x0, x1, __uint_as_float(sv[k]), __uint_as_float(sv[k + 1]), sl2, sl2, nb, nb);
-          ffma2(x2, x3, __uint_as_float(sv[k + 2]), __uint_as_float(sv[k + 3]), sl2, sl2, nb, nb);
-          if (((k / 4) * 3) % 8 < EMU_OF_8) {  // this group of 4 on the FMA pipe
-            exp2_emu2(x0, x1, x0, x1);
-            exp2_emu2(x2, x3, x2, x3);
-          } else {  // on the MUFU
-            x0 = ex2_approx(x0);
-            x1 = ex2_approx(x1);
-            x2 = ex2_approx(x2);
-            x3 = ex2_approx(x3);
-          }
-          fadd2(s0, s1, s0, s1, x0, x1);
-          fadd2(s2, s3, s2, s3, x2, x3);
-          pk[k / 2] = pack_bf16(x0, x1);
-          pk[k / 2 + 1] = pack_bf16(x2, x3);
-        }
-        // P_i (and O_i) are free once P_i.V(j-1) has retired (implied by s_full when P aliases S)
-        if (j > 0) {
-          mbar_wait(&o_done[i], (j - 1) & 1);
+      if (act) {
+        // padded rows pretend to be the last valid position so no row is fully masked
+        const int qpos = ok ? u.pos0 + i * TPT + r / G : u.kv_len - 1;
+        TRACE(i, ti, 6);
+        for (int j = 0; j < nt; ++j, ++ti) {
+          mbar_wait(&s_full[i], ti & 1);
           tc_fence_after();
-        }
+          if (j == 0) TRACE(i, ti, 7);
+          uint32_t sv[KH];
 #pragma unroll
-        for (int c = 0; c < KH / 64; ++c) tmem_st32(tP + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[c * 32]));
-        l += (s0 + s1) + (s2 + s3);
-        if (rescale) {  // this half of the O_i row *= f before P_i.V(j) accumulates into it
+          for (int c = 0; c < KH / 32; ++c) tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[c * 32]));
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_empty[i]);
+          const int lim = qpos - (sg.y + j) * BKV - h * KH;  // key e of this half visible iff e <= lim
+          if (lim < KH - 1) {
+#pragma unroll
+            for (int e = 0; e < KH; ++e)
+              if (e > lim) sv[e] = __float_as_uint(-INFINITY);
+          }
+          float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+          for (int e = 0; e < KH; e += 8)
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              mx4[q] = fmax3(mx4[q], __uint_as_float(sv[e + 2 * q]), __uint_as_float(sv[e + 2 * q + 1]));
+          const float mt = exchange(fmax3(fmaxf(mx4[0], mx4[1]), mx4[2], mx4[3]), ti & 1, true) * sl2;
+          // lazy rescale: move the reference max only when it grew by more than 2^8
+          const bool need = mt > m_used + RESCALE_LOG2;
+          const bool rescale = __any_sync(0xffffffffu, need) && j > 0;
+          float f = 1.f;
+          if (need) {
+            f = ex2_approx(m_used - mt);  // 0 when m_used = -inf
+            l *= f;
+            m_used = mt;
+          }
+          // P = 2^(S*scale - m_used) as bf16 pairs (registers), row sum in fp32; this
+          // overlaps P_i.V(j-1), which still reads the P_i buffer
+          const float nb = m_used == -INFINITY ? 0.f : -m_used;
+          float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+          uint32_t pk[KH / 2];
+#pragma unroll
+          for (int e = 0; e < KH; e += 4) {
+            float x0, x1, x2, x3;
+            ffma2(x0, x1, __uint_as_float(sv[e]), __uint_as_float(sv[e + 1]), sl2, sl2, nb, nb);
+            ffma2(x2, x3, __uint_as_float(sv[e + 2]), __uint_as_float(sv[e + 3]), sl2, sl2, nb, nb);
+            if (((e / 4) * 3) % 8 < EMU_OF_8) {  // this group of 4 on the FMA pipe
+              exp2_emu2(x0, x1, x0, x1);
+              exp2_emu2(x2, x3, x2, x3);
+            } else {  // on the MUFU
+              x0 = ex2_approx(x0);
+              x1 = ex2_approx(x1);
+              x2 = ex2_approx(x2);
+              x3 = ex2_approx(x3);
+            }
+            fadd2(s0, s1, s0, s1, x0, x1);
+            fadd2(s2, s3, s2, s3, x2, x3);
+            pk[e / 2] = pack_bf16(x0, x1);
+            pk[e / 2 + 1] = pack_bf16(x2, x3);
+          }
+          // P_i (and O_i) are free once P_i.V(j-1) has retired (implied by s_full when P aliases S)
+          if (j > 0) {
+            mbar_wait(&o_done[i], (ti - 1) & 1);
+            tc_fence_after();
+          }
+#pragma unroll
+          for (int c = 0; c < KH / 64; ++c) tmem_st32(tP + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[c * 32]));
+          l += (s0 + s1) + (s2 + s3);
+          if (rescale) {  // this half of the O_i row *= f before P_i.V(j) accumulates into it
+#pragma unroll
+            for (int c = 0; c < OH / 32; ++c) {
+              uint32_t ov[32];
+              tmem_ld32(tO + c * 32, ov);
+              tmem_ld_wait();
+#pragma unroll
+              for (int e = 0; e < 32; e += 2) {
+                float a0, a1;
+                fmul2(a0, a1, __uint_as_float(ov[e]), __uint_as_float(ov[e + 1]), f, f);
+                ov[e] = __float_as_uint(a0);
+                ov[e + 1] = __float_as_uint(a1);
+              }
+              tmem_st32(tO + c * 32, ov);
+            }
+          }
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[i]);
+          TRACE(i, ti, 0);
+        }
+        l = exchange(l, ti & 1, false);  // the parity the last tile did NOT use
+        TRACE(i, ti, 1);
+        mbar_wait(&o_done[i], (ti - 1) & 1);
+        tc_fence_after();
+        TRACE(i, ti, 2);
+      }
+      // ---- the segment's O rows (every lane of an active tile joins the .sync.aligned TMEM loads)
+      if (sg.w == SEG_HEAD) {  // wait until every later part of this unit is published
+        if (threadIdx.x == 0) {
+          const long long W = Wtot;
+          const long long uend = sk_bound(blockIdx.x + 1, W, gridDim.x) + (u.n_all - sg.z);
+          for (int c = blockIdx.x + 1; c < (int)gridDim.x && sk_bound(c, W, gridDim.x) < uend; ++c) {
+            if (sk_bound(c + 1, W, gridDim.x) == sk_bound(c, W, gridDim.x)) continue;
+            long long spins = 0;
+            while (ld_acquire_gpu(p.sk_flag + c) == 0)
+              if (++spins > (1ll << 31)) __trap();
+          }
+        }
+        softmax_bar();
+      }
+      if (act) {
+        if (sg.w == SEG_PART) {
+          // unnormalised partial at scale m_used for the unit's head CTA; slot layout
+          // [dh/4][256 rows][4] so a warp's float4 stores cover 512 contiguous bytes
+          float4* dst = reinterpret_cast<float4*>(p.sk_o + (long long)blockIdx.x * 2 * ROWS * DH) + i * ROWS + r;
+#pragma unroll
+          for (int c = 0; c < DH / 32; ++c) {
+            uint32_t ov[32];
+            tmem_ld32(tO + c * 32, ov);
+            tmem_ld_wait();
+            if (ok)
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                dst[(c * 8 + e) * 2 * ROWS] = make_float4(__uint_as_float(ov[4 * e]), __uint_as_float(ov[4 * e + 1]),
+                                                          __uint_as_float(ov[4 * e + 2]), __uint_as_float(ov[4 * e + 3]));
+          }
+          if (ok) p.sk_ml[(long long)blockIdx.x * 2 * ROWS + i * ROWS + r] = make_float2(m_used, l);
+        } else {
+          // merge the later parts (SEG_HEAD): O = sum_c o_c 2^(m_c - M), L likewise
+          float M = m_used, L = 0.f;
+          long long W = 0, uend = 0;
+          if (sg.w == SEG_HEAD) {
+            W = Wtot;
+            uend = sk_bound(blockIdx.x + 1, W, gridDim.x) + (u.n_all - sg.z);
+          }
+          auto for_parts = [&](auto&& fn) {  // fn(slot row index, part CTA)
+            if (sg.w != SEG_HEAD || !ok) return;
+            for (int c = blockIdx.x + 1; c < (int)gridDim.x && sk_bound(c, W, gridDim.x) < uend; ++c)
+              if (sk_bound(c + 1, W, gridDim.x) > sk_bound(c, W, gridDim.x)) fn((long long)c * 2 * ROWS + i * ROWS + r, c);
+          };
+          for_parts([&](long long slot, int) { M = fmaxf(M, __ldcg(&p.sk_ml[slot].x)); });
+          const float w0 = M == m_used ? 1.f : ex2_approx(m_used - M);
+          L = l * w0;
+          for_parts([&](long long slot, int) {
+            const float2 ml = __ldcg(&p.sk_ml[slot]);
+            L += ml.y * ex2_approx(ml.x - M);
+          });
+          const float inv = L > 0.f ? 1.f / L : 0.f;
 #pragma unroll
           for (int c = 0; c < OH / 32; ++c) {
             uint32_t ov[32];
             tmem_ld32(tO + c * 32, ov);
             tmem_ld_wait();
+            if (!ok) continue;
+            const int col = h * OH + c * 32;
+            if (sg.w == SEG_SPLIT) {
+              // unnormalised partial at scale m_used; combined by attn_split_combine_kernel
+              const int ks = (gridDim.x - 1 - blockIdx.x) % p.kv_splits;
+              float4* dst = reinterpret_cast<float4*>(p.split_o + (((long long)ks * p.n_tokens + trow) * p.hq + head) * DH + col);
 #pragma unroll
-            for (int e = 0; e < 32; e += 2) {
-              float a0, a1;
-              fmul2(a0, a1, __uint_as_float(ov[e]), __uint_as_float(ov[e + 1]), f, f);
-              ov[e] = __float_as_uint(a0);
-              ov[e + 1] = __float_as_uint(a1);
+              for (int e = 0; e < 8; ++e)
+                dst[e] = make_float4(__uint_as_float(ov[4 * e]), __uint_as_float(ov[4 * e + 1]),
+                                     __uint_as_float(ov[4 * e + 2]), __uint_as_float(ov[4 * e + 3]));
+              continue;
             }
-            tmem_st32(tO + c * 32, ov);
+            float a[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) a[e] = __uint_as_float(ov[e]) * w0;
+            for_parts([&](long long slot, int pc) {
+              const float wc = ex2_approx(__ldcg(&p.sk_ml[slot].x) - M);
+              const float4* src =
+                  reinterpret_cast<const float4*>(p.sk_o + (long long)pc * 2 * ROWS * DH) + (slot - (long long)pc * 2 * ROWS);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const float4 t = __ldcg(src + (col / 4 + e) * 2 * ROWS);
+                a[4 * e] += t.x * wc;
+                a[4 * e + 1] += t.y * wc;
+                a[4 * e + 2] += t.z * wc;
+                a[4 * e + 3] += t.w * wc;
+              }
+            });
+            uint4* dst = reinterpret_cast<uint4*>(p.o + trow * p.ldo + (long long)head * DH + col);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              dst[e] = make_uint4(pack_bf16(a[8 * e] * inv, a[8 * e + 1] * inv), pack_bf16(a[8 * e + 2] * inv, a[8 * e + 3] * inv),
+                                  pack_bf16(a[8 * e + 4] * inv, a[8 * e + 5] * inv), pack_bf16(a[8 * e + 6] * inv, a[8 * e + 7] * inv));
+          }
+          if (ok && h == 0 && sg.w == SEG_SPLIT) {
+            const int ks = (gridDim.x - 1 - blockIdx.x) % p.kv_splits;
+            p.split_ml[((long long)ks * p.n_tokens + trow) * p.hq + head] = make_float2(m_used, l);
           }
         }
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[i]);
+      } else if (sg.w == SEG_SPLIT && nt == 0 && i < u.n_q && ok && h == 0) {
+        // empty split: mark the partial as absent
+        const int ks = (gridDim.x - 1 - blockIdx.x) % p.kv_splits;
+        p.split_ml[((long long)ks * p.n_tokens + trow) * p.hq + head] = make_float2(-INFINITY, 0.f);
       }
-      // final O row: wait for the last P.V, normalise, store (each half its O columns)
-      const float lt = exchange(l, n_tiles & 1, false);  // the parity the last tile did NOT use
-      mbar_wait(&o_done[i], (n_tiles - 1) & 1);
-      tc_fence_after();
-      const bool ok = r < nrows;  // every lane joins the .sync.aligned TMEM loads; valid rows store
-      const long long trow = row_base + i * TPT + (ok ? r : 0) / G;  // token row in [0, T)
-      const int head = kvh * G + (ok ? r : 0) % G;
-      const float inv = lt > 0.f ? 1.f / lt : 0.f;
-#pragma unroll
-      for (int c = 0; c < OH / 32; ++c) {
-        uint32_t ov[32];
-        tmem_ld32(tO + c * 32, ov);
-        tmem_ld_wait();
-        if (!ok) continue;
-        const int col = h * OH + c * 32;
-        if (p.kv_splits > 1) {
-          // unnormalised partial at scale m_used; combined by attn_split_combine_kernel
-          float4* dst =
-              reinterpret_cast<float4*>(p.split_o + (((long long)ks * p.n_tokens + trow) * p.hq + head) * DH + col);
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            dst[e] = make_float4(__uint_as_float(ov[4 * e]), __uint_as_float(ov[4 * e + 1]),
-                                 __uint_as_float(ov[4 * e + 2]), __uint_as_float(ov[4 * e + 3]));
-        } else {
-          uint4* dst = reinterpret_cast<uint4*>(p.o + trow * p.ldo + (long long)head * DH + col);
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            dst[e] = make_uint4(pack_bf16(__uint_as_float(ov[8 * e]) * inv, __uint_as_float(ov[8 * e + 1]) * inv),
-                                pack_bf16(__uint_as_float(ov[8 * e + 2]) * inv, __uint_as_float(ov[8 * e + 3]) * inv),
-                                pack_bf16(__uint_as_float(ov[8 * e + 4]) * inv, __uint_as_float(ov[8 * e + 5]) * inv),
-                                pack_bf16(__uint_as_float(ov[8 * e + 6]) * inv, __uint_as_float(ov[8 * e + 7]) * inv));
+      if (sg.w == SEG_PART) {  // rows written: the Q-loader warp publishes them (release store)
+        TRACE(i, ti, 3);
+        asm volatile("bar.sync %0, %1;" ::"n"(SK_PUB), "n"(NS * 32 + 32) : "memory");
+        TRACE(i, ti, 4);
+      } else if (sg.w == SEG_HEAD) {  // consumed: re-arm the parts' flags for the next launch
+        softmax_bar();
+        if (threadIdx.x == 0) {
+          const long long W = Wtot;
+          const long long uend = sk_bound(blockIdx.x + 1, W, gridDim.x) + (u.n_all - sg.z);
+          for (int c = blockIdx.x + 1; c < (int)gridDim.x && sk_bound(c, W, gridDim.x) < uend; ++c) p.sk_flag[c] = 0;
         }
       }
-      if (ok && h == 0 && p.kv_splits > 1)
-        p.split_ml[((long long)ks * p.n_tokens + trow) * p.hq + head] = make_float2(m_used, lt);
-    } else if (p.kv_splits > 1 && n_tiles == 0 && r < nrows && h == 0) {
-      // empty split: mark the partial as absent
-      const long long trow = row_base + i * TPT + r / G;
-      p.split_ml[((long long)ks * p.n_tokens + trow) * p.hq + kvh * G + r % G] = make_float2(-INFINITY, 0.f);
     }
   }
   tc_fence_before();
@@ -500,35 +781,56 @@ __global__ void __launch_bounds__(256) attn_split_combine_kernel(AttnParams p) {
   for (int e = 0; e < PER; ++e) dst[lane + 32 * e] = __float2bfloat16(acc[e] * inv);
 }
 
+template <int DH, int SPL, bool SK>
+int set_smem_attr() {
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(attn_tc_kernel<DH, SPL, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)TcCfg<DH>::SMEM));
+    attr = true;
+  }
+  return 0;
+}
+
 template <int DH, int SPL>
 int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
   using C = TcCfg<DH>;
-  static bool attr = false;
-  if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(attn_tc_kernel<DH, SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-    attr = true;
-  }
   // plane view: rows = hkv * slots, cols = dh
   const long long rows = (long long)p.hkv * (p.head_stride / DH);
   CUtensorMap tk, tv;
   RDKV_TRY(make_tmap(&tk, p.kplane, rows, DH, DH, HALF));
   RDKV_TRY(make_tmap(&tv, p.vplane, rows, DH, DH, HALF));
+  CUtensorMap tq;
+  RDKV_TRY(make_tmap_q(&tq, p.q, p.n_tokens, p.hq, DH, p.ldq, p.hq / p.hkv, ROWS / (p.hq / p.hkv)));
   const int tok_per_cta = 2 * ROWS / (p.hq / p.hkv);  // two Q tiles per CTA
   const int qblocks = (max_new + tok_per_cta - 1) / tok_per_cta;
-  // split the KV range when the (query block x kv head x sequence) grid is too
-  // small for 148 SMs (single-query TTFT) and scratch is available
   AttnParams q = p;
   q.kv_splits = 1;
+  q.n_seqs = n_seqs;
+  q.sk_qblocks = qblocks;
   const int ctas = qblocks * p.hkv * n_seqs, sms = num_sms();
   const int max_tiles = (p.max_ctx + BKV - 1) / BKV;
+  // stream-K (opt-in: p.sk_mode) when the unit grid is at least half a wave; measured
+  // slower than one CTA per unit on the C2/C3 shapes (profiles/r1_attn_experiments.md)
+  if constexpr (SPL == 1) {
+    if (p.sk_mode && p.sk_o && p.sk_ctas >= sms && ctas * 2 > sms && ctas <= SK_MAXSEG) {
+      RDKV_TRY((set_smem_attr<DH, SPL, true>()));
+      CUDA_TRY(launch_k(attn_tc_kernel<DH, SPL, true>, dim3(sms), dim3(Roles<SPL>::THREADS), C::SMEM, st, tk, tv, tq, q));
+      CUDA_TRY(cudaGetLastError());
+      return 0;
+    }
+  }
+  // split the KV range when the (query block x kv head x sequence) grid is too
+  // small for 148 SMs (single-query TTFT) and scratch is available
   if (p.split_o && ctas * 2 <= sms && max_tiles >= 4) {
     int k = sms / ctas;
     k = k < max_tiles / 2 ? k : max_tiles / 2;
     k = k < 16 ? k : 16;
     if (k >= 2 && (size_t)k * p.n_tokens * p.hq * (DH * 4 + 8) <= p.split_bytes) q.kv_splits = k;
   }
+  RDKV_TRY((set_smem_attr<DH, SPL, false>()));
   dim3 grid(qblocks * q.kv_splits, p.hkv, n_seqs);
-  CUDA_TRY(launch_k(attn_tc_kernel<DH, SPL>, grid, dim3(Roles<SPL>::THREADS), C::SMEM, st, tk, tv, q));
+  CUDA_TRY(launch_k(attn_tc_kernel<DH, SPL, false>, grid, dim3(Roles<SPL>::THREADS), C::SMEM, st, tk, tv, tq, q));
   CUDA_TRY(cudaGetLastError());
   if (q.kv_splits > 1) {
     CUDA_TRY(launch_k(attn_split_combine_kernel<DH>, dim3(p.n_tokens, (p.hq + 7) / 8), dim3(256), 0, st, q));
@@ -569,5 +871,23 @@ namespace rdkv {
 size_t attention_split_scratch_bytes(int T, int hq, int dh) {
   if (T <= 0 || T > 512) return 0;
   return (size_t)16 * T * hq * (dh * 4 + 8);
+}
+
+size_t attention_sk_scratch_bytes(int ctas, int dh) {
+  const size_t o = (size_t)ctas * 2 * ROWS * dh * 4, ml = (size_t)ctas * 2 * ROWS * 8, fl = (size_t)ctas * 4;
+  return o + ml + ((fl + 255) / 256) * 256;
+}
+
+void attention_sk_carve(AttnParams& p, void* base, int ctas, int dh) {
+  auto* b = static_cast<uint8_t*>(base);
+  p.sk_o = reinterpret_cast<float*>(b);
+  p.sk_ml = reinterpret_cast<float2*>(b + (size_t)ctas * 2 * ROWS * dh * 4);
+  p.sk_flag = reinterpret_cast<int*>(b + (size_t)ctas * 2 * ROWS * dh * 4 + (size_t)ctas * 2 * ROWS * 8);
+  p.sk_ctas = ctas;
+}
+
+int attention_sk_zero_flags(const AttnParams& p, cudaStream_t st) {
+  if (p.sk_flag) CUDA_TRY(cudaMemsetAsync(p.sk_flag, 0, (size_t)p.sk_ctas * 4, st));
+  return 0;
 }
 }  // namespace rdkv

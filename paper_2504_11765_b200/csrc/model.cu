@@ -85,6 +85,7 @@ struct Ws {
   size_t splitk_bytes;
   void* attn_split;
   size_t attn_split_bytes;
+  void* attn_sk;  // stream-K attention partials + flags (num_sms() CTAs)
   void* argmax;
 };
 
@@ -109,11 +110,13 @@ size_t ws_layout(const rdkv_model_desc& d, int T, int S, Ws* ws, void* base) {
   const size_t osk = take(sk);
   const size_t ask = attention_split_scratch_bytes(T, d.n_heads, d.head_dim);
   const size_t oask = take(ask);
+  const size_t osk_attn = take(attention_sk_scratch_bytes(num_sms(), d.head_dim));
   const size_t oam = take(argmax_scratch_bytes(S));
   if (ws && base) {
     ws->argmax = static_cast<uint8_t*>(base) + oam;
     ws->attn_split = ask ? static_cast<uint8_t*>(base) + oask : nullptr;
     ws->attn_split_bytes = ask;
+    ws->attn_sk = static_cast<uint8_t*>(base) + osk_attn;
     ws->splitk = sk ? static_cast<uint8_t*>(base) + osk : nullptr;
     ws->splitk_bytes = sk;
     auto* b = static_cast<uint8_t*>(base);
@@ -235,6 +238,12 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     ws.splitk_bytes = 0;
     ws.attn_split = nullptr;
     ws.attn_split_bytes = 0;
+    ws.attn_sk = nullptr;
+  }
+  if (ws.attn_sk) {  // stream-K flags start at zero (every launch leaves them zero)
+    AttnParams z{};
+    attention_sk_carve(z, ws.attn_sk, num_sms(), dh);
+    RDKV_TRY(attention_sk_zero_flags(z, st));
   }
   LAUNCH(RDKV_PROF_MISC, 0.0, launch_embed(b->tokens, W(m, 0), ws.x, T, d.hidden, d.vocab, st));
   // small batches run the residual GEMMs split-K; their finalize also applies the
@@ -293,6 +302,14 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
       ap.split_o = static_cast<float*>(ws.attn_split);
       ap.split_ml = reinterpret_cast<float2*>(static_cast<uint8_t*>(ws.attn_split) + o_bytes);
       ap.split_bytes = ws.attn_split_bytes;
+    }
+    static const bool attn_sk = [] {
+      const char* e = std::getenv("RDKV_ATTN_SK");  // "1": stream-K attention schedule (A/B)
+      return e && e[0] == '1';
+    }();
+    if (ws.attn_sk && attn_sk) {
+      ap.sk_mode = 1;
+      attention_sk_carve(ap, ws.attn_sk, num_sms(), dh);
     }
     if (b->layer_ready && b->layer_ready[l])  // layer-wise streaming: this layer's cached KV has landed
       CUDA_TRY(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(b->layer_ready[l]), 0));

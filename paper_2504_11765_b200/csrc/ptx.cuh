@@ -100,6 +100,14 @@ __device__ __forceinline__ void tma_load_2d_nohint(const CUtensorMap* m, uint64_
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_3d_nohint(const CUtensorMap* m, uint64_t* bar, void* dst, int c0,
+                                                   int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
 // L2 eviction-priority policies (createpolicy).
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;

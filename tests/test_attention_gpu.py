@@ -132,3 +132,34 @@ def test_deterministic():
     a = _run(c, 0)
     b = _run(c, 0)
     assert torch.equal(a, b)
+
+
+def _ragged(S, seed, max_new=300, max_cached=3000):
+    r = np.random.default_rng(seed)
+    return [int(x) for x in r.integers(1, max_new, S)], [int(x) for x in r.integers(0, max_cached, S)]
+
+
+# impl 2: grids of more than half a wave of (query block, kv head, sequence)
+# units run stream-K: 148 persistent CTAs with equal KV-tile shares, units cut at
+# share boundaries merged through (m, l, O) partials
+SK_CASES = [
+    ([64] * 32, [2560] * 32, 32, 8, 64),           # the C2 bench batch (256 units)
+    (*_ragged(24, 1), 32, 8, 64),                  # ragged: multi-block queries, one-tile units
+    ([64] * 16, [5120] * 16, 32, 8, 128),          # C3 batch (128 units on 148 SMs)
+    ([64] * 12, [1000, 3, 2000, 64] * 3, 64, 8, 128),  # G = 8: two query blocks per query
+    ([100] * 10, [50] * 10, 16, 16, 64),           # G = 1: one Q tile per unit
+    (*_ragged(40, 2, max_new=70, max_cached=200), 32, 8, 64),  # many short units
+]
+
+
+@pytest.mark.parametrize("case", SK_CASES, ids=[f"sk{i}" for i in range(len(SK_CASES))])
+def test_stream_k_matches_torch_fp32_and_per_unit_grid(case):
+    c = _case(*case)
+    got = _run(c, 2)
+    ref = _reference(c)
+    assert torch.isfinite(got).all()
+    err = (got - ref).abs().max().item() / ref.abs().max().item()
+    assert err <= TOL, f"rel err {err:.3e}"
+    plain = _run(c, 0)  # one CTA per unit
+    assert (got - plain).abs().max().item() / ref.abs().max().item() <= 1e-2
+    assert torch.equal(got, _run(c, 2))  # same batch -> same shares -> same bits
