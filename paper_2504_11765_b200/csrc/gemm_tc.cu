@@ -151,7 +151,7 @@ __device__ __forceinline__ void epilogue_rows(uint32_t taddr, int row, int nb, i
     static_assert(BN % DH == 0, "tile must hold whole heads");
     const int p = row_ok ? ep.pos[row] : 0;
     const int sl = row_ok ? ep.slot[row] : 0;
-    constexpr int HEADS = BN / DH, PER = HEADS > 1 ? HEADS / 2 : 1;
+    constexpr int HEADS = BN / DH, PER = (HEADS + 1) / 2;  // heads per epilogue warpgroup
 #pragma unroll 1
     for (int hh = half * PER; hh < (half + 1) * PER && hh < HEADS; ++hh) {
       float v[DH];
@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 // which is what lifts the L2 -> SM traffic ceiling (~12 TB/s on B200).
 template <int BN>
 struct PairCfg {
-  static constexpr int STAGES = BN == 256 ? 6 : 8;
+  static constexpr int STAGES = BN == 256 ? 6 : BN == 192 ? 7 : 8;
   static constexpr uint32_t A_BYTES = 128 * BK * 2, B_BYTES = (BN / 2) * BK * 2, STAGE = A_BYTES + B_BYTES;
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE + 256;
 };
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   using C = PairCfg<BN>;
   constexpr int STAGES = C::STAGES;
   constexpr uint32_t A_BYTES = C::A_BYTES, B_BYTES = C::B_BYTES, STAGE = C::STAGE;
-  constexpr uint32_t TMEM_COLS = 2 * BN;
+  constexpr uint32_t TMEM_COLS = BN == 192 ? 512 : 2 * BN;  // allocation: a power of two >= 2 x BN
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -965,12 +965,15 @@ int dispatch_pair(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B,
     case EPI_STORE: return launch_pair<BN, EPI_STORE, 0>(ta, tb, M, N, K, ep, stream);
     case EPI_STORE_F32: return launch_pair<BN, EPI_STORE_F32, 0>(ta, tb, M, N, K, ep, stream);
     case EPI_RESID: return launch_pair<BN, EPI_RESID, 0>(ta, tb, M, N, K, ep, stream);
-    case EPI_SWIGLU: return launch_pair<BN, EPI_SWIGLU, 0>(ta, tb, M, N, K, ep, stream);
+    case EPI_SWIGLU:
+      if constexpr (BN % 128 == 0) return launch_pair<BN, EPI_SWIGLU, 0>(ta, tb, M, N, K, ep, stream);
+      return set_error(RDKV_ERR_ARG, "swiglu: tile N %d must hold whole gate/up block pairs", BN);
     case EPI_PUSH: return launch_pair<BN, EPI_PUSH, 0>(ta, tb, M, N, K, ep, stream);
     case EPI_QKV:
       if (dh == 64) return launch_pair<BN, EPI_QKV, 64>(ta, tb, M, N, K, ep, stream);
-      if (dh == 128) return launch_pair<BN, EPI_QKV, 128>(ta, tb, M, N, K, ep, stream);
-      return set_error(RDKV_ERR_ARG, "qkv: head_dim %d unsupported (64 or 128)", dh);
+      if constexpr (BN % 128 == 0)
+        if (dh == 128) return launch_pair<BN, EPI_QKV, 128>(ta, tb, M, N, K, ep, stream);
+      return set_error(RDKV_ERR_ARG, "qkv: head_dim %d unsupported with tile N %d", dh, BN);
     default: return set_error(RDKV_ERR_ARG, "gemm: unknown epilogue %d", kind);
   }
 }
@@ -989,20 +992,23 @@ bool pairs_enabled() {
   }();
   return on;
 }
-TilePlan pick_tiles(int M, int N) {
+TilePlan pick_tiles(int M, int N, bool allow192) {
   const int sms = num_sms();
   struct Cand {
     bool pair;
     int bn;
     double eff;
-  } cands[3] = {{false, 128, 0.60}, {false, 256, 0.83}, {true, 256, 0.90}};
+  } cands[4] = {{false, 128, 0.60}, {false, 256, 0.83}, {true, 256, 0.90}, {true, 192, 0.88}};
   // (efficiencies measured with scripts/gemm_tiles.py at the model shapes; the 256 x 128
   // CTA-pair tile measured slower than both neighbours everywhere and is only reachable
-  // explicitly, tile_n = 384)
+  // explicitly, tile_n = 384.  256 x 192 pairs fit N = 3072 (the 1B-shaped QKV) into
+  // 128 tiles instead of 96 — 1.7 waves of 74 pairs instead of 1.3; not for SwiGLU, whose
+  // tiles hold gate/up 64-column block pairs, nor for 128-wide heads)
   double best = 1e30;
   TilePlan plan{false, 256};
   for (const Cand& c : cands) {
     if (c.pair && (M < 256 || !pairs_enabled())) continue;
+    if (c.bn == 192 && (!allow192 || N % 192)) continue;
     const int rows = c.pair ? 256 : 128;
     const long long units = (long long)((M + rows - 1) / rows) * ((N + c.bn - 1) / c.bn);
     const int slots = c.pair ? sms / 2 : sms;
@@ -1038,9 +1044,15 @@ int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, l
     }
   }
   if (bn == 0 && splits == 1) {
-    const TilePlan tp = pick_tiles(M, N);
+    static const bool allow192_env = [] {
+      const char* e = std::getenv("RDKV_GEMM_192");  // "0": no 256 x 192 pair tiles (A/B)
+      return !(e && e[0] == '0');
+    }();
+    const bool allow192 = allow192_env && kind != EPI_SWIGLU && !(kind == EPI_QKV && dh != 64);
+    const TilePlan tp = pick_tiles(M, N, allow192);
     if (tp.pair && !(kind == EPI_SWIGLU && N % tp.bn != 0)) {
       if (tp.bn == 128) return dispatch_pair<128>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
+      if (tp.bn == 192) return dispatch_pair<192>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
       return dispatch_pair<256>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
     }
     bn = tp.bn;

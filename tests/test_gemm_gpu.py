@@ -36,7 +36,7 @@ def _inputs(M, N, K, seed=0):
 
 
 SHAPES = [(128, 128, 64), (256, 384, 512), (200, 96, 128), (37, 4096, 2048), (2048, 2048, 2048),
-          (1000, 3072, 2048), (64, 2048, 8192)]
+          (1000, 3072, 2048), (2048, 3072, 2048), (64, 2048, 8192)]  # N = 3072: 256 x 192 CTA-pair tiles
 SCRATCH = 64 << 20  # bytes: enables split-K for the small-M shapes below
 
 
@@ -71,7 +71,7 @@ def test_store_f32(M, N, K, tile, split, scratch):
 
 @pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("tile", TILES)
-@pytest.mark.parametrize("M,N,K", [(300, 512, 1024), (2048, 2048, 8192), (64, 2048, 8192)])
+@pytest.mark.parametrize("M,N,K", [(300, 512, 1024), (2048, 2048, 8192), (64, 2048, 8192), (512, 3072, 1024)])
 def test_residual_in_place(M, N, K, tile, split, scratch):
     A, B = _inputs(M, N, K, seed=2)
     X = torch.randn(M, N, device="cuda").to(torch.bfloat16)
