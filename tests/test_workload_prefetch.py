@@ -7,7 +7,7 @@ import pytest
 
 from paper_2504_11765_b200.codec import ModelProfile, synth_blob
 from paper_2504_11765_b200.costs import cached_prefill_work, prefill_work
-from paper_2504_11765_b200.prefetch import PendingQuery, PrefetchState, plan_tasks, prepare, scan
+from paper_2504_11765_b200.prefetch import PendingQuery, PrefetchState, plan_tasks, prepare, promote, scan
 from paper_2504_11765_b200.service import SharedCacheService
 from paper_2504_11765_b200.store import CacheTier, KvKey, KvStore
 from paper_2504_11765_b200.workload import poissonize, uniform_arrivals, zipf_stream
@@ -91,3 +91,21 @@ def test_prepare_failure_resets_state(tmp_path):
     q = PendingQuery(1, 0.0, 1, 8, doc_ids=(2,), doc_tokens=(4,), flagged=True)
     prepare(q, None, svc, None, prof, generator=boom)
     assert q.prefetch_state is PrefetchState.NONE
+
+
+def test_promote_moves_the_longest_disk_prefix_into_memory(tmp_path):
+    prof = ModelProfile("tiny", 2, 256, 4, 64, 2)
+    store = KvStore(tmp_path, 0)  # memory tier off while writing: entries land on disk only
+    for ids in ((1,), (1, 2)):
+        store.put(KvKey(prof.model_hash, ids), synth_blob(prof, ids, 8 * len(ids)))
+    q = PendingQuery(7, 0.0, 3, 16, doc_ids=(1, 2, 3), doc_tokens=(8, 8, 8))
+    assert promote(q, store, prof) is None  # memory tier off: nothing to do
+    store.set_memory_capacity(1 << 20)
+    key = promote(q, store, prof)
+    assert key == KvKey(prof.model_hash, (1, 2))
+    assert store.contains(key) is CacheTier.IN_MEMORY
+    assert store.contains(KvKey(prof.model_hash, (1,))) is CacheTier.ON_DISK
+    assert store.stats().disk_hits == 1
+    assert promote(q, store, prof) is None  # the longest cached prefix is resident now
+    assert store.get(key).outcome.name == "MEMORY_HIT"
+    assert promote(PendingQuery(8, 0.0, 1, 16, doc_ids=(9,), doc_tokens=(8,)), store, prof) is None
