@@ -147,6 +147,63 @@ __device__ __forceinline__ void epilogue_rows(uint32_t taddr, int row, int nb, i
         st_bf16x32(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + col, w);
       }
     }
+  } else if constexpr (EPI == EPI_QKV && DH == 64) {
+    // dh = 64: each epilogue warpgroup takes one quarter of every head and its RoPE
+    // partner quarter (columns 16h.. and 32+16h..), so both halves do the same work
+    // for any head count per tile (a 256x192 tile has 3 heads), and the (cos, sin)
+    // of this token's 16 frequencies is loaded once for all heads of the tile
+    static_assert(BN % DH == 0, "tile must hold whole heads");
+    constexpr int HEADS = BN / DH;
+    const int p = row_ok ? ep.pos[row] : 0;
+    const int sl = row_ok ? ep.slot[row] : 0;
+    float2 cs[16];
+    {
+      const float4* src = reinterpret_cast<const float4*>(ep.rope + (long long)p * DH + half * 32);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float4 t = src[i];
+        cs[2 * i] = make_float2(t.x, t.y);
+        cs[2 * i + 1] = make_float2(t.z, t.w);
+      }
+    }
+#pragma unroll 1
+    for (int hh = 0; hh < HEADS; ++hh) {
+      uint32_t ra[16], rb[16];
+      tmem_ld16(taddr + hh * DH + half * 16, ra);
+      tmem_ld16(taddr + hh * DH + 32 + half * 16, rb);
+      tmem_ld_wait();
+      const int g = (nb * BN + hh * DH) / DH;  // global head index in [q | k | v]
+      if (!row_ok || g >= ep.hq + 2 * ep.hkv) continue;
+      uint32_t wa[8], wb[8];
+      if (g < ep.hq + ep.hkv) {
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          const float a0 = __uint_as_float(ra[i]), a1 = __uint_as_float(ra[i + 1]);
+          const float b0 = __uint_as_float(rb[i]), b1 = __uint_as_float(rb[i + 1]);
+          wa[i / 2] = pack_bf16(a0 * cs[i].x - b0 * cs[i].y, a1 * cs[i + 1].x - b1 * cs[i + 1].y);
+          wb[i / 2] = pack_bf16(b0 * cs[i].x + a0 * cs[i].y, b1 * cs[i + 1].x + a1 * cs[i + 1].y);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          wa[i / 2] = pack_bf16(__uint_as_float(ra[i]), __uint_as_float(ra[i + 1]));
+          wb[i / 2] = pack_bf16(__uint_as_float(rb[i]), __uint_as_float(rb[i + 1]));
+        }
+      }
+      __nv_bfloat16* dst;
+      if (g < ep.hq)
+        dst = ep.q + (long long)row * ep.ldq + (long long)g * DH;
+      else if (g < ep.hq + ep.hkv)
+        dst = ep.kplane + (long long)(g - ep.hq) * ep.head_stride + (long long)sl * DH;
+      else
+        dst = ep.vplane + (long long)(g - ep.hq - ep.hkv) * ep.head_stride + (long long)sl * DH;
+      uint4* da = reinterpret_cast<uint4*>(dst + half * 16);
+      uint4* db = reinterpret_cast<uint4*>(dst + 32 + half * 16);
+      da[0] = make_uint4(wa[0], wa[1], wa[2], wa[3]);
+      da[1] = make_uint4(wa[4], wa[5], wa[6], wa[7]);
+      db[0] = make_uint4(wb[0], wb[1], wb[2], wb[3]);
+      db[1] = make_uint4(wb[4], wb[5], wb[6], wb[7]);
+    }
   } else if constexpr (EPI == EPI_QKV) {
     static_assert(BN % DH == 0, "tile must hold whole heads");
     const int p = row_ok ? ep.pos[row] : 0;
