@@ -36,6 +36,13 @@ struct GemmCfg {
 
 __device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 
+// One 32-byte (full L2 sector) store; `dst` must be 32-B aligned.
+__device__ __forceinline__ void st_global_256(void* dst, const uint32_t (&w)[8]) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "r"(w[0]), "r"(w[1]),
+               "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+               : "memory");
+}
+
 // Store 32 consecutive bf16 values (packed in 16 words) with 16-byte stores.
 __device__ __forceinline__ void st_bf16x32(__nv_bfloat16* dst, const uint32_t (&w)[16]) {
   uint4* d = reinterpret_cast<uint4*>(dst);
@@ -197,12 +204,8 @@ __device__ __forceinline__ void epilogue_rows(uint32_t taddr, int row, int nb, i
         dst = ep.kplane + (long long)(g - ep.hq) * ep.head_stride + (long long)sl * DH;
       else
         dst = ep.vplane + (long long)(g - ep.hq - ep.hkv) * ep.head_stride + (long long)sl * DH;
-      uint4* da = reinterpret_cast<uint4*>(dst + half * 16);
-      uint4* db = reinterpret_cast<uint4*>(dst + 32 + half * 16);
-      da[0] = make_uint4(wa[0], wa[1], wa[2], wa[3]);
-      da[1] = make_uint4(wa[4], wa[5], wa[6], wa[7]);
-      db[0] = make_uint4(wb[0], wb[1], wb[2], wb[3]);
-      db[1] = make_uint4(wb[4], wb[5], wb[6], wb[7]);
+      st_global_256(dst + half * 16, wa);  // 32-B aligned: head rows are 128 B
+      st_global_256(dst + 32 + half * 16, wb);
     }
   } else if constexpr (EPI == EPI_QKV) {
     static_assert(BN % DH == 0, "tile must hold whole heads");
