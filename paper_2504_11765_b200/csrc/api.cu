@@ -88,7 +88,7 @@ extern "C" int rdkv_attention(const void* q, int64_t ldq, void* o, int64_t ldo, 
   const size_t need = attention_split_scratch_bytes(n_tokens, n_heads, head_dim);
   if (scratch && need && scratch_bytes >= need) {
     ap.split_o = static_cast<float*>(scratch);
-    ap.split_ml = reinterpret_cast<float2*>(static_cast<uint8_t*>(scratch) + (size_t)16 * n_tokens * n_heads * head_dim * 4);
+    ap.split_ml = reinterpret_cast<float2*>(static_cast<uint8_t*>(scratch) + (size_t)attention_split_cap(n_tokens) * n_tokens * n_heads * head_dim * 4);
     ap.split_bytes = need;
   }
   auto st = static_cast<cudaStream_t>(stream);

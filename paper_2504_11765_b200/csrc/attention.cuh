@@ -23,6 +23,8 @@ struct AttnParams {
   int contiguous;               // 1: each sequence's KV is one block (blob layout)
   // split-KV (tensor-core kernel): scratch for per-split partials, chosen at launch
   int kv_splits;
+  int seq_off;                  // first sequence of this launch's split units (grid z = sequences seq_off..)
+  int tail_ctas;                // > 0: tail-split grid, CTAs [0, tail_ctas) are whole units of sequences [0, seq_off)
   int n_tokens;                 // T (rows of q / o)
   int max_ctx;                  // max over sequences of n_cached + n_new
   float* split_o;               // [splits][T][hq][dh] fp32
@@ -44,7 +46,9 @@ size_t attention_sk_scratch_bytes(int ctas, int dh);
 void attention_sk_carve(AttnParams& p, void* base, int ctas, int dh);
 int attention_sk_zero_flags(const AttnParams& p, cudaStream_t st);
 
-// split-KV scratch bytes for T tokens (0 when T is too large to ever split)
+// split-KV scratch: attention_split_cap(T) partial slabs of [T][hq][dh] fp32, then
+// as many [T][hq] (max, sum) pairs
+inline int attention_split_cap(int T) { return T <= 512 ? 16 : 4; }
 size_t attention_split_scratch_bytes(int T, int hq, int dh);
 
 // mma.sync kernel (any group size dividing 128, any block size)

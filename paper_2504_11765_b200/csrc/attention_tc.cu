@@ -222,18 +222,44 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
   const int G = p.hq / p.hkv;
   const int TPT = ROWS / G;                 // tokens per Q tile
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int QBn = SK ? p.sk_qblocks : gridDim.x / p.kv_splits;
-  // the single segment of a non-stream-K CTA
+  const int QBn = SK || p.tail_ctas ? p.sk_qblocks : gridDim.x / p.kv_splits;
+  // the single segment of a non-stream-K CTA, and its KV split index
   int4 seg0 = make_int4(0, 0, 0, SEG_WHOLE);
+  int ks0 = 0;
   if constexpr (!SK) {
-    const int s = blockIdx.z, kvh = blockIdx.y;
-    const int xb = gridDim.x - 1 - blockIdx.x;  // longest causal rows first
-    const int qb = xb / p.kv_splits, ks = xb % p.kv_splits;
+    int s, kvh, qb, ks = 0, nsplit = p.kv_splits;
+    if (p.tail_ctas) {
+      // tail-split grid (1-D): CTAs [0, tail_ctas) = whole units of sequences
+      // [0, seq_off) (dispatched first: the full waves); the rest = units of the
+      // remaining sequences in kv_splits KV ranges each, filling the last wave
+      const int ups = QBn * p.hkv;
+      int r;
+      if ((int)blockIdx.x < p.tail_ctas) {
+        s = blockIdx.x / ups;
+        r = blockIdx.x % ups;
+        nsplit = 1;
+      } else {
+        const int v = blockIdx.x - p.tail_ctas;
+        s = p.seq_off + v / (ups * p.kv_splits);
+        r = v % (ups * p.kv_splits);
+        ks = r % p.kv_splits;
+        r /= p.kv_splits;
+      }
+      kvh = r % p.hkv;
+      qb = r / p.hkv;
+    } else {
+      s = blockIdx.z + p.seq_off;
+      kvh = blockIdx.y;
+      const int xb = gridDim.x - 1 - blockIdx.x;  // longest causal rows first
+      qb = xb / p.kv_splits;
+      ks = xb % p.kv_splits;
+    }
     const Unit u = unit_of(p.seq_start, p.seq_new, p.seq_cached, s, qb, kvh, TPT);
     if (u.ntok == 0) return;
-    const int per_split = (u.n_all + p.kv_splits - 1) / p.kv_splits;
+    const int per_split = (u.n_all + nsplit - 1) / nsplit;
     const int ta = min(u.n_all, ks * per_split), tb = min(u.n_all, ta + per_split);
-    seg0 = make_int4((s * QBn + qb) * p.hkv + kvh, ta, tb, p.kv_splits > 1 ? SEG_SPLIT : SEG_WHOLE);
+    seg0 = make_int4((s * QBn + qb) * p.hkv + kvh, ta, tb, nsplit > 1 ? SEG_SPLIT : SEG_WHOLE);
+    ks0 = ks;
   }
 
   if (warp == NS) {
@@ -692,7 +718,7 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
             const int col = h * OH + c * 32;
             if (sg.w == SEG_SPLIT) {
               // unnormalised partial at scale m_used; combined by attn_split_combine_kernel
-              const int ks = (gridDim.x - 1 - blockIdx.x) % p.kv_splits;
+              const int ks = ks0;
               float4* dst = reinterpret_cast<float4*>(p.split_o + (((long long)ks * p.n_tokens + trow) * p.hq + head) * DH + col);
 #pragma unroll
               for (int e = 0; e < 8; ++e)
@@ -723,13 +749,13 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
                                   pack_bf16(a[8 * e + 4] * inv, a[8 * e + 5] * inv), pack_bf16(a[8 * e + 6] * inv, a[8 * e + 7] * inv));
           }
           if (ok && h == 0 && sg.w == SEG_SPLIT) {
-            const int ks = (gridDim.x - 1 - blockIdx.x) % p.kv_splits;
+            const int ks = ks0;
             p.split_ml[((long long)ks * p.n_tokens + trow) * p.hq + head] = make_float2(m_used, l);
           }
         }
       } else if (sg.w == SEG_SPLIT && nt == 0 && i < u.n_q && ok && h == 0) {
         // empty split: mark the partial as absent
-        const int ks = (gridDim.x - 1 - blockIdx.x) % p.kv_splits;
+        const int ks = ks0;
         p.split_ml[((long long)ks * p.n_tokens + trow) * p.hq + head] = make_float2(-INFINITY, 0.f);
       }
       if (sg.w == SEG_PART) {  // rows written: the Q-loader warp publishes them (release store)
@@ -760,7 +786,7 @@ __global__ void __launch_bounds__(256) attn_split_combine_kernel(AttnParams p) {
   pdl_trigger();
   pdl_wait();
   const int t = blockIdx.x, head = blockIdx.y * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (head >= p.hq) return;
+  if (head >= p.hq || t < p.seq_start[p.seq_off]) return;  // tokens of this launch's sequences only
   float M = -INFINITY;
   for (int k = 0; k < p.kv_splits; ++k) M = fmaxf(M, p.split_ml[((long long)k * p.n_tokens + t) * p.hq + head].x);
   constexpr int PER = DH / 32;
@@ -820,6 +846,34 @@ int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
       return 0;
     }
   }
+  // More than one wave whose last wave would leave many SMs idle (the C2 batch: 256
+  // units on 148 SMs): the sequences that fill whole waves run one CTA per unit, the
+  // rest split their KV range in 4 and are merged by the combine kernel; launched
+  // back to back (PDL), the small split CTAs fill the SMs as the first wave drains.
+  static const bool tail_env = [] {
+    const char* e = std::getenv("RDKV_ATTN_TAIL");  // "0": whole units only (A/B)
+    return !(e && e[0] == '0');
+  }();
+  const int ups = qblocks * p.hkv;  // units per sequence
+  const int s_a = ups > 0 ? (ctas / sms) * sms / ups : 0;
+  const double last = (double)(ctas % sms) / sms;
+  constexpr int KT = 4;
+  // (only when a split keeps >= 8 KV tiles: a CTA's fixed cost — TMEM / barrier setup,
+  // pipeline fill, the O store — is several tiles' worth; the C2 batch, 21 tiles per
+  // unit, measured 77 -> 103 us with 5-tile splits, a 41-tile dh=128 batch 212 -> 189 us)
+  if (tail_env && p.split_o && ctas > sms && last > 0.0 && last < 0.9 && s_a >= 1 && s_a < n_seqs &&
+      max_tiles >= 8 * KT && (size_t)KT * p.n_tokens * p.hq * (DH * 4 + 8) <= p.split_bytes) {
+    RDKV_TRY((set_smem_attr<DH, SPL, false>()));
+    AttnParams b = q;
+    b.seq_off = s_a;
+    b.kv_splits = KT;
+    b.tail_ctas = s_a * ups;
+    const int grid = s_a * ups + (n_seqs - s_a) * ups * KT;
+    CUDA_TRY(launch_k(attn_tc_kernel<DH, SPL, false>, dim3(grid), dim3(Roles<SPL>::THREADS), C::SMEM, st, tk, tv, tq, b));
+    CUDA_TRY(launch_k(attn_split_combine_kernel<DH>, dim3(p.n_tokens, (p.hq + 7) / 8), dim3(256), 0, st, b));
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
   // split the KV range when the (query block x kv head x sequence) grid is too
   // small for 148 SMs (single-query TTFT) and scratch is available
   if (p.split_o && ctas * 2 <= sms && max_tiles >= 4) {
@@ -869,8 +923,9 @@ int launch_attention_tc(const AttnParams& p, int head_dim, int n_seqs, int max_n
 
 namespace rdkv {
 size_t attention_split_scratch_bytes(int T, int hq, int dh) {
-  if (T <= 0 || T > 512) return 0;
-  return (size_t)16 * T * hq * (dh * 4 + 8);
+  if (T <= 0) return 0;
+  // up to 16 KV splits for small batches (single-query TTFT), 4 for the tail of large ones
+  return (size_t)attention_split_cap(T) * T * hq * (dh * 4 + 8);
 }
 
 size_t attention_sk_scratch_bytes(int ctas, int dh) {

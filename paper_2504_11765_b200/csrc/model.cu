@@ -298,7 +298,7 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     ap.n_tokens = T;
     ap.max_ctx = b->max_ctx > 0 ? b->max_ctx : 0;
     if (ws.attn_split && b->max_ctx > 0) {
-      const size_t o_bytes = (size_t)16 * T * hq * dh * 4;
+      const size_t o_bytes = (size_t)attention_split_cap(T) * T * hq * dh * 4;
       ap.split_o = static_cast<float*>(ws.attn_split);
       ap.split_ml = reinterpret_cast<float2*>(static_cast<uint8_t*>(ws.attn_split) + o_bytes);
       ap.split_bytes = ws.attn_split_bytes;

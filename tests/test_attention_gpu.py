@@ -163,3 +163,25 @@ def test_stream_k_matches_torch_fp32_and_per_unit_grid(case):
     plain = _run(c, 0)  # one CTA per unit
     assert (got - plain).abs().max().item() / ref.abs().max().item() <= 1e-2
     assert torch.equal(got, _run(c, 2))  # same batch -> same shares -> same bits
+
+
+# more than one wave with a mostly idle last wave: the sequences that fill whole waves
+# run one CTA per unit, the rest split their KV range in 4 (+ combine)
+TAIL_CASES = [
+    ([64] * 24, [5120] * 24, 32, 8, 128),          # dh = 128: 192 units, 18 sequences whole, 6 split
+    ([64] * 40, [4100] * 40, 32, 8, 64),           # dh = 64: 320 units of 33 KV tiles
+    (*_ragged(30, 3, max_new=200, max_cached=6000), 32, 8, 64),
+]
+
+
+@pytest.mark.parametrize("case", TAIL_CASES, ids=[f"tail{i}" for i in range(len(TAIL_CASES))])
+def test_tail_split_matches_torch_fp32_and_whole_units(case):
+    c = _case(*case)
+    got = _run(c, 0, scratch=True)
+    ref = _reference(c)
+    assert torch.isfinite(got).all()
+    err = (got - ref).abs().max().item() / ref.abs().max().item()
+    assert err <= TOL, f"rel err {err:.3e}"
+    whole = _run(c, 0, scratch=False)
+    assert (got - whole).abs().max().item() / ref.abs().max().item() <= 1e-2
+    assert torch.equal(got, _run(c, 0, scratch=True))
