@@ -109,10 +109,29 @@ constexpr float RESCALE_LOG2 = 8.f;   // lazy O rescale: keep a stale row max un
 #endif
 #if RDKV_ATTN_TRACE
 __device__ long long g_attn_trace[6][64][8];
+__device__ long long g_attn_cta[2048][4];  // per CTA: smid, start, after prologue, end (globaltimer ns)
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define CTA_TRACE(ev)                                                                              \
+  do {                                                                                             \
+    const int _c = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);                 \
+    if (threadIdx.x == 0 && _c < 2048) {                                                           \
+      if ((ev) == 1) {                                                                             \
+        unsigned _sm;                                                                              \
+        asm volatile("mov.u32 %0, %smid;" : "=r"(_sm));                                           \
+        g_attn_cta[_c][0] = _sm;                                                                   \
+      }                                                                                            \
+      g_attn_cta[_c][ev] = gtimer();                                                               \
+    }                                                                                              \
+  } while (0)
 #define TRACE(who, j, ev) \
   do { if (blockIdx.x == gridDim.x - 1 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 64) g_attn_trace[who][j][ev] = clock64(); } while (0)
 #else
 #define TRACE(who, j, ev) do { } while (0)
+#define CTA_TRACE(ev) do { } while (0)
 #endif
 #ifndef RDKV_ATTN_EMU
 #define RDKV_ATTN_EMU 3
@@ -201,6 +220,7 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
   constexpr int KH = BKV / SPL;  // keys of a tile per softmax thread
   constexpr int ST = C::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  CTA_TRACE(1);
   uint8_t* smem = smem_raw;
   const uint32_t sb = smem_u32(smem);
   if (sb & 1023) __trap();  // SW128 operands need 1024-B alignment
@@ -359,6 +379,7 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
   };
   pdl_trigger();
   pdl_wait();  // q / KV planes written by the predecessor are visible from here
+  CTA_TRACE(2);
 
   // register budget: the softmax warpgroups hold a 128-score row per thread,
   // the TMA / MMA warpgroup gives its registers up
@@ -774,6 +795,7 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  CTA_TRACE(3);
   if (warp == NS + 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
@@ -898,6 +920,9 @@ int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
 #if RDKV_ATTN_TRACE
 extern "C" RDKV_API int rdkv_debug_attn_trace(long long* out) {
   return cudaMemcpyFromSymbol(out, g_attn_trace, sizeof(g_attn_trace)) == cudaSuccess ? 0 : -8;
+}
+extern "C" RDKV_API int rdkv_debug_attn_cta_trace(long long* out) {
+  return cudaMemcpyFromSymbol(out, g_attn_cta, sizeof(g_attn_cta)) == cudaSuccess ? 0 : -8;
 }
 #endif
 
