@@ -64,15 +64,18 @@ static int make_tmap_q(CUtensorMap* m, const void* q, long long tokens, int hq, 
 namespace {
 
 constexpr int ROWS = 128;
-constexpr int BKV = 128;  // key positions per tile
 constexpr int HALF = 64;  // rows per TMA box (= one KV block of the pool)
 
 template <int DH>
 struct TcCfg {
-  // dh=128 fills TMEM with S0,S1,O0,O1 (4 x 128 columns), so P_i is written over
-  // S_i (already in registers); dh=64 has room for separate P buffers
-  static constexpr bool ALIAS = DH == 128;
-  static constexpr int STAGES = DH == 64 ? 5 : 2;
+  // key positions per tile: 128 at dh = 64; 64 at dh = 128, so S_i (BKV columns),
+  // O_i (dh) and P_i (BKV / 2) of both Q tiles fit the 512 TMEM columns (448) and
+  // Q_i.K^T of the next tile is issued while the softmax still works on this one
+  // (with 128-key tiles at dh = 128, P_i had to live over S_i and each Q tile's
+  // S -> P -> P.V -> next S chain serialised: ~4.3k cycles per 128 keys)
+  static constexpr int BKV = DH == 128 ? 64 : 128;
+  static constexpr bool ALIAS = false;  // P_i over S_i (kept for reference; no shape needs it now)
+  static constexpr int STAGES = DH == 64 ? 5 : 4;
   static constexpr uint32_t QB = ROWS * DH * 2;    // one Q tile
   static constexpr uint32_t KB = BKV * DH * 2;     // one K (or V) tile
   static constexpr uint32_t OFF_Q = 0;             // [2 Q tiles]
@@ -167,6 +170,7 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
 struct Unit {
   int s, kvh, tok0, ntok, n_q, pos0, kv_len, n_all, row_base;
 };
+template <int BKV>
 __device__ __forceinline__ Unit unit_of(const int* seq_start, const int* seq_new, const int* seq_cached, int s, int qb,
                                        int kvh, int TPT) {
   Unit u;
@@ -217,7 +221,10 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
   using R = Roles<SPL>;
   static_assert(!SK || SPL == 1, "stream-K runs one softmax warp per row");
   constexpr int NS = R::NS;
-  constexpr int KH = BKV / SPL;  // keys of a tile per softmax thread
+  constexpr int BKV = C::BKV;
+  constexpr int NH = BKV / HALF;  // TMA boxes (KV blocks) per tile
+  constexpr int KH = BKV / SPL;   // keys of a tile per softmax thread
+  static_assert(KH % 64 == 0, "a softmax thread stores P in 32-column TMEM chunks");
   constexpr int ST = C::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   CTA_TRACE(1);
@@ -274,7 +281,7 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
       qb = xb / p.kv_splits;
       ks = xb % p.kv_splits;
     }
-    const Unit u = unit_of(p.seq_start, p.seq_new, p.seq_cached, s, qb, kvh, TPT);
+    const Unit u = unit_of<BKV>(p.seq_start, p.seq_new, p.seq_cached, s, qb, kvh, TPT);
     if (u.ntok == 0) return;
     const int per_split = (u.n_all + nsplit - 1) / nsplit;
     const int ta = min(u.n_all, ks * per_split), tb = min(u.n_all, ta + per_split);
@@ -316,7 +323,7 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
         seq_s[512 + q] = p.seq_new[q];
         seq_s[1024 + q] = p.seq_cached[q];
       }
-      auto cost = [&](int pr) { return unit_of(p.seq_start, p.seq_new, p.seq_cached, pr / QBn, pr % QBn, 0, TPT).n_all; };
+      auto cost = [&](int pr) { return unit_of<BKV>(p.seq_start, p.seq_new, p.seq_cached, pr / QBn, pr % QBn, 0, TPT).n_all; };
       const int chunk = (npair + 31) / 32;
       const int c0 = min(npair, lane * chunk), c1 = min(npair, c0 + chunk);
       long long mine = 0;
@@ -374,8 +381,8 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
   const int* seq_s = reinterpret_cast<const int*>(smem + C::OFF_SEQ);
   auto unit_at = [&](int code) {
     const int pr = code / p.hkv;
-    if constexpr (SK) return unit_of(seq_s, seq_s + 512, seq_s + 1024, pr / QBn, pr % QBn, code % p.hkv, TPT);
-    return unit_of(p.seq_start, p.seq_new, p.seq_cached, pr / QBn, pr % QBn, code % p.hkv, TPT);
+    if constexpr (SK) return unit_of<BKV>(seq_s, seq_s + 512, seq_s + 1024, pr / QBn, pr % QBn, code % p.hkv, TPT);
+    return unit_of<BKV>(p.seq_start, p.seq_new, p.seq_cached, pr / QBn, pr % QBn, code % p.hkv, TPT);
   };
   pdl_trigger();
   pdl_wait();  // q / KV planes written by the predecessor are visible from here
@@ -395,18 +402,19 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
       const Unit u = unit_at(sg.x);
       const long long row0 = (long long)u.kvh * (p.head_stride / DH);  // first row of this head in the plane view
       const int* bt = p.block_table + (long long)u.s * p.bt_stride;
-      int my_rows[2] = {0, 0};
+      int my_rows[NH] = {};
       for (int j = sg.y; j < sg.z; ++j, ++it) {
         if (((j - sg.y) & 31) == 0 && j + lane < sg.z) {
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
+          for (int h = 0; h < NH; ++h) {
             int pos = (j + lane) * BKV + h * HALF;
             if (pos >= u.kv_len) pos = (j + lane) * BKV;  // masked half: any valid, finite block
             my_rows[h] = (int)(row0 + (long long)bt[pos / p.block_size] * p.block_size + pos % p.block_size);
           }
         }
-        const int rows[2] = {__shfl_sync(0xffffffffu, my_rows[0], (j - sg.y) & 31),
-                             __shfl_sync(0xffffffffu, my_rows[1], (j - sg.y) & 31)};
+        int rows[NH];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) rows[h] = __shfl_sync(0xffffffffu, my_rows[h], (j - sg.y) & 31);
         if (lane == 0) {
           const int st = it % ST;
           TRACE(4, it, 0);
@@ -416,14 +424,14 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
 #pragma unroll
           for (int c = 0; c < DH / 64; ++c)
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
+            for (int h = 0; h < NH; ++h)
               tma_load_2d_nohint(&tmK, &k_full[st], smem + C::OFF_K + st * C::KB + c * (BKV * 128) + h * (HALF * 128),
                                  c * 64, rows[h]);
           mbar_arrive_expect_tx(&v_full[st], C::KB);
 #pragma unroll
           for (int c = 0; c < DH / 64; ++c)
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
+            for (int h = 0; h < NH; ++h)
               tma_load_2d_nohint(&tmV, &v_full[st], smem + C::OFF_V + st * C::KB + c * (BKV * 128) + h * (HALF * 128),
                                  c * 64, rows[h]);
         }
@@ -857,7 +865,7 @@ int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
   q.n_seqs = n_seqs;
   q.sk_qblocks = qblocks;
   const int ctas = qblocks * p.hkv * n_seqs, sms = num_sms();
-  const int max_tiles = (p.max_ctx + BKV - 1) / BKV;
+  const int max_tiles = (p.max_ctx + C::BKV - 1) / C::BKV;
   // stream-K (opt-in: p.sk_mode) when the unit grid is at least half a wave; measured
   // slower than one CTA per unit on the C2/C3 shapes (profiles/r1_attn_experiments.md)
   if constexpr (SPL == 1) {
@@ -941,7 +949,7 @@ int launch_attention_tc(const AttnParams& p, int head_dim, int n_seqs, int max_n
     return e && e[0] == '2' ? 2 : 1;
   }();
   if (head_dim == 64) return spl == 2 ? launch_tc<64, 2>(p, n_seqs, max_new, st) : launch_tc<64, 1>(p, n_seqs, max_new, st);
-  return spl == 2 ? launch_tc<128, 2>(p, n_seqs, max_new, st) : launch_tc<128, 1>(p, n_seqs, max_new, st);
+  return launch_tc<128, 1>(p, n_seqs, max_new, st);  // 64-key tiles at dh = 128: one softmax warp per row
 }
 
 }  // namespace rdkv
