@@ -505,6 +505,12 @@ def _extras(a, eng, gen, spec, items, blobs, keys, qtoks, ws, rank, dev):
         for label, verifier in (("cold_disk", GpuVerifier(dev)), ("cold_disk_host_fnv", None)):
             store = KvStore(root / label, memory_capacity_bytes=0, verifier=verifier)
             cold = []
+            # untimed warm-up: the process's first 80-MiB pinned read buffer costs a
+            # cudaHostAlloc (~50 ms) once; served queries reuse it through the caching allocator
+            store.put(keys[n - 1], blobs[n - 1])
+            _lib.lib().rdkv_drop_page_cache(str(store.path_of(keys[n - 1])).encode())
+            prefill_batch(eng, [PrefillRequest(store.get(keys[n - 1]), None, qtoks[n - 1], None)], timed=False)
+            torch.cuda.synchronize()
             for i in range(min(4, n)):
                 store.put(keys[i], blobs[i])
                 p = str(store.path_of(keys[i])).encode()
@@ -515,6 +521,7 @@ def _extras(a, eng, gen, spec, items, blobs, keys, qtoks, ws, rank, dev):
                 r = prefill_batch(eng, [PrefillRequest(look, None, qtoks[i], None)], timed=False)
                 int(r.next_token[0])
                 cold.append(time.perf_counter() - t0)
+                del look, r  # a served query drops its blob (memory tier off): the pinned read buffer is reused
             res[label] = pct(cold)
     finally:
         import shutil
