@@ -9,27 +9,28 @@
 // tiles (for G = 4: 64 query tokens = a whole C2 query) that share every K/V
 // tile the TMA brings in.
 //
-// Warp roles (320 threads, one CTA per SM):
+// Warp roles (384 threads, one CTA per SM):
 //   warps 0-3   softmax of Q tile 0, warps 4-7 softmax of Q tile 1: one query
 //               row per thread (= one TMEM lane).  Per KV tile: tcgen05.ld the
-//               128 scores, mask, row max (FMNMX3), P = 2^(s*scale - m) with
+//               BKV scores, mask, row max (FMNMX3), P = 2^(s*scale - m) with
 //               packed FFMA2 + MUFU ex2, tcgen05.st of P (bf16 pairs) into TMEM.
 //               The row max is moved lazily (only when it grows by > 2^8), and
 //               only then is the O row in TMEM rescaled.  The two warpgroups
 //               run independently, so one's exp2 overlaps the other's loads.
-//   warp 8      TMA producer: K and V tiles of 128 positions (two 64-row boxes
-//               each, one per KV block of the paged pool / blob), STAGES-deep
-//               smem ring, 128-byte swizzle.
+//   warp 8      TMA producer: K and V tiles of BKV positions (64-row boxes, one
+//               per KV block of the paged pool / blob), STAGES-deep smem ring,
+//               128-byte swizzle.  BKV = 128 at dh = 64, 64 at dh = 128.
 //   warps 9,10  MMA issuers, one thread per Q tile (warp 9 also allocates
-//               TMEM): S_i = Q_i.K^T (M=128, N=128, K=dh, smem operands) and
+//               TMEM): S_i = Q_i.K^T (M=128, N=BKV, K=dh, smem operands) and
 //               O_i += P_i.V with P_i read from TMEM (tcgen05.mma A-from-TMEM,
 //               V as the MN-major B).  Separate issuers keep the two Q tiles'
 //               pipelines independent.
 //   warp 11     Q loader: TMA of each segment's Q tiles (3-D map: dh x heads x
 //               tokens, so the G heads of one kv head land as consecutive rows)
 //               as soon as the previous segment's last Q.K^T has retired.
-// TMEM (512 columns): S_0 S_1 (128 each), O_0 O_1 (dh each), P_0 P_1 (64 each,
-// dh=64) or P_i over S_i (dh=128, after S_i is in registers).
+// TMEM: S_0 S_1 (BKV each), O_0 O_1 (dh each), P_0 P_1 (BKV/2 each): 512 columns
+// at dh = 64, 448 at dh = 128.  Q.K^T of tile j+1 is issued as soon as the
+// softmax has read S(j), so the tensor pipe works while the softmax does.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
