@@ -376,7 +376,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 // which is what lifts the L2 -> SM traffic ceiling (~12 TB/s on B200).
 template <int BN>
 struct PairCfg {
-  static constexpr int STAGES = BN == 256 ? 6 : BN == 192 ? 7 : 8;
+  // BN = 384: a single TMEM accumulator (384 of 512 columns) filled by two MMAs per
+  // k-step (N = 256 + 128); only planned when every pair gets at most one tile
+  static constexpr int NACC = BN == 384 ? 1 : 2;
+  static constexpr int STAGES = BN == 384 ? 5 : BN == 256 ? 6 : BN == 192 ? 7 : 8;
   static constexpr uint32_t A_BYTES = 128 * BK * 2, B_BYTES = (BN / 2) * BK * 2, STAGE = A_BYTES + B_BYTES;
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE + 256;
 };
@@ -388,7 +391,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   using C = PairCfg<BN>;
   constexpr int STAGES = C::STAGES;
   constexpr uint32_t A_BYTES = C::A_BYTES, B_BYTES = C::B_BYTES, STAGE = C::STAGE;
-  constexpr uint32_t TMEM_COLS = BN == 192 ? 512 : 2 * BN;  // allocation: a power of two >= 2 x BN
+  constexpr int NACC = C::NACC;
+  constexpr uint32_t TMEM_COLS = NACC * BN <= 256 ? NACC * BN : 512;  // a power of two >= NACC x BN
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -441,7 +445,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * STAGE);
           const uint32_t bar = mapa_shared(smem_u32(&full[stage]), 0);
           tma_load_2d_2sm(&tmA, bar, sA + stage * A_BYTES, kb * BK, mb * 256 + (int)rank * 128, pol_act);
-          tma_load_2d_2sm(&tmB, bar, sB + stage * B_BYTES, kb * BK, nb * BN + (int)rank * (BN / 2), pol_act);
+          if constexpr (BN == 384) {
+            // each CTA holds its N-half of both MMAs: rows [128 r, +128) of the N = 256 one and
+            // [256 + 64 r, +64) of the N = 128 one (64-row boxes)
+            uint8_t* b = sB + stage * B_BYTES;
+            tma_load_2d_2sm(&tmB, bar, b, kb * BK, nb * BN + (int)rank * 128, pol_act);
+            tma_load_2d_2sm(&tmB, bar, b + 64 * 128, kb * BK, nb * BN + (int)rank * 128 + 64, pol_act);
+            tma_load_2d_2sm(&tmB, bar, b + 128 * 128, kb * BK, nb * BN + 256 + (int)rank * 64, pol_act);
+          } else {
+            tma_load_2d_2sm(&tmB, bar, sB + stage * B_BYTES, kb * BK, nb * BN + (int)rank * (BN / 2), pol_act);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -451,7 +464,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(256, BN);
+      constexpr int BN1 = BN == 384 ? 256 : BN;  // first (or only) MMA's N
+      constexpr uint32_t idesc = idesc_bf16_f32(256, BN1);
+      constexpr uint32_t idesc2 = idesc_bf16_f32(256, 128);
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
       for (int u = pair; u < units; u += npairs) {
@@ -465,6 +480,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           const uint64_t bd = sdesc_k_sw128(smem_u32(sB + stage * B_BYTES));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) umma_bf16_2sm(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+          if constexpr (BN == 384) {
+            const uint64_t bd2 = sdesc_k_sw128(smem_u32(sB + stage * B_BYTES + 128 * 128));
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              umma_bf16_2sm(d + 256, ad + 2 * k, bd2 + 2 * k, idesc2, (kb | k) != 0 ? 1u : 0u);
+          }
           umma_commit_2sm(&empty[stage], 0x3);
           if (++stage == STAGES) {
             stage = 0;
@@ -472,7 +493,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         }
         umma_commit_2sm(&tfull[acc], 0x3);
-        acc ^= 1;
+        if (NACC == 2) acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
     }
@@ -492,7 +513,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(acc ? tempty1 : tempty0);
-      acc ^= 1;
+      if (NACC == 2) acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
   }
@@ -1020,7 +1041,7 @@ int dispatch_pair(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B,
                   int kind, int dh, const GemmEpi& ep, cudaStream_t stream) {
   CUtensorMap ta, tb;
   RDKV_TRY(make_tmap(&ta, A, M, K, lda, 128));
-  RDKV_TRY(make_tmap(&tb, B, N, K, ldb, BN / 2));
+  RDKV_TRY(make_tmap(&tb, B, N, K, ldb, BN == 384 ? 64 : BN / 2));
   switch (kind) {
     case EPI_STORE: return launch_pair<BN, EPI_STORE, 0>(ta, tb, M, N, K, ep, stream);
     case EPI_STORE_F32: return launch_pair<BN, EPI_STORE_F32, 0>(ta, tb, M, N, K, ep, stream);
@@ -1058,7 +1079,7 @@ TilePlan pick_tiles(int M, int N, bool allow192) {
     bool pair;
     int bn;
     double eff;
-  } cands[4] = {{false, 128, 0.60}, {false, 256, 0.83}, {true, 256, 0.90}, {true, 192, 0.88}};
+  } cands[5] = {{false, 128, 0.60}, {false, 256, 0.83}, {true, 256, 0.90}, {true, 192, 0.88}, {true, 384, 0.90}};
   // (efficiencies measured with scripts/gemm_tiles.py at the model shapes; the 256 x 128
   // CTA-pair tile measured slower than both neighbours everywhere and is only reachable
   // explicitly, tile_n = 384.  256 x 192 pairs fit N = 3072 (the 1B-shaped QKV) into
@@ -1069,6 +1090,13 @@ TilePlan pick_tiles(int M, int N, bool allow192) {
   for (const Cand& c : cands) {
     if (c.pair && (M < 256 || !pairs_enabled())) continue;
     if (c.bn == 192 && (!allow192 || N % 192)) continue;
+    // 256 x 384 pairs: one accumulator, so only when every pair gets at most one tile
+    // (the N = 6144 QKV of the 8B shape: 64 tiles instead of 96 256 x 256 ones on 74 pairs)
+    static const bool allow384 = [] {
+      const char* e = std::getenv("RDKV_GEMM_384");  // "0": no 256 x 384 pair tiles (A/B)
+      return !(e && e[0] == '0');
+    }();
+    if (c.bn == 384 && (!allow384 || N % 384 || (long long)((M + 255) / 256) * (N / 384) > sms / 2)) continue;
     const int rows = c.pair ? 256 : 128;
     const long long units = (long long)((M + rows - 1) / rows) * ((N + c.bn - 1) / c.bn);
     const int slots = c.pair ? sms / 2 : sms;
@@ -1089,8 +1117,8 @@ int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, l
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15)
     return set_error(RDKV_ERR_ARG, "gemm: operands must be 16-byte aligned");
   if ((lda | ldb) & 7) return set_error(RDKV_ERR_ARG, "gemm: leading dims must be multiples of 8");
-  if (bn != 0 && bn != 128 && bn != 256 && bn != 384 && bn != 512)
-    return set_error(RDKV_ERR_ARG, "gemm: tile N %d must be 128, 256 (or 384/512 for CTA pairs)", bn);
+  if (bn != 0 && bn != 128 && bn != 256 && bn != 384 && bn != 512 && bn != 640)
+    return set_error(RDKV_ERR_ARG, "gemm: tile N %d must be 128, 256 (or 384/512/640 for CTA pairs)", bn);
   if (kind == EPI_SWIGLU && N % 128 != 0) return set_error(RDKV_ERR_ARG, "swiglu: N must be a multiple of 128");
   int splits = 1;
   if (ep.splitk_ws) {
@@ -1113,13 +1141,19 @@ int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, l
     if (tp.pair && !(kind == EPI_SWIGLU && N % tp.bn != 0)) {
       if (tp.bn == 128) return dispatch_pair<128>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
       if (tp.bn == 192) return dispatch_pair<192>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
+      if (tp.bn == 384) return dispatch_pair<384>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
       return dispatch_pair<256>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
     }
     bn = tp.bn;
   }
-  if (bn == 512 || bn == 384) {  // explicit CTA-pair request (tests): 512 -> 256 x 256, 384 -> 256 x 128
+  if (bn == 512 || bn == 384 || bn == 640) {  // explicit CTA-pair request (tests): 512 -> 256 x 256, 384 -> 256 x 128,
+    // 640 -> 256 x 384 (one accumulator)
     if (M < 256) return set_error(RDKV_ERR_ARG, "gemm: CTA-pair tiles need M >= 256");
     if (bn == 384) return dispatch_pair<128>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
+    if (bn == 640) {
+      if (N % 384) return set_error(RDKV_ERR_ARG, "gemm: 256 x 384 tiles need N %% 384 == 0");
+      return dispatch_pair<384>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
+    }
     return dispatch_pair<256>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
   }
   if (bn == 0) bn = pick_bn(M, N);

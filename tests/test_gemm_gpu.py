@@ -9,7 +9,7 @@ from paper_2504_11765_b200 import _lib
 
 pytestmark = pytest.mark.gpu
 
-TILES = [0, 128, 256, 384, 512]  # 0 automatic; 384 / 512 = CTA-pair (cta_group::2) 256x128 / 256x256 tiles
+TILES = [0, 128, 256, 384, 512, 640]  # 0 automatic; 384 / 512 / 640 = CTA-pair (cta_group::2) 256x128 / 256x256 / 256x384 tiles
 
 
 def _ptr(t):
@@ -19,9 +19,11 @@ def _ptr(t):
 def _gemm(A, B, D, epi, R=None, tile=0, scratch=None):
     s = torch.cuda.current_stream().cuda_stream
     M, K = A.shape
-    if tile in (384, 512) and M < 256:
+    if tile in (384, 512, 640) and M < 256:
         pytest.skip("CTA-pair tiles need M >= 256")
     N = B.shape[0]
+    if tile == 640 and N % 384:
+        pytest.skip("256x384 tiles need N % 384 == 0")
     _lib.check(_lib.lib().rdkv_gemm_bf16_ex(
         _ptr(A), A.stride(0), _ptr(B), B.stride(0), _ptr(D), D.stride(0),
         _ptr(R), R.stride(0) if R is not None else 0, M, N, K, epi, tile,
@@ -83,7 +85,7 @@ def test_residual_in_place(M, N, K, tile, split, scratch):
 
 @pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("tile", TILES)
-@pytest.mark.parametrize("M,N,K", [(130, 256, 128), (640, 2 * 8192, 2048), (64, 384, 512), (64, 4096, 2048)])
+@pytest.mark.parametrize("M,N,K", [(130, 256, 128), (640, 2 * 8192, 2048), (64, 384, 512), (64, 4096, 2048), (512, 3072, 512)])
 def test_swiglu(M, N, K, tile, split, scratch):
     A, B = _inputs(M, N, K, seed=3)
     D = torch.full((M, N // 2), float("nan"), device="cuda", dtype=torch.bfloat16)
