@@ -155,6 +155,10 @@ class CalibratedExecutor:
     that one GPU cannot host; results are modeled, and labeled as such."""
 
     costs: dict
+    # per-byte cost of a memory-tier hit; None = the measured pinned-host-tier load.
+    # C4 "P2P on" sets it to a peer-HBM fetch (K3p over NVLink) — the memory tier
+    # then stands for the instances' pooled HBM
+    memory_tier_s_per_byte: float | None = None
 
     def bind(self, config: SimConfig, cache: TierMirror) -> None:
         self.cfg = config
@@ -167,7 +171,8 @@ class CalibratedExecutor:
         prefill = c["prefill_s_by_cached_docs"][d.best]
         if d.best == 0:
             return 0.0, prefill
-        per = c["host_tier_load_s_per_byte"] if d.tier is Tier.MEMORY else c["disk_read_verify_s_per_byte"]
+        mem = c["host_tier_load_s_per_byte"] if self.memory_tier_s_per_byte is None else self.memory_tier_s_per_byte
+        per = mem if d.tier is Tier.MEMORY else c["disk_read_verify_s_per_byte"]
         return per * d.size_bytes, prefill
 
     def generation_time(self, task: GenTask) -> float:

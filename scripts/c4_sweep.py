@@ -24,7 +24,14 @@ spec = get_spec("llama-3-8b")
 items = zipf_stream(10000, 1.0, 2000, seed=1, k=10, q_tokens=64, doc_tokens=512)
 full = costs["prefill_s_by_cached_docs"][0]
 cap = 8 / full  # all-miss capacity of 8 instances
-for gen, mem in ((False, 0), (True, 0), (True, 256 << 30)):
+# "P2P on": the memory tier is the 8 instances' pooled HBM KV tiers (100 GiB each),
+# a hit fetched from the holder over NVLink by the K3p gather (modeled: NVLink 5 at
+# 0.85 x 900 GB/s; one GPU here cannot measure it).  "P2P off": the shared pinned
+# host tier (256 GiB) at the measured layer-streamed H2D cost.
+NVLINK_S_PER_BYTE = 1.0 / (0.85 * 900e9)
+configs = ((False, 0, None, "none"), (True, 0, None, "none"), (True, 256 << 30, None, "host tier (P2P off)"),
+           (True, 8 * (100 << 30), NVLINK_S_PER_BYTE, "peer HBM tier (P2P on, modeled NVLink)"))
+for gen, mem, mem_cost, tier in configs:
     for frac in (0.5, 1.0, 1.5, 2.0, 3.0):
         rate = cap * frac
         devs = tuple(DeviceProfile(f"b200-{i}", DeviceKind.INFERENCE_GPU, 1.0) for i in range(8))
@@ -33,10 +40,11 @@ for gen, mem in ((False, 0), (True, 0), (True, 256 << 30)):
         cfg = SimConfig(configuration=Configuration.SHARED_GPU_N, devices=devs,
                         cost=CostParams(model=spec.profile(), network_delay=0.0), arrival=ArrivalSpec(rate=rate),
                         k=10, tries=3, seed=1, threshold=0.5, memory_capacity_bytes=mem)
-        report, records = run(cfg, items, CalibratedExecutor(costs))
+        report, records = run(cfg, items, CalibratedExecutor(costs, memory_tier_s_per_byte=mem_cost))
         s = summarize(records)
         tries = report.per_try
-        print(json.dumps({"instances": 8, "generator": gen, "host_memory_tier_bytes": mem, "rate_qps": rate,
+        print(json.dumps({"instances": 8, "generator": gen, "memory_tier": tier, "memory_tier_bytes": mem,
+                          "rate_qps": rate,
                           "rate_over_all_miss_capacity": frac,
                           "qps_per_try": [t.throughput for t in tries],
                           "latency_median_ms_per_try": [t.latency_median * 1e3 for t in tries],

@@ -126,6 +126,9 @@ def test_calibrated_executor_uses_measured_costs():
     assert ex.serve(disk) == (1000 * 1e-9, 0.02)
     mem = Dispatch(0, it, it.doc_ids[:2], it.doc_tokens[:2], 2, Tier.MEMORY, 16, 4, 1000)
     assert ex.serve(mem) == (1000 * 1e-11, 0.01)
+    peer = CalibratedExecutor(costs, memory_tier_s_per_byte=2e-12)  # C4 "P2P on": memory tier = pooled peer HBM
+    peer.bind(cfg, None)
+    assert peer.serve(mem) == (1000 * 2e-12, 0.01) and peer.serve(disk) == (1000 * 1e-9, 0.02)
     assert ex.generation_time(GenTask(it.doc_ids[:2], 16, 100)) == 0.09
     report, records = run(cfg, zipf_stream(50, 1.0, 20, seed=0, k=2, q_tokens=4, doc_tokens=8), CalibratedExecutor(costs))
     assert len(records) == 20 and all(r.prefill == 0.03 for r in records)   # no generator: every query misses
