@@ -69,13 +69,19 @@ def _peaks():
 
 
 def _config(a, n):
+    from paper_2504_11765_b200.model import get_spec
+    spec = get_spec(a.model)
+    name = {"tiny": "C1", "llama-3.2-1b": "C2", "llama-3-8b": "C3"}.get(a.model, "custom")
+    kv_gb = a.batch * a.k * a.doc_tokens * spec.kv_bytes_per_token() / 1e9
+    w_gb = (spec.nonembedding_params() + spec.vocab * spec.hidden) * 2 / 1e9  # layers + LM head (embedding: gathered rows only)
     return {
-        "workload": f"C2 {a.model}-shaped random-init, {a.k} docs x {a.doc_tokens} tok + {a.q_tokens}-tok query, "
+        "workload": f"{name} {a.model}-shaped random-init, {a.k} docs x {a.doc_tokens} tok + {a.q_tokens}-tok query, "
                     f"warm composite-prefix KV cache, Zipf(1.0) over 10k docs",
         "queries_per_step_per_gpu": a.batch, "global_queries_per_step": a.batch * n,
         "docs_per_query": a.k, "doc_tokens": a.doc_tokens, "query_tokens": a.q_tokens,
         "cached_tokens_per_query": a.k * a.doc_tokens, "parallelism": f"replicas x{n} (one instance per GPU)",
-        "l2_policy": "inputs exceed L2: each step reads >2 GB of KV plus 2.5 GB of weights (126 MB L2)",
+        "l2_policy": f"inputs exceed L2: each step reads {kv_gb:.1f} GB of cached KV plus {w_gb:.1f} GB of weights "
+                     f"(126 MB L2)",
     }
 
 

@@ -29,7 +29,7 @@ def test_reference_arm_prints_the_contract_line():
     assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == line["value"] and cb["sample"]
     assert line["e2e"] == {"value": line["value"], "unit": "queries/s", "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
-    assert line["config"]["workload"].startswith("C2 tiny-shaped")
+    assert line["config"]["workload"].startswith("C1 tiny-shaped")
 
 
 def test_roofline_inputs_from_committed_profiles():
