@@ -178,6 +178,21 @@ RDKV_API int rdkv_kv_unpack_heads(const rdkv_unpack_job* jobs_dev, int n_jobs, i
                                   int kv_heads, int head_dim, int64_t pool_slots, int elem_width, int layer_begin,
                                   int layer_end, int head_begin, int src_kv_heads, void* stream);
 
+/* Layer-wise streaming of one batch's cached KV (host tier -> HBM -> pool) in one
+ * call: for every layer l, the H2D copy of layer slice l of each (host_src[c],
+ * dev_dst[c]) payload pair (copy_layers layers per copy, bytes_per_layer[c] each)
+ * on h2d_stream, then on unpack_stream a wait for copied_events[l], the K3
+ * unpack of layer l (rdkv_kv_unpack_heads semantics) and a record of
+ * layer_events[l] — the events rdkv_batch.layer_ready hands to the forward.
+ * n_copies = 0 unpacks device-resident payloads only.  Events must exist
+ * (created/recorded once before). */
+RDKV_API int rdkv_kv_stream_layers(const rdkv_unpack_job* jobs_dev, int n_jobs, int max_tokens,
+                                   const int32_t* block_table_dev, int block_size, void* pool_base, int layers,
+                                   int kv_heads, int head_dim, int64_t pool_slots, int elem_width, int head_begin,
+                                   int src_kv_heads, int n_copies, void* const* host_src, void* const* dev_dst,
+                                   const size_t* bytes_per_layer, int copy_layers, void* h2d_stream,
+                                   void* unpack_stream, void* const* copied_events, void* const* layer_events);
+
 /* Copy the first n_tokens slots of pool block src_block into dst_block, in every
  * (layer, K|V, head) plane: one strided DMA (cudaMemcpy2DAsync, L*2*Hkv rows).
  * Copy-on-write of a resident prefix's partial last block, so a query can append

@@ -428,6 +428,34 @@ int rdkv_kv_unpack(const rdkv_unpack_job* jobs_dev, int n_jobs, int max_tokens, 
                               head_dim, pool_slots, elem_width, layer_begin, layer_end, 0, kv_heads, stream);
 }
 
+int rdkv_kv_stream_layers(const rdkv_unpack_job* jobs_dev, int n_jobs, int max_tokens, const int32_t* block_table_dev,
+                          int block_size, void* pool_base, int layers, int kv_heads, int head_dim, int64_t pool_slots,
+                          int elem_width, int head_begin, int src_kv_heads, int n_copies, void* const* host_src,
+                          void* const* dev_dst, const size_t* bytes_per_layer, int copy_layers, void* h2d_stream,
+                          void* unpack_stream, void* const* copied_events, void* const* layer_events) {
+  if (block_size <= 0 || !pool_base || !jobs_dev || layers <= 0 || !layer_events || copy_layers <= 0 ||
+      (n_copies > 0 && (!host_src || !dev_dst || !bytes_per_layer || !copied_events)))
+    return set_error(RDKV_ERR_ARG, "kv_stream_layers: bad arguments");
+  auto h2d = static_cast<cudaStream_t>(h2d_stream), up = static_cast<cudaStream_t>(unpack_stream);
+  for (int l = 0; l < layers; ++l) {
+    if (n_copies > 0 && l % copy_layers == 0) {
+      const int l1 = std::min(layers, l + copy_layers);
+      for (int c = 0; c < n_copies; ++c) {
+        const size_t per = bytes_per_layer[c];
+        CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(dev_dst[c]) + (size_t)l * per,
+                                 static_cast<const uint8_t*>(host_src[c]) + (size_t)l * per, (size_t)(l1 - l) * per,
+                                 cudaMemcpyHostToDevice, h2d));
+      }
+      for (int ll = l; ll < l1; ++ll) CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(copied_events[ll]), h2d));
+    }
+    if (n_copies > 0) CUDA_TRY(cudaStreamWaitEvent(up, static_cast<cudaEvent_t>(copied_events[l]), 0));
+    RDKV_TRY(launch_kv_unpack(jobs_dev, n_jobs, max_tokens, block_table_dev, block_size, pool_base, l, l + 1, kv_heads,
+                              head_dim, pool_slots, elem_width, up, head_begin, src_kv_heads));
+    CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(layer_events[l]), up));
+  }
+  return 0;
+}
+
 int rdkv_kv_unpack_heads(const rdkv_unpack_job* jobs_dev, int n_jobs, int max_tokens, const int32_t* block_table_dev,
                          int block_size, void* pool_base, int layers, int kv_heads, int head_dim, int64_t pool_slots,
                          int elem_width, int layer_begin, int layer_end, int head_begin, int src_kv_heads,

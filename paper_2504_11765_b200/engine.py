@@ -71,6 +71,10 @@ _N_SIG = {
                                        C.c_void_p]),
     "rdkv_kv_copy_block": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int,
                                      C.c_int, C.c_void_p]),
+    "rdkv_kv_stream_layers": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int,
+                                        C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int,
+                                        C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_size_t), C.c_int,
+                                        C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
     "rdkv_ipc_handle": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),
     "rdkv_ipc_open": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "rdkv_ipc_close": (C.c_int, [C.c_void_p]),
@@ -337,6 +341,14 @@ class LayerStreamer:
         # 88% at 16 — fewer, larger DMAs, still early enough for the first attention)
         self.copy_layers = max(1, int(os.environ.get("RDKV_H2D_LAYERS", "2")))
         self.handles = (C.c_void_p * L)()
+        self.copied_handles = (C.c_void_p * L)()
+        # torch creates CUDA events lazily: record each once so the native call gets real handles
+        cur = torch.cuda.current_stream(engine.device)
+        for l in range(L):
+            self.events[l].record(cur)
+            self.copied[l].record(cur)
+            self.handles[l] = self.events[l].cuda_event
+            self.copied_handles[l] = self.copied[l].cuda_event
 
     def launch(self, pool: KvPool, jobs, block_table: torch.Tensor, jobs_dev: torch.Tensor, main: torch.cuda.Stream,
                first_event=None, last_event=None, h2d: Sequence[tuple[torch.Tensor, torch.Tensor]] = (),
@@ -354,28 +366,30 @@ class LayerStreamer:
             self.h2d.wait_stream(main)
             for _, dev in h2d:
                 dev.record_stream(self.h2d)
-        g = self.copy_layers
-        for l in range(L):
-            if h2d and l % g == 0:
-                l1 = min(L, l + g)
-                with torch.cuda.stream(self.h2d):
-                    for host, dev in h2d:
-                        per = host.numel() // L
-                        dev[l * per:l1 * per].copy_(host[l * per:l1 * per], non_blocking=True)
-                    for ll in range(l, l1):
-                        self.copied[ll].record(self.h2d)
-            with torch.cuda.stream(self.stream):
-                if l == 0 and first_event is not None:
-                    first_event.record(self.stream)
-                if h2d:
-                    self.stream.wait_event(self.copied[l])
-                kv_unpack(pool, jobs, block_table, stream=self.stream, layers=(l, l + 1), jobs_dev=jobs_dev,
-                          heads=heads)
-                self.events[l].record(self.stream)
+        if first_event is not None:
+            first_event.record(self.stream)
+        if not jobs:  # nothing to move: the layer events complete at once
+            for ev in self.events:
+                ev.record(self.stream)
+            if last_event is not None:
+                last_event.record(self.stream)
+            return self.handles
+        # the whole per-layer [H2D ->] unpack -> event chain is enqueued by one native call
+        # (enqueueing it from Python cost ~0.7 ms of host time per query, which delayed the
+        # forward's launch behind the copies it overlaps with)
+        s = pool.spec
+        h0, src_heads = heads if heads is not None else (0, s.kv_heads)
+        n = len(h2d)
+        hosts = (C.c_void_p * max(n, 1))(*[host.data_ptr() for host, _ in h2d])
+        devs = (C.c_void_p * max(n, 1))(*[dev.data_ptr() for _, dev in h2d])
+        per = (C.c_size_t * max(n, 1))(*[host.numel() * host.element_size() // L for host, _ in h2d])
+        _lib.check(_L().rdkv_kv_stream_layers(
+            jobs_dev.data_ptr(), len(jobs), max(nt for _, nt, _ in jobs), block_table.data_ptr(), pool.block_size,
+            pool.data.data_ptr(), s.layers, s.kv_heads, s.head_dim, pool.slots, 2, h0, src_heads, n, hosts, devs,
+            per, self.copy_layers, _stream_ptr(self.h2d), _stream_ptr(self.stream), self.copied_handles,
+            self.handles))
         if last_event is not None:
             last_event.record(self.stream)
-        for l, ev in enumerate(self.events):
-            self.handles[l] = ev.cuda_event
         return self.handles
 
 

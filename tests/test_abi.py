@@ -32,5 +32,5 @@ def test_abi_version():
 def test_python_signatures_cover_host_symbols():
     # every host-side entry point has a ctypes signature in _lib.SIGNATURES
     host = {n for n in declared_symbols() if not n.startswith(("rdkv_model", "rdkv_forward", "rdkv_workspace",
-                                                               "rdkv_kv_unpack", "rdkv_kv_copy", "rdkv_kv_peer", "rdkv_ipc", "rdkv_tp", "rdkv_memcpy", "rdkv_profile"))}
+                                                               "rdkv_kv_unpack", "rdkv_kv_stream", "rdkv_kv_copy", "rdkv_kv_peer", "rdkv_ipc", "rdkv_tp", "rdkv_memcpy", "rdkv_profile"))}
     assert host <= set(_lib.SIGNATURES), host - set(_lib.SIGNATURES)
