@@ -1073,25 +1073,30 @@ bool pairs_enabled() {
   }();
   return on;
 }
-TilePlan pick_tiles(int M, int N, bool allow192) {
+TilePlan pick_tiles(int M, int N, int K, bool allow192) {
   const int sms = num_sms();
   struct Cand {
     bool pair;
     int bn;
     double eff;
-  } cands[5] = {{false, 128, 0.60}, {false, 256, 0.83}, {true, 256, 0.90}, {true, 192, 0.88}, {true, 384, 0.90}};
-  // (efficiencies measured with scripts/gemm_tiles.py at the model shapes; the 256 x 128
-  // CTA-pair tile measured slower than both neighbours everywhere and is only reachable
-  // explicitly, tile_n = 384.  256 x 192 pairs fit N = 3072 (the 1B-shaped QKV) into
-  // 128 tiles instead of 96 — 1.7 waves of 74 pairs instead of 1.3; not for SwiGLU, whose
-  // tiles hold gate/up 64-column block pairs, nor for 128-wide heads)
+  } cands[5] = {{false, 128, 0.60}, {false, 256, 0.83}, {true, 256, 0.975}, {true, 192, 0.95}, {true, 384, 0.975}};
+  // Cost = waves x k-blocks x tile width / efficiency + a per-kernel fixed cost (prologue,
+  // pipeline fill, the last tile's exposed epilogue), calibrated with scripts/gemm_tiles.py:
+  // at N = 2048 single-CTA 128x256 tiles take 15.2 / 52.3 us for K = 2048 / 8192 and
+  // 256x256 CTA pairs 16.3 / 47.9 us -> pairs stream k-blocks ~18% faster but pay ~3 us
+  // more of fixed cost (cluster launch, 2-SM TMEM allocation and barriers), so short-K
+  // single-wave GEMMs (the O projection) run on single CTAs.  The 256 x 128 CTA-pair tile
+  // measured slower than both neighbours and is only reachable explicitly (tile_n = 384).
+  // 256 x 192 pairs fit N = 3072 into 128 tiles (not for SwiGLU, whose tiles hold gate/up
+  // 64-column block pairs, nor for 128-wide heads); 256 x 384 pairs (one accumulator) only
+  // when every pair gets at most one tile.
+  constexpr double F_SINGLE = 2255.0, F_PAIR = 4597.0;  // in (k-block x 256 / 0.83) units ~ 1.25 ns
+  const double kb = K / (double)BK;
   double best = 1e30;
   TilePlan plan{false, 256};
   for (const Cand& c : cands) {
     if (c.pair && (M < 256 || !pairs_enabled())) continue;
     if (c.bn == 192 && (!allow192 || N % 192)) continue;
-    // 256 x 384 pairs: one accumulator, so only when every pair gets at most one tile
-    // (the N = 6144 QKV of the 8B shape: 64 tiles instead of 96 256 x 256 ones on 74 pairs)
     static const bool allow384 = [] {
       const char* e = std::getenv("RDKV_GEMM_384");  // "0": no 256 x 384 pair tiles (A/B)
       return !(e && e[0] == '0');
@@ -1100,7 +1105,7 @@ TilePlan pick_tiles(int M, int N, bool allow192) {
     const int rows = c.pair ? 256 : 128;
     const long long units = (long long)((M + rows - 1) / rows) * ((N + c.bn - 1) / c.bn);
     const int slots = c.pair ? sms / 2 : sms;
-    const double t = (double)((units + slots - 1) / slots) * 128.0 * c.bn / c.eff;
+    const double t = (double)((units + slots - 1) / slots) * kb * c.bn / c.eff + (c.pair ? F_PAIR : F_SINGLE);
     if (t < best - 1e-9) {
       best = t;
       plan = {c.pair, c.bn};
@@ -1137,7 +1142,7 @@ int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, l
       return !(e && e[0] == '0');
     }();
     const bool allow192 = allow192_env && kind != EPI_SWIGLU && !(kind == EPI_QKV && dh != 64);
-    const TilePlan tp = pick_tiles(M, N, allow192);
+    const TilePlan tp = pick_tiles(M, N, K, allow192);
     if (tp.pair && !(kind == EPI_SWIGLU && N % tp.bn != 0)) {
       if (tp.bn == 128) return dispatch_pair<128>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
       if (tp.bn == 192) return dispatch_pair<192>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
