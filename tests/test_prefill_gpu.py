@@ -272,3 +272,32 @@ def test_prepare_uses_one_prefill_per_combination(tmp_path):
         assert look.outcome is Outcome.DISK_HIT
         ref = gen.generate(q.doc_ids[:j], q.doc_tokens[:j])
         assert look.blob == ref
+
+
+def test_layer_stream_native_chain_matches_unpack():
+    """rdkv_kv_stream_layers (LayerStreamer): per-layer H2D from pinned host memory, the
+    unpack of each layer after its copy, one event per layer — the pool ends up exactly as
+    a whole-payload kv_unpack of the same bytes leaves it."""
+    from paper_2504_11765_b200.engine import LayerStreamer, pack_unpack_jobs
+
+    spec = get_spec("gqa-small-64")
+    eng = Engine(spec, seed=0, pool_tokens=4096)
+    pool = eng.pool
+    g = torch.Generator(device="cuda").manual_seed(1)
+    n = 200
+    payload = torch.randn(spec.layers * 2 * spec.kv_heads * n * spec.head_dim, generator=g, device="cuda").bfloat16()
+    host = payload.view(torch.uint8).cpu().pin_memory()
+    blocks_a, blocks_b = pool.alloc(n), pool.alloc(n)
+    bt = torch.tensor(blocks_a + blocks_b, dtype=torch.int32, device="cuda")
+    kv_unpack(pool, [(payload, n, 0)], bt)  # reference: the device payload, all layers at once
+    staging = torch.empty(host.numel(), dtype=torch.uint8, device="cuda")
+    jobs = [(staging, n, len(blocks_a))]
+    jobs_dev = pack_unpack_jobs(jobs).to("cuda")
+    st = LayerStreamer(eng)
+    main = torch.cuda.current_stream()
+    handles = st.launch(pool, jobs, bt, jobs_dev, main, h2d=[(host, staging)])
+    assert all(h for h in handles)
+    main.wait_event(st.events[-1])
+    torch.cuda.synchronize()
+    assert torch.equal(staging, payload.view(torch.uint8))
+    assert torch.equal(pool.gather(blocks_b, n), pool.gather(blocks_a, n))
