@@ -276,6 +276,9 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     LAUNCH(RDKV_PROF_QKV, 2.0 * T * (hq + 2 * hkv) * dh * d.hidden,
            launch_gemm(ws.h, d.hidden, W(m, wb + 1), d.hidden, T, (int)((hq + 2 * hkv) * dh), d.hidden, EPI_QKV, dh,
                          eq, st));
+    // document-KV generation (no logits): the last layer's KV is written by the QKV
+    // epilogue above; its attention, O projection and MLP feed nothing
+    if (!b->want_logits && l == d.layers - 1) break;
     AttnParams ap{};
     ap.q = ws.q;
     ap.ldq = qd;

@@ -342,6 +342,10 @@ class LayerStreamer:
         self.copy_layers = max(1, int(os.environ.get("RDKV_H2D_LAYERS", "2")))
         self.handles = (C.c_void_p * L)()
         self.copied_handles = (C.c_void_p * L)()
+        # pinned host payloads whose raw cudaMemcpyAsync copies may still be reading
+        # them: held until an event after the last copy has completed (the copies bypass
+        # torch's CachingHostAllocator, which would otherwise recycle the block early)
+        self._in_flight: deque = deque()
         # torch creates CUDA events lazily: record each once so the native call gets real handles
         cur = torch.cuda.current_stream(engine.device)
         for l in range(L):
@@ -388,9 +392,19 @@ class LayerStreamer:
             pool.data.data_ptr(), s.layers, s.kv_heads, s.head_dim, pool.slots, 2, h0, src_heads, n, hosts, devs,
             per, self.copy_layers, _stream_ptr(self.h2d), _stream_ptr(self.stream), self.copied_handles,
             self.handles))
+        if h2d:
+            self._hold([host for host, _ in h2d])
         if last_event is not None:
             last_event.record(self.stream)
         return self.handles
+
+
+    def _hold(self, hosts) -> None:
+        while self._in_flight and self._in_flight[0][0].query():
+            self._in_flight.popleft()
+        done = torch.cuda.Event()
+        done.record(self.h2d)
+        self._in_flight.append((done, hosts))
 
 
 def pack_unpack_jobs(jobs: Sequence[tuple[torch.Tensor, int, int]]) -> torch.Tensor:
@@ -566,11 +580,14 @@ class ResidentKvTier:
             return self.pool.alloc(n_tokens)
 
     def commit(self, key, blocks: list[int], n_tokens: int) -> None:
+        """Publish reserved ``blocks`` as ``key``'s entry.  If another writer got there
+        first, the existing entry wins (a batch may have it pinned and be reading
+        its blocks) and the new blocks go back to the pool."""
         with self._lock:
-            old = self._d.pop(key, None)
-            if old is not None:  # lost a race: keep the newer copy
-                self.used -= len(old.blocks)
-                self.pool.release(old.blocks)
+            if key in self._d:
+                self.used -= len(blocks)
+                self.pool.release(blocks)
+                return
             self._d[key] = ResidentEntry(list(blocks), n_tokens)
 
 

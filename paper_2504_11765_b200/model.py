@@ -149,6 +149,14 @@ class ModelWeights:
         ptrs += [self.final_norm.data_ptr(), self.lm_head.data_ptr()]
         return ptrs
 
+    def to(self, device) -> "ModelWeights":
+        """Copy on ``device`` (tied embeddings stay tied)."""
+        mv = lambda t: t.to(device)
+        out = ModelWeights(spec=self.spec, embed=mv(self.embed), final_norm=mv(self.final_norm))
+        out.lm_head = out.embed if self.lm_head is self.embed else mv(self.lm_head)
+        out.layers = [{k: mv(v) for k, v in lw.items()} for lw in self.layers]
+        return out
+
     # logical (unpacked) views for the oracle -----------------------------------
     def logical_layer(self, i: int) -> dict:
         s = self.spec

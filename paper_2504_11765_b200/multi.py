@@ -200,6 +200,7 @@ class TpGroup:
 
         lib = _L()
         self.engine = engine
+        self.group = group
         self.rank, self.size = dist.get_rank(group), dist.get_world_size(group)
         engine.tp_rank = self.rank  # its KV heads of full-model blobs: [rank * kv_heads, (rank + 1) * kv_heads)
         self.max_elems = max_tokens * engine.spec.hidden
@@ -259,6 +260,9 @@ class TpGroup:
         from .engine import _L
 
         s = self.engine.spec
+        group = self.group
+        # ``root`` is a rank of this TP group; collectives address it by its global rank
+        root_global = dist.get_global_rank(group, root) if group is not None else root
         part = s.layers * 2 * s.kv_heads * n_tokens * s.head_dim  # elements of one rank's share
         full = part * self.size
         if not hasattr(self, "_gather") or self._gather_elems < full:
@@ -272,7 +276,7 @@ class TpGroup:
                 off = C.c_int64()
                 _lib.check(_L().rdkv_ipc_handle(C.c_void_p(self._gather_buf.data_ptr()), h, C.byref(off)))
                 info = [(bytes(h), int(off.value))]
-            dist.broadcast_object_list(info, src=root)
+            dist.broadcast_object_list(info, src=root_global, group=group)
             self._gather_peer = None
             if self.rank == root:
                 self._gather = self._gather_buf.data_ptr()
@@ -282,13 +286,17 @@ class TpGroup:
                 self._gather_peer = base.value
                 self._gather = base.value + info[0][1]
             self._gather_elems = full
+        # the root may still be hashing / copying the previous payload out of the gather
+        # buffer: nobody writes into it before the root has arrived here
+        torch.cuda.current_stream(self.engine.device).synchronize()
+        dist.barrier(group=group)
         width = s.kv_heads * n_tokens * s.head_dim * 2          # bytes of this rank's heads per (layer, K|V)
         pitch = width * self.size                               # bytes of all heads per (layer, K|V)
         dst = self._gather + self.rank * width
         st = torch.cuda.current_stream(self.engine.device)
         _lib.check(_L().rdkv_memcpy_2d(dst, pitch, local.data_ptr(), width, width, s.layers * 2, st.cuda_stream))
         st.synchronize()
-        dist.barrier()
+        dist.barrier(group=group)
         return self._gather_buf[:full] if self.rank == root else None
 
     def generate_blob(self, tokens, doc_ids, root: int = 0):
