@@ -389,6 +389,64 @@ RDKV_API int rdkv_gemm_bf16_ex(const void* A, int64_t lda, const void* B, int64_
                                int epilogue, int tile_n, void* scratch, size_t scratch_bytes,
                                void* stream);
 
+/* ------------------------------------------------------------ node control plane (csrc/shm.cpp)
+ *
+ * One POSIX shared-memory segment per node, shared by the instances (one
+ * process per GPU).  Replaces, across processes, what the reference keeps in
+ * one Python process: the single-flight in-flight map of
+ * SharedCacheService.get_or_generate (service.py:87-127), the central FIFO
+ * every idle instance pulls from (sim.py:403-409) and the generator queue
+ * (sim.py:297-332), plus the HBM-residency directory (holder rank + pool blocks
+ * + pin count) that lets a peer pull a cached prefix over NVLink.
+ * All shared words are lock-free atomics.  Keys are (model_hash, file stem)
+ * (store.py:71-74). */
+typedef struct rdkv_shm rdkv_shm;
+
+#define RDKV_KEY_ABSENT 0     /* nobody asked for it                            */
+#define RDKV_KEY_REQUESTED 1  /* queued on its owner's generation ring          */
+#define RDKV_KEY_GENERATING 2 /* an owner is running generate() (single flight) */
+#define RDKV_KEY_READY 3      /* generated: in the store and/or an HBM tier     */
+#define RDKV_KEY_FAILED 4     /* generate() raised; waiters re-request          */
+
+/* create != 0: make (replacing a stale one) and zero the segment; else attach,
+ * waiting up to timeout_ms for the creator.  table_slots and ring_slots are
+ * powers of two; cell_bytes is the largest ring record. */
+RDKV_API int rdkv_shm_open(const char* name, int create, int world, int table_slots, int max_blocks,
+                           int ring_slots, int cell_bytes, int n_rings, int max_queries, int timeout_ms,
+                           rdkv_shm** out);
+RDKV_API void rdkv_shm_close(rdkv_shm* shm);
+RDKV_API int rdkv_shm_unlink(const char* name);
+RDKV_API int rdkv_shm_world(const rdkv_shm* shm);
+
+/* Single-flight state of a key (RDKV_KEY_*); *owner = the rank that moved it last. */
+RDKV_API int rdkv_shm_key_state(rdkv_shm* shm, uint64_t model_hash, uint64_t stem, int* owner);
+/* Atomic state transition expect -> desired (1 done, 0 state differed). */
+RDKV_API int rdkv_shm_key_cas(rdkv_shm* shm, uint64_t model_hash, uint64_t stem, int expect, int desired,
+                              int owner);
+
+/* HBM residency: the holder publishes its pool blocks for a key (1 published,
+ * 0 another rank holds it); a reader pins (returns the block count, 0 if not
+ * resident), copies over NVLink, unpins; the holder may evict only after
+ * retract succeeds (1 retracted or not held, 0 pinned by a reader). */
+RDKV_API int rdkv_shm_res_publish(rdkv_shm* shm, uint64_t model_hash, uint64_t stem, int rank,
+                                  const int32_t* blocks, int n_blocks, int n_tokens);
+RDKV_API int rdkv_shm_res_pin(rdkv_shm* shm, uint64_t model_hash, uint64_t stem, int* rank, int32_t* blocks,
+                              int cap, int* n_tokens);
+RDKV_API int rdkv_shm_res_unpin(rdkv_shm* shm, uint64_t model_hash, uint64_t stem);
+RDKV_API int rdkv_shm_res_retract(rdkv_shm* shm, uint64_t model_hash, uint64_t stem, int rank);
+RDKV_API int rdkv_shm_res_holder(rdkv_shm* shm, uint64_t model_hash, uint64_t stem);
+
+/* Bounded MPMC ring `ring`: push returns 1 (0 = full); pop returns the record
+ * length (0 = empty). */
+RDKV_API int rdkv_shm_ring_push(rdkv_shm* shm, int ring, const void* data, int len);
+RDKV_API int rdkv_shm_ring_pop(rdkv_shm* shm, int ring, void* out, int cap);
+RDKV_API int64_t rdkv_shm_ring_size(rdkv_shm* shm, int ring);
+
+/* Per-query state byte (queued / dispatched / done) and 64 shared counters. */
+RDKV_API int rdkv_shm_qstate_cas(rdkv_shm* shm, int query, int expect, int desired);
+RDKV_API int rdkv_shm_qstate(rdkv_shm* shm, int query);
+RDKV_API int64_t rdkv_shm_counter_add(rdkv_shm* shm, int index, int64_t delta);
+
 #ifdef __cplusplus
 }
 #endif

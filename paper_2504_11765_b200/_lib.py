@@ -79,6 +79,24 @@ SIGNATURES: dict[str, tuple] = {
     "rdkv_attention_scratch_bytes": (_sz, [_i32, _i32, _i32]),
     "rdkv_gemm_bf16_ex": (_i32, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _sz,
                                  _vp]),
+    # node control plane (csrc/shm.cpp)
+    "rdkv_shm_open": (_i32, [_cp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, C.POINTER(_vp)]),
+    "rdkv_shm_close": (None, [_vp]),
+    "rdkv_shm_unlink": (_i32, [_cp]),
+    "rdkv_shm_world": (_i32, [_vp]),
+    "rdkv_shm_key_state": (_i32, [_vp, _u64, _u64, C.POINTER(_i32)]),
+    "rdkv_shm_key_cas": (_i32, [_vp, _u64, _u64, _i32, _i32, _i32]),
+    "rdkv_shm_res_publish": (_i32, [_vp, _u64, _u64, _i32, C.POINTER(C.c_int32), _i32, _i32]),
+    "rdkv_shm_res_pin": (_i32, [_vp, _u64, _u64, C.POINTER(_i32), C.POINTER(C.c_int32), _i32, C.POINTER(_i32)]),
+    "rdkv_shm_res_unpin": (_i32, [_vp, _u64, _u64]),
+    "rdkv_shm_res_retract": (_i32, [_vp, _u64, _u64, _i32]),
+    "rdkv_shm_res_holder": (_i32, [_vp, _u64, _u64]),
+    "rdkv_shm_ring_push": (_i32, [_vp, _i32, _vp, _i32]),
+    "rdkv_shm_ring_pop": (_i32, [_vp, _i32, _vp, _i32]),
+    "rdkv_shm_ring_size": (_i64, [_vp, _i32]),
+    "rdkv_shm_qstate_cas": (_i32, [_vp, _i32, _i32, _i32]),
+    "rdkv_shm_qstate": (_i32, [_vp, _i32]),
+    "rdkv_shm_counter_add": (_i64, [_vp, _i32, _i64]),
 }
 
 _lock = threading.Lock()

@@ -135,6 +135,12 @@ class KvPool:
         # values (0 * NaN would poison P.V); later contents are always written KV.
         self.data = torch.zeros(numel, dtype=torch.bfloat16, device=device)
         self._free: deque[int] = deque(range(n_blocks))
+        # released blocks return to the free list only once the work enqueued before the
+        # release has finished: several streams (serving, generation, peer copies) share
+        # the pool, so stream order alone no longer protects a block's last readers
+        self._pending: deque = deque()          # (event, blocks)
+        self._lock = threading.Lock()
+        self.reader_stream: torch.cuda.Stream | None = None  # where readers run (default: caller's stream)
 
     def blocks_for(self, n_tokens: int) -> int:
         return (n_tokens + self.block_size - 1) // self.block_size
@@ -142,17 +148,35 @@ class KvPool:
     def alloc(self, n_tokens: int) -> list[int]:
         return self.alloc_blocks(self.blocks_for(n_tokens))
 
+    def _reclaim(self, need: int) -> None:
+        while self._pending and (len(self._free) < need or self._pending[0][0].query()):
+            ev, blocks = self._pending.popleft()
+            ev.synchronize()
+            self._free.extend(blocks)
+
     def alloc_blocks(self, n: int) -> list[int]:
-        if n > len(self._free):
-            raise MemoryError(f"KV pool exhausted: need {n} blocks, {len(self._free)} free")
-        return [self._free.popleft() for _ in range(n)]
+        with self._lock:
+            self._reclaim(n)
+            if n > len(self._free):
+                raise MemoryError(f"KV pool exhausted: need {n} blocks, {len(self._free)} free")
+            return [self._free.popleft() for _ in range(n)]
 
     def release(self, blocks: Sequence[int]) -> None:
-        self._free.extend(blocks)
+        if not len(blocks):
+            return
+        if self.data.is_cuda:
+            ev = torch.cuda.Event()
+            ev.record(self.reader_stream or torch.cuda.current_stream(self.data.device))
+            with self._lock:
+                self._pending.append((ev, list(blocks)))
+        else:
+            with self._lock:
+                self._free.extend(blocks)
 
     @property
     def free_blocks(self) -> int:
-        return len(self._free)
+        with self._lock:
+            return len(self._free) + sum(len(b) for _, b in self._pending)
 
     def gather(self, blocks: Sequence[int], n_tokens: int) -> torch.Tensor:
         """[L][2][Hkv][n_tokens][dh] copy of a sequence's KV (tests/debug)."""
@@ -260,7 +284,7 @@ class DeviceModel:
         with torch.cuda.device(self.device):
             _lib.check(_L().rdkv_model_create(C.byref(desc), arr, len(ptrs), C.byref(h)))
         self._h = h
-        self._ws: torch.Tensor | None = None
+        self._ws: dict | None = None
 
     def close(self) -> None:
         if self._h:
@@ -273,11 +297,19 @@ class DeviceModel:
         except Exception:
             pass
 
-    def workspace(self, n_tokens: int, n_seqs: int) -> torch.Tensor:
+    def workspace(self, n_tokens: int, n_seqs: int, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """Scratch for one forward; one buffer per stream, so forwards on different
+        streams (serving and queue-time generation) never share scratch."""
         need = int(_L().rdkv_workspace_bytes(self._h, n_tokens, n_seqs))
-        if self._ws is None or self._ws.numel() < need:
-            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
-        return self._ws
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if self._ws is None:
+            self._ws = {}
+        ws = self._ws.get(st.cuda_stream)
+        if ws is None or ws.numel() < need:
+            with torch.cuda.stream(st):
+                ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            self._ws[st.cuda_stream] = ws
+        return ws
 
     def profile(self, on: bool) -> None:
         _lib.check(_L().rdkv_profile_enable(self._h, 1 if on else 0))
@@ -291,7 +323,7 @@ class DeviceModel:
 
     def forward(self, plan: BatchPlan, kv_base: int, kv_slots: int, logits=None, next_token=None,
                 stream: torch.cuda.Stream | None = None, layer_ready=None) -> None:
-        ws = self.workspace(plan.n_tokens, plan.n_seqs)
+        ws = self.workspace(plan.n_tokens, plan.n_seqs, stream)
         b = plan.struct(kv_base, kv_slots, logits, next_token, layer_ready)
         _lib.check(_L().rdkv_forward(self._h, C.byref(b), ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
 
@@ -510,6 +542,7 @@ class ResidentEntry:
     blocks: list[int]       # pool blocks holding positions [0, n_tokens)
     n_tokens: int
     pins: int = 0           # batches currently reading the blocks
+    ready: object = None    # CUDA event after which the blocks hold the KV (None: already complete)
 
 
 class ResidentKvTier:
@@ -520,18 +553,31 @@ class ResidentKvTier:
     block is copied on write).  Entries are filled once, by one K3 unpack of
     the blob payload, when a composite is generated or first streamed in.
 
-    Purely a *placement* layer under the store: the logical outcome of every
-    access (MEMORY_HIT / DISK_HIT / MISS and its accounting) is still decided
-    by the KvStore; this only changes where the bytes come from (SURVEY §8e
-    invariant).  Eviction returns blocks to the pool free list, which is
-    stream-ordered: later writers are enqueued after earlier readers."""
+    Prefixes share blocks: the KV of prefix ``doc_ids[:j]`` is exactly the
+    first rows of its combination's KV (causal attention, row-deterministic
+    kernels — SURVEY H-e), so :meth:`alias` makes all k prefix keys of a
+    resident combination resident at the cost of the combination alone.
+    Blocks are reference-counted; an entry's eviction frees only blocks no
+    other entry shares.
+
+    Purely a *placement* layer: what the store holds and how it accounts an
+    access is unchanged; this only changes where the bytes come from (SURVEY
+    §8e invariant).  ``can_evict(key)`` (the control plane's retract) vetoes
+    evicting an entry a peer is still copying over NVLink."""
 
     def __init__(self, pool: "KvPool", capacity_blocks: int) -> None:
         self.pool = pool
         self.capacity = capacity_blocks
-        self.used = 0
         self._d: "OrderedDict[object, ResidentEntry]" = OrderedDict()
+        self._ref: dict[int, int] = {}
+        self._reserved = 0
         self._lock = threading.Lock()
+        self.can_evict = None
+        self.evictions = 0
+
+    @property
+    def used(self) -> int:
+        return len(self._ref) + self._reserved
 
     def __contains__(self, key) -> bool:
         with self._lock:
@@ -543,6 +589,10 @@ class ResidentKvTier:
     def items(self) -> list:
         with self._lock:
             return list(self._d.items())
+
+    def get(self, key) -> ResidentEntry | None:
+        with self._lock:
+            return self._d.get(key)
 
     def acquire(self, key) -> ResidentEntry | None:
         """Pin and return the entry (MRU), or None."""
@@ -559,9 +609,23 @@ class ResidentKvTier:
             if e is not None and e.pins > 0:
                 e.pins -= 1
 
+    def _drop(self, key) -> list[int]:
+        e = self._d.pop(key)
+        freed = []
+        for b in e.blocks:
+            r = self._ref[b] - 1
+            if r:
+                self._ref[b] = r
+            else:
+                del self._ref[b]
+                freed.append(b)
+        self.evictions += 1
+        return freed
+
     def reserve(self, n_tokens: int) -> list[int] | None:
         """Blocks for a new entry, evicting unpinned LRU entries; None if it cannot fit."""
         need = self.pool.blocks_for(n_tokens)
+        freed: list[int] = []
         with self._lock:
             if need > self.capacity:
                 return None
@@ -569,26 +633,68 @@ class ResidentKvTier:
                 if self.used + need <= self.capacity:
                     break
                 e = self._d[k]
-                if e.pins:
+                if e.pins or (self.can_evict is not None and not self.can_evict(k)):
                     continue
-                del self._d[k]
-                self.used -= len(e.blocks)
-                self.pool.release(e.blocks)
-            if self.used + need > self.capacity or need > self.pool.free_blocks:
-                return None
-            self.used += need
-            return self.pool.alloc(n_tokens)
+                freed += self._drop(k)
+            ok = self.used + need <= self.capacity
+            if ok:
+                self._reserved += need
+        self.pool.release(freed)
+        if not ok:
+            return None
+        try:
+            return self.pool.alloc_blocks(need)
+        except MemoryError:
+            with self._lock:
+                self._reserved -= need
+            return None
 
-    def commit(self, key, blocks: list[int], n_tokens: int) -> None:
+    def unreserve(self, blocks: list[int]) -> None:
+        with self._lock:
+            self._reserved -= len(blocks)
+        self.pool.release(blocks)
+
+    def commit(self, key, blocks: list[int], n_tokens: int, ready=None) -> bool:
         """Publish reserved ``blocks`` as ``key``'s entry.  If another writer got there
         first, the existing entry wins (a batch may have it pinned and be reading
-        its blocks) and the new blocks go back to the pool."""
+        its blocks) and the new blocks go back to the pool.  False in that case."""
+        with self._lock:
+            self._reserved -= len(blocks)
+            if key in self._d:
+                lost = True
+            else:
+                lost = False
+                for b in blocks:
+                    self._ref[b] = self._ref.get(b, 0) + 1
+                self._d[key] = ResidentEntry(list(blocks), n_tokens, ready=ready)
+        if lost:
+            self.pool.release(blocks)
+        return not lost
+
+    def alias(self, key, base_key, n_tokens: int) -> bool:
+        """Make ``key`` resident as the first ``n_tokens`` positions of ``base_key``'s
+        entry (its leading blocks, shared).  False if the base is not resident."""
         with self._lock:
             if key in self._d:
-                self.used -= len(blocks)
-                self.pool.release(blocks)
-                return
-            self._d[key] = ResidentEntry(list(blocks), n_tokens)
+                return True
+            base = self._d.get(base_key)
+            if base is None or n_tokens > base.n_tokens:
+                return False
+            blocks = base.blocks[: self.pool.blocks_for(n_tokens)]
+            for b in blocks:
+                self._ref[b] += 1
+            self._d[key] = ResidentEntry(list(blocks), n_tokens, ready=base.ready)
+            return True
+
+    def evict(self, key) -> bool:
+        """Drop ``key`` (if unpinned); its unshared blocks return to the pool."""
+        with self._lock:
+            e = self._d.get(key)
+            if e is None or e.pins:
+                return False
+            freed = self._drop(key)
+        self.pool.release(freed)
+        return True
 
 
 class Engine:
@@ -599,6 +705,8 @@ class Engine:
         """``pool_tokens`` = working KV slots for in-flight queries; ``device_cache_bytes``
         = extra pool capacity reserved for the HBM-resident tier of cached prefixes."""
         self.device = torch.device(device)
+        if self.device.type == "cuda" and self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         self.spec = spec
         self.weights = weights if weights is not None else init_weights(spec, seed, self.device)
         self.model = DeviceModel(self.weights)
@@ -628,12 +736,15 @@ class Engine:
         blocks = self.resident.reserve(n_tokens)
         if blocks is None:
             return False
-        bt = torch.tensor(blocks, dtype=torch.int32).pin_memory().to(self.device, non_blocking=True)
-        kv_unpack(self.pool, [(payload, n_tokens, 0)], bt, stream=stream)
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(s):
+            bt = torch.tensor(blocks, dtype=torch.int32).pin_memory().to(self.device, non_blocking=True)
+        kv_unpack(self.pool, [(payload, n_tokens, 0)], bt, stream=s)
         payload.record_stream(s)
         bt.record_stream(s)
-        self.resident.commit(key, blocks, n_tokens)
+        ready = torch.cuda.Event()
+        ready.record(s)
+        self.resident.commit(key, blocks, n_tokens, ready=ready)
         return True
 
     def copy_block(self, src_block: int, dst_block: int, n_tokens: int,

@@ -33,6 +33,7 @@ class KvGenerator:
         self.profile = engine.spec.profile()
         self.token_seed = token_seed
         self.keep_on_device = keep_on_device
+        self.copy_stream = engine.copy_stream  # D2H into the host tier (the runtime gives generation its own)
 
     def tokens(self, doc_ids: Sequence[int], doc_token_counts: Sequence[int]) -> np.ndarray:
         return combo_tokens(doc_ids, doc_token_counts, self.engine.spec.vocab, self.token_seed)
@@ -54,13 +55,14 @@ class KvGenerator:
         eng = self.engine
         raw = kv.view(torch.uint8)
         main = torch.cuda.current_stream(eng.device)
-        eng.copy_stream.wait_stream(main)
+        cs = self.copy_stream
+        cs.wait_stream(main)
         host = torch.empty(raw.numel(), dtype=torch.uint8, pin_memory=True)
-        with torch.cuda.stream(eng.copy_stream):
+        with torch.cuda.stream(cs):
             host.copy_(raw, non_blocking=True)
-        raw.record_stream(eng.copy_stream)
+        raw.record_stream(cs)
         checksum = fnv1a64_device(raw)
-        eng.copy_stream.synchronize()
+        cs.synchronize()
         if self.keep_on_device:
             eng.make_resident(KvKey(self.profile.model_hash, ids), kv, n)
         return KvBlob.trusted(make_header(self.profile, ids, n, checksum), host)

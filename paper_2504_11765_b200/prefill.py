@@ -65,14 +65,20 @@ def prefill_batch(engine: Engine, requests: Sequence[PrefillRequest], timed: boo
     try:
         for i, r in enumerate(requests):
             hit = r.lookup.outcome is not Outcome.MISS
-            n_cached = int(r.lookup.blob.header.token_count) if hit else 0
             new = np.asarray(r.new_tokens, np.int32) if hit else np.concatenate(
                 [np.asarray(r.prefix_tokens, np.int32), np.asarray(r.new_tokens, np.int32)])
             entry = engine.resident.acquire(r.key) if hit and r.key is not None else None
             if entry is not None:
+                pinned.append(r.key)
+            if hit and r.lookup.blob is None and entry is None:
+                raise ValueError(f"request {i}: an HBM-tier hit needs the prefix resident in the pool")
+            n_cached = (entry.n_tokens if r.lookup.blob is None else int(r.lookup.blob.header.token_count)) \
+                if hit else 0
+            if entry is not None:
                 # HBM-tier hit: the prefix is already in pool blocks; only the new
                 # tokens get fresh blocks (a partial last block is copied on write)
-                pinned.append(r.key)
+                if entry.ready is not None:  # filled on another stream (queue-time generation, peer fetch)
+                    main.wait_event(entry.ready)
                 if entry.n_tokens != n_cached:
                     raise ValueError("resident entry does not match the lookup's token count")
                 prefix = list(entry.blocks)
