@@ -686,6 +686,11 @@ class ResidentKvTier:
             self._d[key] = ResidentEntry(list(blocks), n_tokens, ready=base.ready)
             return True
 
+    def clear(self) -> int:
+        """Evict every unpinned entry; returns how many were dropped."""
+        keys = [k for k, _ in self.items()]
+        return sum(self.evict(k) for k in keys)
+
     def evict(self, key) -> bool:
         """Drop ``key`` (if unpinned); its unshared blocks return to the pool."""
         with self._lock:

@@ -461,10 +461,13 @@ class Driver:
             self.cp.add(Counter.GENERATION_REQUESTS)
             self.requests += 1
 
-    def run(self, arrivals: Sequence[tuple[float, object]], index0: int, t0: float) -> None:
+    def run(self, arrivals: Sequence[tuple[float, object]], index0: int, t0: float,
+            deadline_s: float = 900.0) -> None:
         """Push ``arrivals`` ((offset seconds, WorkItem), sorted) at t0 + offset;
-        flag waiting queries at the threshold; return when all are served."""
+        flag waiting queries at the threshold; return when all are served
+        (raise if that takes longer than ``deadline_s``)."""
         cfg = self.cfg
+        deadline = t0 + deadline_s
         pending: list[PendingQuery] = []
         n, i = len(arrivals), 0
         while True:
@@ -489,6 +492,9 @@ class Driver:
                 return
             if self.cp.counter(STOP):
                 raise RuntimeError("an instance stopped the node (worker error)")
+            if now > deadline:
+                raise TimeoutError(f"{sum(self.cp.qstate(index0 + j) is not QState.DONE for j in range(n))} of "
+                                   f"{n} queries unserved after {deadline_s:.0f} s")
             nxt = [t0 + arrivals[i][0]] if i < n else []
             nxt += [p.arrival_time + cfg.threshold for p in pending if not p.flagged]
             wait = (min(nxt) - time.monotonic()) if nxt else cfg.idle_sleep_s
