@@ -72,3 +72,34 @@ class StoreModel:
             _, s = self.lru.pop(0)
             self.stats["memory_bytes_used"] -= s
             self.stats["evictions"] += 1
+
+    # Two-phase disk hit, for replaying logs of concurrent runs (SURVEY H-i): the
+    # reference decides a disk hit under its lock, reads the file outside it and
+    # promotes under the lock again (store.py:250-280), so other operations can
+    # interleave between the two halves.
+    def read_decision(self, key) -> str:
+        """First half of a disk hit: the outcome as decided before the read."""
+        if self._resident(key):
+            return "memory_hit"
+        return "disk_hit" if key in self.disk else "miss"
+
+    def promote(self, key, size) -> None:
+        """Second half: count the disk hit and insert into the memory tier."""
+        self.stats["disk_hits"] += 1
+        self._touch(key, size)
+
+
+def replay_oplog(oplog, capacity: int) -> dict:
+    """Replay a ``KvStore.oplog`` (a real, possibly concurrent run) through the
+    store law; asserts every recorded outcome and returns the final stats."""
+    m = StoreModel(capacity)
+    for op in oplog:
+        if op[0] == "put":
+            assert m.put(op[1], op[2], op[3]) == op[4], op
+        elif op[0] == "read":                      # a disk hit decided; the file is read outside the lock
+            assert m.read_decision(op[1]) == "disk_hit", op
+        elif op[2] == "disk_hit":                  # ... and promoted once read
+            m.promote(op[1], op[3])
+        else:
+            assert m.get(op[1]) == (op[2], op[3]), op
+    return m.stats

@@ -9,6 +9,7 @@
 // RMSNorm, the LM head (fp32 logits) and argmax = the first token.
 #include <cmath>
 #include <cstdlib>
+#include <mutex>
 #include <new>
 #include <algorithm>
 #include <vector>
@@ -35,6 +36,9 @@ struct rdkv_model {
   std::vector<cudaEvent_t> spare;
   int64_t launches[RDKV_PROF_N] = {};
   double flops[RDKV_PROF_N] = {};
+  // forwards may run concurrently on several streams (serving and queue-time
+  // generation share the handle): counters and event records are guarded
+  std::mutex mu;
 
   cudaEvent_t event() {
     if (!spare.empty()) {
@@ -56,6 +60,7 @@ struct ProfScope {
   cudaStream_t st;
   cudaEvent_t a = nullptr;
   ProfScope(rdkv_model* m_, int cat_, cudaStream_t st_, double fl = 0.0) : m(m_), cat(cat_), st(st_) {
+    std::lock_guard<std::mutex> g(m->mu);
     m->launches[cat] += 1;
     m->flops[cat] += fl;
     if (m->prof) {
@@ -65,6 +70,7 @@ struct ProfScope {
   }
   ~ProfScope() {
     if (m->prof) {
+      std::lock_guard<std::mutex> g(m->mu);
       cudaEvent_t b = m->event();
       cudaEventRecord(b, st);
       m->recs.push_back({cat, a, b});
@@ -316,7 +322,9 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     }
     if (b->layer_ready && b->layer_ready[l])  // layer-wise streaming: this layer's cached KV has landed
       CUDA_TRY(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(b->layer_ready[l]), 0));
-    if (use_tc_attn && attention_tc_supported(ap, dh))
+    // the tcgen05 kernel is the product path: an unsupported shape is an error, not a
+    // silent fallback; the legacy mma.sync kernel runs only when asked for (RDKV_ATTN=mma, A/B)
+    if (use_tc_attn)
       LAUNCH(RDKV_PROF_ATTN, 0.0, launch_attention_tc(ap, dh, S, b->max_new, st));
     else
       LAUNCH(RDKV_PROF_ATTN, 0.0, launch_attention(ap, dh, S, b->max_new, st));
@@ -391,6 +399,7 @@ int rdkv_profile_enable(rdkv_model* m, int on) {
 int rdkv_profile_collect(rdkv_model* m, double* ms, int64_t* launches, double* flops) {
   if (!m) return set_error(RDKV_ERR_ARG, "profile_collect: null model");
   double acc[RDKV_PROF_N] = {};
+  std::lock_guard<std::mutex> g(m->mu);
   for (auto& r : m->recs) {
     CUDA_TRY(cudaEventSynchronize(r.b));
     float t = 0.f;

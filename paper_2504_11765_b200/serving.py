@@ -186,7 +186,12 @@ def summarize(records, access_log=None) -> dict:
     """TTFT percentiles (both definitions) and throughput of a run."""
     lat = np.array([r.first_token - r.arrival for r in records])
     ttft = np.array([r.kv_load + r.prefill + r.network_delay for r in records])
-    span = max(r.first_token for r in records) - min(r.arrival for r in records)
+    # throughput over the SUM of per-try makespans (reference build_report, sim.py:226-240):
+    # the tries run back to back on the same clock origin, so one span would double-count
+    tries: dict[int, list] = {}
+    for r in records:
+        tries.setdefault(getattr(r, "try_index", 1), []).append(r)
+    span = sum(max(r.first_token for r in g) - min(r.arrival for r in g) for g in tries.values())
     origins: dict[str, int] = {}
     for r in records:
         for o in r.origins:

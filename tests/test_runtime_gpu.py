@@ -139,3 +139,38 @@ def test_two_instances_share_one_gpu_peer_fetch():
     assert sum(counters["generated_by_rank"]) == counters["keys_generated"] > 0
     assert all(g > 0 for g in counters["generated_by_rank"])    # owner-partitioned: both ranks generated
     assert counters["peer_fetches"] > 0 and sources.get("peer", 0) > 0   # NVLink (IPC) pulls from the peer's HBM
+
+
+def test_runtime_store_path_oplog_replays():
+    """HBM tier off: generated prefixes live only in the shared store (memory tier
+    + disk); try 2 is served through KvStore.get.  The real store's operation log
+    of the concurrent run (serve thread gets, writer puts) replays into the store
+    law with identical outcomes and stats (SURVEY H-i)."""
+    from dataclasses import asdict
+
+    from oracle.store_ref import replay_oplog
+    from paper_2504_11765_b200.engine import Engine
+    from paper_2504_11765_b200.model import get_spec
+    from paper_2504_11765_b200.runtime import RuntimeConfig, serve
+    from paper_2504_11765_b200.store import KvStore
+
+    spec = get_spec("gqa-small-64")
+    k = 3
+    eng = Engine(spec, seed=0, pool_tokens=32768, device_cache_bytes=0)
+    items = _items(k=k)
+    expected = _expected_tokens(eng, items, k)
+    cap = 3 << 20  # a few composites: the memory tier evicts
+    with tempfile.TemporaryDirectory() as root:
+        store = KvStore(root, memory_capacity_bytes=cap)
+        store.oplog = []
+        out = serve(eng, store, RuntimeConfig(k=k, threshold=0.0, max_batch=4, persist="all"), items,
+                    rate=400.0, tries=2)
+        rep = out["summary"]
+        assert rep["each_key_generated_once"] and rep["queries"] == 2 * len(items)
+        assert {"memory", "disk"} & set(rep["sources"])            # served through the store tiers
+        _check_tokens(out["results"], expected)
+        want = replay_oplog(store.oplog, cap)
+        got = asdict(store.stats())
+        assert all(got[f] == v for f, v in want.items()), (got, want)
+        gets = [op for op in store.oplog if op[0] == "get"]
+        assert len(gets) >= len(out["access_log"]) > 0
