@@ -288,7 +288,14 @@ typedef struct rdkv_model_desc {
   int32_t max_pos;
   float rope_theta;
   float norm_eps;
+  int32_t flags; /* RDKV_MODEL_* */
 } rdkv_model_desc;
+
+/* The attention / MLP RMSNorm gains are folded into the columns of w_qkv / w_gate_up
+ * (W'[n][k] = W[n][k] * gain[k]); the gain vectors are then ignored.  Lets large
+ * batches fuse the norms across GEMMs: the residual epilogues emit per-row sums of
+ * squares and the consuming QKV / gate-up epilogues apply rsqrt(mean + eps). */
+#define RDKV_MODEL_NORM_FOLDED 1
 
 /* Weight pointers (device, 16-B aligned), in this order:
  *   [0]                 embedding       bf16 [vocab][hidden]

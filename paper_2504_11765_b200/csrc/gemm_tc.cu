@@ -85,9 +85,34 @@ __device__ __forceinline__ void qkv_head_out(float (&v)[DH], int g, int row, int
 
 // One accumulator tile -> fused epilogue -> global.  `row` is this thread's output row
 // (its TMEM lane), `taddr` the tile's TMEM address for this warp's lane quadrant.
+// Per-row RMSNorm scale from the producer's per-chunk sums of squares (fixed
+// summation order: row-deterministic).
+__device__ __forceinline__ float row_rscale(const GemmEpi& ep, int row, int M) {
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  const float* p = ep.ssq_in + row;
+  int c = 0;
+  for (; c + 4 <= ep.ssq_parts; c += 4) {
+    s0 += p[(long long)c * M];
+    s1 += p[(long long)(c + 1) * M];
+    s2 += p[(long long)(c + 2) * M];
+    s3 += p[(long long)(c + 3) * M];
+  }
+  for (; c < ep.ssq_parts; ++c) s0 += p[(long long)c * M];
+  return rsqrtf(((s0 + s1) + (s2 + s3)) / (float)ep.ssq_dim + ep.norm_eps);
+}
+
+template <int EPI>
+__device__ __forceinline__ float epi_rscale(const GemmEpi& ep, int row, int M) {
+  if constexpr (EPI == EPI_QKV || EPI == EPI_SWIGLU)
+    return ep.ssq_in && row < M ? row_rscale(ep, row, M) : 1.f;
+  return 1.f;
+}
+
 template <int BN, int EPI, int DH>
 __device__ __forceinline__ void epilogue_rows(uint32_t taddr, int row, int nb, int sp, int M, int N,
-                                              const GemmEpi& ep, int half) {
+                                              const GemmEpi& ep, int half, float rs) {
+  // rs: the fused RMSNorm scale of this A row (QKV / SWIGLU consumers; 1 otherwise),
+  // computed by the caller while the tile's MMAs were still running
   const bool row_ok = row < M;
 
   if constexpr (EPI == EPI_STORE || EPI == EPI_STORE_F32 || EPI == EPI_RESID || EPI == EPI_PARTIAL || EPI == EPI_PUSH) {
@@ -130,6 +155,18 @@ __device__ __forceinline__ void epilogue_rows(uint32_t taddr, int row, int nb, i
           } else {
             st_bf16x32(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + col, w);
           }
+          if constexpr (EPI == EPI_RESID) {
+            if (ep.ssq_out) {  // the next RMSNorm's statistics, from the values just stored
+              float ss = 0.f;
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const float2 f = unpack_bf16(w[i]);
+                ss = fmaf(f.x, f.x, ss);
+                ss = fmaf(f.y, f.y, ss);
+              }
+              ep.ssq_out[(long long)(col >> 5) * M + row] = ss;
+            }
+          }
         }
       }
     }
@@ -147,8 +184,8 @@ __device__ __forceinline__ void epilogue_rows(uint32_t taddr, int row, int nb, i
         uint32_t w[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float a0 = silu(__uint_as_float(g[2 * i])) * __uint_as_float(v[2 * i]);
-          const float a1 = silu(__uint_as_float(g[2 * i + 1])) * __uint_as_float(v[2 * i + 1]);
+          const float a0 = silu(rs * __uint_as_float(g[2 * i])) * (rs * __uint_as_float(v[2 * i]));
+          const float a1 = silu(rs * __uint_as_float(g[2 * i + 1])) * (rs * __uint_as_float(v[2 * i + 1]));
           w[i] = pack_bf16(a0, a1);
         }
         st_bf16x32(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + col, w);
@@ -185,16 +222,16 @@ __device__ __forceinline__ void epilogue_rows(uint32_t taddr, int row, int nb, i
       if (g < ep.hq + ep.hkv) {
 #pragma unroll
         for (int i = 0; i < 16; i += 2) {
-          const float a0 = __uint_as_float(ra[i]), a1 = __uint_as_float(ra[i + 1]);
-          const float b0 = __uint_as_float(rb[i]), b1 = __uint_as_float(rb[i + 1]);
+          const float a0 = rs * __uint_as_float(ra[i]), a1 = rs * __uint_as_float(ra[i + 1]);
+          const float b0 = rs * __uint_as_float(rb[i]), b1 = rs * __uint_as_float(rb[i + 1]);
           wa[i / 2] = pack_bf16(a0 * cs[i].x - b0 * cs[i].y, a1 * cs[i + 1].x - b1 * cs[i + 1].y);
           wb[i / 2] = pack_bf16(b0 * cs[i].x + a0 * cs[i].y, b1 * cs[i + 1].x + a1 * cs[i + 1].y);
         }
       } else {
 #pragma unroll
         for (int i = 0; i < 16; i += 2) {
-          wa[i / 2] = pack_bf16(__uint_as_float(ra[i]), __uint_as_float(ra[i + 1]));
-          wb[i / 2] = pack_bf16(__uint_as_float(rb[i]), __uint_as_float(rb[i + 1]));
+          wa[i / 2] = pack_bf16(rs * __uint_as_float(ra[i]), rs * __uint_as_float(ra[i + 1]));
+          wb[i / 2] = pack_bf16(rs * __uint_as_float(rb[i]), rs * __uint_as_float(rb[i + 1]));
         }
       }
       __nv_bfloat16* dst;
@@ -221,7 +258,7 @@ __device__ __forceinline__ void epilogue_rows(uint32_t taddr, int row, int nb, i
         tmem_ld32(taddr + hh * DH + c * 32, r);
         tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[c * 32 + i] = __uint_as_float(r[i]);
+        for (int i = 0; i < 32; ++i) v[c * 32 + i] = rs * __uint_as_float(r[i]);
       }
       const int g = (nb * BN + hh * DH) / DH;  // global head index in [q | k | v]
       if (!row_ok || g >= ep.hq + 2 * ep.hkv) continue;
@@ -347,11 +384,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       int mb, nb, kb0, kb1, sp;
       decode(u, mb, nb, kb0, kb1, sp);
+      const int row = mb * BM + wq * 32 + lane;
+      const float rs = epi_rscale<EPI>(ep, row, M);  // overlaps this tile's MMAs
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = mb * BM + wq * 32 + lane;
       const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(wq * 32) << 16);
-      epilogue_rows<BN, EPI, DH>(taddr, row, nb, sp, M, N, ep, (warp - 4) >> 2);
+      epilogue_rows<BN, EPI, DH>(taddr, row, nb, sp, M, N, ep, (warp - 4) >> 2, rs);
       if constexpr (EPI == EPI_PUSH) __threadfence_system();
       tc_fence_before();
       __syncwarp();
@@ -504,11 +542,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 0), tempty1 = mapa_shared(smem_u32(&tempty[1]), 0);
     for (int u = pair; u < units; u += npairs) {
       const int mb = u % m_tiles, nb = u / m_tiles;
+      const int row = mb * 256 + (int)rank * 128 + wq * 32 + lane;
+      const float rs = epi_rscale<EPI>(ep, row, M);  // overlaps this tile's MMAs
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = mb * 256 + (int)rank * 128 + wq * 32 + lane;
       const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(wq * 32) << 16);
-      epilogue_rows<BN, EPI, DH>(taddr, row, nb, 0, M, N, ep, (warp - 4) >> 2);
+      epilogue_rows<BN, EPI, DH>(taddr, row, nb, 0, M, N, ep, (warp - 4) >> 2, rs);
       if constexpr (EPI == EPI_PUSH) __threadfence_system();
       tc_fence_before();
       __syncwarp();

@@ -52,6 +52,15 @@ struct GemmEpi {
   // CUDA-IPC mappings, so the stores cross NVLink while later tiles still compute
   __nv_bfloat16* push[8];
   int npush;
+  // RMSNorm fused across GEMMs (RDKV_MODEL_NORM_FOLDED: the norm gains are folded into
+  // the consuming weights).  RESID writes, per output row and 32-column chunk, the
+  // sum of squares of its bf16 outputs to ssq_out[chunk][M]; QKV / SWIGLU read the
+  // ssq_parts partials of their A rows in a fixed order and scale the accumulators
+  // by rsqrt(sum / ssq_dim + norm_eps) before RoPE / SiLU.  Null = off.
+  float* ssq_out;
+  const float* ssq_in;
+  int ssq_parts;
+  int ssq_dim;
 };
 
 // True when launch_gemm will take the split-K path for this shape (small M).

@@ -79,8 +79,10 @@ __global__ void __launch_bounds__(256) kv_unpack_kernel(const UnpackJob* __restr
 }
 
 // ---------------------------------------------------------------- embed
+// With ssq != null also the first RMSNorm's statistics: per row and 32-column chunk
+// the sum of squares, ssq[chunk][n] (the layout GEMM residual epilogues write).
 __global__ void embed_kernel(const int* __restrict__ tok, const __nv_bfloat16* __restrict__ table,
-                             __nv_bfloat16* __restrict__ out, int d, int vocab) {
+                             __nv_bfloat16* __restrict__ out, int d, int vocab, float* __restrict__ ssq, int n) {
   pdl_trigger();
   pdl_wait();
   const int t = blockIdx.x;
@@ -88,7 +90,23 @@ __global__ void embed_kernel(const int* __restrict__ tok, const __nv_bfloat16* _
   id = id < 0 ? 0 : (id >= vocab ? vocab - 1 : id);
   const uint4* src = reinterpret_cast<const uint4*>(table + (long long)id * d);
   uint4* dst = reinterpret_cast<uint4*>(out + (long long)t * d);
-  for (int i = threadIdx.x; i < d / 8; i += blockDim.x) dst[i] = src[i];
+  for (int i = threadIdx.x; i < d / 8; i += blockDim.x) {  // blockDim is a multiple of 4: chunks stay in-warp
+    const uint4 v = src[i];
+    dst[i] = v;
+    if (ssq) {
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+      float ss = 0.f;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = unpack_bf16_f(w[j]);
+        ss = fmaf(f.x, f.x, ss);
+        ss = fmaf(f.y, f.y, ss);
+      }
+      ss += __shfl_xor_sync(0xffffffff, ss, 1);
+      ss += __shfl_xor_sync(0xffffffff, ss, 2);
+      if ((i & 3) == 0) ssq[(long long)(i >> 2) * n + t] = ss;
+    }
+  }
 }
 
 // ---------------------------------------------------------------- rmsnorm
@@ -227,9 +245,10 @@ int launch_kv_unpack(const UnpackJob* jobs_dev, int n_jobs, int max_tokens, cons
 }
 
 int launch_embed(const int* tok, const __nv_bfloat16* table, __nv_bfloat16* out, int n, int d, int vocab,
-                 cudaStream_t st) {
+                 cudaStream_t st, float* ssq) {
   if (n <= 0) return 0;
-  CUDA_TRY(launch_k(embed_kernel, dim3(n), dim3(128), 0, st, tok, table, out, d, vocab));
+  if (ssq && d % 256 != 0) return set_error(RDKV_ERR_ARG, "embed: fused norm statistics need d %% 256 == 0");
+  CUDA_TRY(launch_k(embed_kernel, dim3(n), dim3(128), 0, st, tok, table, out, d, vocab, ssq, n));
   CUDA_TRY(cudaGetLastError());
   return 0;
 }

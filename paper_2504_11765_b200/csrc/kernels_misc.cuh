@@ -20,7 +20,7 @@ int launch_kv_unpack(const UnpackJob* jobs_dev, int n_jobs, int max_tokens, cons
                      void* pool, int layer_begin, int layer_end, int hkv, int dh, long long slots, int elem_width,
                      cudaStream_t st, int head_begin = 0, int src_kv_heads = 0);
 int launch_embed(const int* tok, const __nv_bfloat16* table, __nv_bfloat16* out, int n, int d, int vocab,
-                 cudaStream_t st);
+                 cudaStream_t st, float* ssq = nullptr);
 int launch_rmsnorm(const __nv_bfloat16* x, long long ldx, const int* rows, const float* gain, __nv_bfloat16* out,
                    long long ldo, int n_rows, int d, float eps, cudaStream_t st);
 size_t argmax_scratch_bytes(int rows);

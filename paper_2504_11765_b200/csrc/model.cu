@@ -24,6 +24,7 @@ struct rdkv_model {
   rdkv_model_desc d;
   std::vector<const void*> w;  // see rdkv.h for the order
   float* rope = nullptr;        // [max_pos][dh/2] (cos, sin)
+  float* ones = nullptr;        // unit gain [hidden] (norm gains folded into the weights)
   int device = 0;
   rdkv_tp_comm* tp = nullptr;  // tensor-parallel group (row-parallel outputs all-reduced), or null
   // measurement (rdkv_profile_*)
@@ -87,6 +88,7 @@ inline size_t up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Ws {
   __nv_bfloat16 *x, *h, *q, *o, *a, *hl;
+  float* ssq;  // fused-RMSNorm statistics [hidden/32][T]
   void* splitk;
   size_t splitk_bytes;
   void* attn_split;
@@ -118,7 +120,9 @@ size_t ws_layout(const rdkv_model_desc& d, int T, int S, Ws* ws, void* base) {
   const size_t oask = take(ask);
   const size_t osk_attn = take(attention_sk_scratch_bytes(num_sms(), d.head_dim));
   const size_t oam = take(argmax_scratch_bytes(S));
+  const size_t ossq = take((size_t)(d.hidden / 32) * T * sizeof(float));
   if (ws && base) {
+    ws->ssq = reinterpret_cast<float*>(static_cast<uint8_t*>(base) + ossq);
     ws->argmax = static_cast<uint8_t*>(base) + oam;
     ws->attn_split = ask ? static_cast<uint8_t*>(base) + oask : nullptr;
     ws->attn_split_bytes = ask;
@@ -180,11 +184,15 @@ int rdkv_model_create(const rdkv_model_desc* desc, const void* const* weights, s
       tab[((size_t)p * half + i) * 2] = (float)std::cos(a);
       tab[((size_t)p * half + i) * 2 + 1] = (float)std::sin(a);
     }
+  const std::vector<float> ones((size_t)d.hidden, 1.0f);
   if (cudaMalloc(&m->rope, tab.size() * sizeof(float)) != cudaSuccess ||
-      cudaMemcpy(m->rope, tab.data(), tab.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaMemcpy(m->rope, tab.data(), tab.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMalloc(&m->ones, ones.size() * sizeof(float)) != cudaSuccess ||
+      cudaMemcpy(m->ones, ones.data(), ones.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess) {
     cudaFree(m->rope);
+    cudaFree(m->ones);
     delete m;
-    return set_error(RDKV_ERR_CUDA, "model_create: rope table upload failed");
+    return set_error(RDKV_ERR_CUDA, "model_create: rope / gain table upload failed");
   }
   *out = m;
   return 0;
@@ -198,6 +206,7 @@ void rdkv_model_destroy(rdkv_model* m) {
   }
   for (auto e : m->spare) cudaEventDestroy(e);
   cudaFree(m->rope);
+  cudaFree(m->ones);
   delete m;
 }
 
@@ -251,12 +260,26 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     attention_sk_carve(z, ws.attn_sk, num_sms(), dh);
     RDKV_TRY(attention_sk_zero_flags(z, st));
   }
-  LAUNCH(RDKV_PROF_MISC, 0.0, launch_embed(b->tokens, W(m, 0), ws.x, T, d.hidden, d.vocab, st));
   // small batches run the residual GEMMs split-K; their finalize also applies the
   // following RMSNorm, saving a launch per norm
   rdkv_tp_comm* tp = m->tp && m->tp->size > 1 ? m->tp : nullptr;
   const bool o_fused = !tp && gemm_splits(T, d.hidden, (int)qd, ws.splitk_bytes);
   const bool down_fused = !tp && gemm_splits(T, d.hidden, d.ffn, ws.splitk_bytes);
+  // norm gains folded into w_qkv / w_gate_up: the attention / MLP norms carry unit gain
+  const bool folded = (d.flags & RDKV_MODEL_NORM_FOLDED) != 0;
+  auto gain = [&](int i) { return folded ? static_cast<const float*>(m->ones) : G(m, i); };
+  // large batches fuse the norms across GEMMs (no rmsnorm launches): the embedding and
+  // residual epilogues emit per-row sums of squares, the QKV / gate-up epilogues scale
+  const int qkv_n = (int)((hq + 2 * hkv) * dh);
+  static const bool fuse_norm_env = [] {
+    const char* e = std::getenv("RDKV_FUSED_NORM");  // "0": rmsnorm launches instead (A/B)
+    return !(e && e[0] == '0');
+  }();
+  const bool ssq_path = fuse_norm_env && folded && !tp && !o_fused && !down_fused && d.hidden % 256 == 0 &&
+                        !gemm_splits(T, qkv_n, d.hidden, ws.splitk_bytes) &&
+                        !gemm_splits(T, 2 * d.ffn, d.hidden, ws.splitk_bytes);
+  LAUNCH(RDKV_PROF_MISC, 0.0, launch_embed(b->tokens, W(m, 0), ws.x, T, d.hidden, d.vocab, st,
+                                           ssq_path ? ws.ssq : nullptr));
   int ar = 0;  // all-reduces issued by this forward (2 per layer: parity selects the partial buffer)
   bool h_ready = false;  // ws.h already holds this layer's attention-norm output
   for (int l = 0; l < d.layers; ++l) {
@@ -264,11 +287,17 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     __nv_bfloat16* kpl = kv + (2LL * l) * plane;
     __nv_bfloat16* vpl = kv + (2LL * l + 1) * plane;
     // attention block
-    if (!h_ready)
-      LAUNCH(RDKV_PROF_MISC, 0.0, launch_rmsnorm(ws.x, d.hidden, nullptr, G(m, wb + 0), ws.h, d.hidden, T, d.hidden, d.norm_eps, st));
+    if (!h_ready && !ssq_path)
+      LAUNCH(RDKV_PROF_MISC, 0.0, launch_rmsnorm(ws.x, d.hidden, nullptr, gain(wb + 0), ws.h, d.hidden, T, d.hidden, d.norm_eps, st));
     GemmEpi eq{};
-    eq.splitk_ws = ws.splitk;
-    eq.splitk_bytes = ws.splitk_bytes;
+    eq.splitk_ws = ssq_path ? nullptr : ws.splitk;
+    eq.splitk_bytes = ssq_path ? 0 : ws.splitk_bytes;
+    if (ssq_path) {
+      eq.ssq_in = ws.ssq;
+      eq.ssq_parts = d.hidden / 32;
+      eq.ssq_dim = d.hidden;
+      eq.norm_eps = d.norm_eps;
+    }
     eq.q = ws.q;
     eq.ldq = qd;
     eq.kplane = kpl;
@@ -280,7 +309,7 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     eq.hq = hq;
     eq.hkv = hkv;
     LAUNCH(RDKV_PROF_QKV, 2.0 * T * (hq + 2 * hkv) * dh * d.hidden,
-           launch_gemm(ws.h, d.hidden, W(m, wb + 1), d.hidden, T, (int)((hq + 2 * hkv) * dh), d.hidden, EPI_QKV, dh,
+           launch_gemm(ssq_path ? ws.x : ws.h, d.hidden, W(m, wb + 1), d.hidden, T, qkv_n, d.hidden, EPI_QKV, dh,
                          eq, st));
     // document-KV generation (no logits): the last layer's KV is written by the QKV
     // epilogue above; its attention, O projection and MLP feed nothing
@@ -329,15 +358,16 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     else
       LAUNCH(RDKV_PROF_ATTN, 0.0, launch_attention(ap, dh, S, b->max_new, st));
     GemmEpi er{};
-    er.splitk_ws = ws.splitk;
-    er.splitk_bytes = ws.splitk_bytes;
+    er.splitk_ws = ssq_path ? nullptr : ws.splitk;
+    er.splitk_bytes = ssq_path ? 0 : ws.splitk_bytes;
     er.out = ws.x;
     er.ldo = d.hidden;
     er.resid = ws.x;
     er.ldr = d.hidden;
     er.norm_eps = d.norm_eps;
+    if (ssq_path) er.ssq_out = ws.ssq;
     if (o_fused) {
-      er.norm_gain = G(m, wb + 3);
+      er.norm_gain = gain(wb + 3);
       er.norm_out = ws.h;
     }
     if (tp) {  // row-parallel: the GEMM pushes its bf16 tiles to every rank (NVLink), then reduce + residual
@@ -349,16 +379,22 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
       LAUNCH(RDKV_PROF_O, 2.0 * T * qd * d.hidden, launch_gemm(ws.o, qd, W(m, wb + 2), qd, T, d.hidden, (int)qd, EPI_RESID, 0, er, st));
     }
     // MLP block
-    if (!o_fused)
-      LAUNCH(RDKV_PROF_MISC, 0.0, launch_rmsnorm(ws.x, d.hidden, nullptr, G(m, wb + 3), ws.h, d.hidden, T, d.hidden, d.norm_eps, st));
+    if (!o_fused && !ssq_path)
+      LAUNCH(RDKV_PROF_MISC, 0.0, launch_rmsnorm(ws.x, d.hidden, nullptr, gain(wb + 3), ws.h, d.hidden, T, d.hidden, d.norm_eps, st));
     GemmEpi eg{};
-    eg.splitk_ws = ws.splitk;
-    eg.splitk_bytes = ws.splitk_bytes;
+    eg.splitk_ws = ssq_path ? nullptr : ws.splitk;
+    eg.splitk_bytes = ssq_path ? 0 : ws.splitk_bytes;
     eg.out = ws.a;
     eg.ldo = d.ffn;
-    LAUNCH(RDKV_PROF_GU, 4.0 * T * d.ffn * d.hidden, launch_gemm(ws.h, d.hidden, W(m, wb + 4), d.hidden, T, 2 * d.ffn, d.hidden, EPI_SWIGLU, 0, eg, st));
+    if (ssq_path) {
+      eg.ssq_in = ws.ssq;
+      eg.ssq_parts = d.hidden / 32;
+      eg.ssq_dim = d.hidden;
+      eg.norm_eps = d.norm_eps;
+    }
+    LAUNCH(RDKV_PROF_GU, 4.0 * T * d.ffn * d.hidden, launch_gemm(ssq_path ? ws.x : ws.h, d.hidden, W(m, wb + 4), d.hidden, T, 2 * d.ffn, d.hidden, EPI_SWIGLU, 0, eg, st));
     h_ready = down_fused && l + 1 < d.layers;
-    er.norm_gain = h_ready ? G(m, wb + RDKV_WEIGHTS_PER_LAYER + 0) : nullptr;  // next layer's attention norm
+    er.norm_gain = h_ready ? gain(wb + RDKV_WEIGHTS_PER_LAYER + 0) : nullptr;  // next layer's attention norm
     er.norm_out = h_ready ? ws.h : nullptr;
     if (tp) {
       const GemmEpi ep = tp_push_epi(er, tp, ar, d.hidden);

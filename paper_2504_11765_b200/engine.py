@@ -39,7 +39,9 @@ from .model import ModelSpec, ModelWeights, init_weights
 class RdkvModelDesc(C.Structure):
     _fields_ = [("layers", C.c_int32), ("hidden", C.c_int32), ("n_heads", C.c_int32), ("kv_heads", C.c_int32),
                 ("head_dim", C.c_int32), ("ffn", C.c_int32), ("vocab", C.c_int32), ("max_pos", C.c_int32),
-                ("rope_theta", C.c_float), ("norm_eps", C.c_float)]
+                ("rope_theta", C.c_float), ("norm_eps", C.c_float), ("flags", C.c_int32)]
+
+RDKV_MODEL_NORM_FOLDED = 1
 
 
 class RdkvBatch(C.Structure):
@@ -271,13 +273,16 @@ class BatchPlan:
 class DeviceModel:
     """Owns an rdkv_model handle over device-resident weights."""
 
-    def __init__(self, weights: ModelWeights) -> None:
+    def __init__(self, weights: ModelWeights, fold_norms: bool = True) -> None:
         s = weights.spec
         self.spec, self.weights = s, weights
         self.device = weights.embed.device
+        if fold_norms:
+            fold_norm_gains(weights)
         desc = RdkvModelDesc(layers=s.layers, hidden=s.hidden, n_heads=s.n_heads, kv_heads=s.kv_heads,
                              head_dim=s.head_dim, ffn=s.ffn, vocab=s.vocab, max_pos=s.max_pos,
-                             rope_theta=s.rope_theta, norm_eps=s.norm_eps)
+                             rope_theta=s.rope_theta, norm_eps=s.norm_eps,
+                             flags=RDKV_MODEL_NORM_FOLDED if fold_norms else 0)
         ptrs = weights.pointer_list()
         arr = (C.c_void_p * len(ptrs))(*ptrs)
         h = C.c_void_p()
@@ -326,6 +331,24 @@ class DeviceModel:
         ws = self.workspace(plan.n_tokens, plan.n_seqs, stream)
         b = plan.struct(kv_base, kv_slots, logits, next_token, layer_ready)
         _lib.check(_L().rdkv_forward(self._h, C.byref(b), ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
+
+
+def fold_norm_gains(w: ModelWeights) -> None:
+    """Fold the attention / MLP RMSNorm gains into the columns of w_qkv / w_gate_up
+    (W'[n, k] = bf16(W[n, k] * gain[k])) in place and replace the gains by ones, so
+    the weights describe the same function with unit-gain norms (the oracle reads
+    them the same way).  The device then fuses each norm across its GEMMs
+    (RDKV_MODEL_NORM_FOLDED).  Idempotent: folded gains are exactly 1."""
+    for lw in w.layers:
+        for wk, gk in (("wqkv", "attn_norm"), ("wgu", "mlp_norm")):
+            g = lw[gk]
+            if bool((g == 1).all()):
+                continue
+            W = lw[wk]
+            for r0 in range(0, W.shape[0], 4096):  # bounded fp32 temporaries
+                blk = W[r0:r0 + 4096]
+                blk.copy_((blk.float() * g.float()[None, :]).to(W.dtype))
+            lw[gk] = torch.ones_like(g)  # new tensor: gains shared with other shards stay intact
 
 
 def kv_unpack(pool: KvPool, jobs: Sequence[tuple[torch.Tensor, int, int]], block_table: torch.Tensor,

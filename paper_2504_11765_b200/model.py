@@ -121,7 +121,7 @@ def shard_weights(w: "ModelWeights", rank: int, size: int) -> "ModelWeights":
             "attn_norm": lw["attn_norm"], "mlp_norm": lw["mlp_norm"],
             "wqkv": torch.cat([wq, wk, wv]).contiguous(),
             "wo": lw["wo"][:, rank * hq * dh:(rank + 1) * hq * dh].contiguous(),
-            "wgu": blocks.reshape(2 * f, d).contiguous(),
+            "wgu": blocks.reshape(2 * f, d).clone(),  # own storage: a shard's norm-gain fold stays in the shard
             "wdown": lw["wdown"][:, rank * f:(rank + 1) * f].contiguous(),
         })
     return out

@@ -600,7 +600,7 @@ def serve(engine: Engine, store: KvStore, cfg: RuntimeConfig, items: Sequence, r
             "hbm_tier": {"entries": len(engine.resident), "blocks": engine.resident.used,
                          "evictions": engine.resident.evictions},
         })
-        out = {"summary": rep, "results": results, "access_log": access}
+        out = {"summary": rep, "results": results, "access_log": access, "generated": generated}
     inst.close()
     if dist is not None:
         dist.barrier(group=group)
