@@ -62,6 +62,9 @@ static int make_tmap_q(CUtensorMap* m, const void* q, long long tokens, int hq, 
   return 0;
 }
 
+#ifndef RDKV_ATTN_LSUM
+#define RDKV_ATTN_LSUM 0  // 1: dh = 128 row sums on the tensor cores (L += P.ones; measured slower: 111 vs 98 us)
+#endif
 namespace {
 
 constexpr int ROWS = 128;
@@ -76,7 +79,13 @@ struct TcCfg {
   // S -> P -> P.V -> next S chain serialised: ~4.3k cycles per 128 keys)
   static constexpr int BKV = DH == 128 ? 64 : 128;
   static constexpr bool ALIAS = false;  // P_i over S_i (kept for reference; no shape needs it now)
-  static constexpr int STAGES = DH == 64 ? 5 : 4;
+#ifndef RDKV_ATTN_ST64
+#define RDKV_ATTN_ST64 5
+#endif
+#ifndef RDKV_ATTN_ST128
+#define RDKV_ATTN_ST128 4
+#endif
+  static constexpr int STAGES = DH == 64 ? RDKV_ATTN_ST64 : RDKV_ATTN_ST128;
   static constexpr uint32_t QB = ROWS * DH * 2;    // one Q tile
   static constexpr uint32_t KB = BKV * DH * 2;     // one K (or V) tile
   static constexpr uint32_t OFF_Q = 0;             // [2 Q tiles]
@@ -87,12 +96,18 @@ struct TcCfg {
   static constexpr uint32_t OFF_MISC = (OFF_BAR + 8 * (4 + 3 * STAGES + 8) + 15) / 16 * 16;  // TMEM base, segment count, W
   static constexpr uint32_t OFF_SEG = OFF_MISC + 16;                        // stream-K segments (int4)
   static constexpr uint32_t OFF_SEQ = OFF_SEG + 16 * 512;                   // stream-K: [3][512] seq start/new/cached
-  static constexpr size_t SMEM = OFF_SEQ + 3 * 4 * 512;
+  // row sums on the tensor cores (dh = 128, where TMEM has room): L_i += P_i . ones, with a
+  // constant [16 x BKV] bf16 ones tile as the K-major B operand (16 columns of L_i, all equal)
+  static constexpr bool LSUM = RDKV_ATTN_LSUM && DH == 128 && !ALIAS;
+  static constexpr uint32_t OFF_ONES = (OFF_SEQ + 3 * 4 * 512 + 1023) / 1024 * 1024;
+  static constexpr size_t SMEM = LSUM ? OFF_ONES + 16 * 128 : OFF_SEQ + 3 * 4 * 512;
   // TMEM columns
   static constexpr uint32_t COL_S = 0;                          // S_i at 128 i
   static constexpr uint32_t COL_O = 2 * BKV;                    // O_i at 256 + DH i
   static constexpr uint32_t COL_P = ALIAS ? 0 : 2 * BKV + 2 * DH;  // P_i at COL_P + (ALIAS ? 128 : 64) i
   static constexpr uint32_t P_STRIDE = ALIAS ? BKV : BKV / 2;
+  static constexpr uint32_t COL_L = COL_P + 2 * P_STRIDE;     // L_i at COL_L + 16 i (LSUM)
+  static_assert(!LSUM || COL_L + 32 <= 512, "TMEM: L columns do not fit");
 };
 
 // SPL softmax warps per query row (each takes BKV / SPL keys of a tile):
@@ -142,6 +157,9 @@ __device__ __forceinline__ long long gtimer() {
 #endif
 constexpr int EMU_OF_8 = RDKV_ATTN_EMU;  // exp2 of this many of every 8 score groups runs as a polynomial
 
+#ifndef RDKV_ATTN_PF
+#define RDKV_ATTN_PF 0  // TMA producer L2 prefetch distance in tiles (0: off; 2-8 measured no faster)
+#endif
 #ifndef RDKV_ATTN_SPIN
 #define RDKV_ATTN_SPIN 1
 #endif
@@ -372,6 +390,13 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
     }
   }
   if (warp == NS + 1) tmem_alloc(tmem_slot, 512);
+  if constexpr (C::LSUM) {
+    if (warp == NS + 3) {  // constant B operand of the row-sum MMA: bf16 1.0 everywhere
+      uint32_t* ones = reinterpret_cast<uint32_t*>(smem + C::OFF_ONES);
+      for (int w = lane; w < 16 * 128 / 4; w += 32) ones[w] = 0x3F803F80u;
+      fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core (async proxy)
+    }
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -435,6 +460,23 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
             for (int h = 0; h < NH; ++h)
               tma_load_2d_nohint(&tmV, &v_full[st], smem + C::OFF_V + st * C::KB + c * (BKV * 128) + h * (HALF * 128),
                                  c * 64, rows[h]);
+          // the smem ring holds only STAGES tiles and a stage is refilled only after its
+          // P.V retired: with the KV stream coming from HBM under full load (~4.5k cycles
+          // latency measured) the ring alone runs dry, so warm L2 RDKV_ATTN_PF tiles ahead
+          if (RDKV_ATTN_PF > 0 && j + RDKV_ATTN_PF < sg.z) {
+            const int jp = j + RDKV_ATTN_PF;
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+              int pos = jp * BKV + h * HALF;
+              if (pos >= u.kv_len) continue;
+              const int prow = (int)(row0 + (long long)bt[pos / p.block_size] * p.block_size + pos % p.block_size);
+#pragma unroll
+              for (int c = 0; c < DH / 64; ++c) {
+                tma_prefetch_2d(&tmK, c * 64, prow);
+                tma_prefetch_2d(&tmV, c * 64, prow);
+              }
+            }
+          }
         }
         __syncwarp();
       }
@@ -502,6 +544,14 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
             // P of keys [16kk, 16kk+16): with P over S each half writes inside its own S columns
             const uint32_t pcol = C::ALIAS ? (kk / (KH / 16)) * KH + (kk % (KH / 16)) * 8 : kk * 8;
             umma_bf16_ts(tO, tP + pcol, desc_mn(va + kk * 2048, BKV * 128), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          if constexpr (C::LSUM) {  // L_i (+)= P_i . ones: the row sums, off the softmax warps
+            constexpr uint32_t idesc_l = idesc_bf16_f32(ROWS, 16);
+            const uint32_t oa = sb + C::OFF_ONES;
+#pragma unroll
+            for (int kk = 0; kk < BKV / 16; ++kk)
+              umma_bf16_ts(tmem + C::COL_L + i * 16, tP + kk * 8, desc_k(oa + (kk & 3) * 32), idesc_l,
+                           (j > 0 || kk > 0) ? 1u : 0u);
           }
           umma_commit(&o_done[i]);
           TRACE(2 + i, ti, 1);
@@ -598,6 +648,7 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
           mbar_wait(&s_full[i], ti & 1);
           tc_fence_after();
           if (j == 0) TRACE(i, ti, 7);
+          if (j + 1 < nt) TRACE(i, ti, 2);
           uint32_t sv[KH];
 #pragma unroll
           for (int c = 0; c < KH / 32; ++c) tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[c * 32]));
@@ -646,19 +697,31 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
               x2 = ex2_approx(x2);
               x3 = ex2_approx(x3);
             }
-            fadd2(s0, s1, s0, s1, x0, x1);
-            fadd2(s2, s3, s2, s3, x2, x3);
+            if constexpr (!C::LSUM) {
+              fadd2(s0, s1, s0, s1, x0, x1);
+              fadd2(s2, s3, s2, s3, x2, x3);
+            }
             pk[e / 2] = pack_bf16(x0, x1);
             pk[e / 2 + 1] = pack_bf16(x2, x3);
           }
           // P_i (and O_i) are free once P_i.V(j-1) has retired (implied by s_full when P aliases S)
+          if (j + 1 < nt) TRACE(i, ti, 3);
           if (j > 0) {
             mbar_wait(&o_done[i], (ti - 1) & 1);
             tc_fence_after();
           }
+          if (j + 1 < nt) TRACE(i, ti, 4);
 #pragma unroll
           for (int c = 0; c < KH / 64; ++c) tmem_st32(tP + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[c * 32]));
           l += (s0 + s1) + (s2 + s3);
+          if (C::LSUM && rescale) {  // L_i (tensor-core row sums) at the new scale too
+            uint32_t lv[16];
+            tmem_ld16(tmem + C::COL_L + i * 16 + lane_off, lv);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) lv[e] = __float_as_uint(__uint_as_float(lv[e]) * f);
+            tmem_st16(tmem + C::COL_L + i * 16 + lane_off, lv);
+          }
           if (rescale) {  // this half of the O_i row *= f before P_i.V(j) accumulates into it
 #pragma unroll
             for (int c = 0; c < OH / 32; ++c) {
@@ -685,6 +748,12 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
         TRACE(i, ti, 1);
         mbar_wait(&o_done[i], (ti - 1) & 1);
         tc_fence_after();
+        if constexpr (C::LSUM) {  // the row sum of the bf16 P the tensor cores multiplied V by
+          uint32_t lv[16];
+          tmem_ld16(tmem + C::COL_L + i * 16 + lane_off, lv);
+          tmem_ld_wait();
+          l = __uint_as_float(lv[0]);
+        }
         TRACE(i, ti, 2);
       }
       // ---- the segment's O rows (every lane of an active tile joins the .sync.aligned TMEM loads)
