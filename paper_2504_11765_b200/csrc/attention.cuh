@@ -39,6 +39,11 @@ struct AttnParams {
   int* sk_flag;                 // [ctas]
   int sk_ctas;                  // CTAs the scratch was sized for (0 = no stream-K)
   int sk_mode;                  // 1: use stream-K where it applies (rdkv_attention impl 2, RDKV_ATTN_SK=1)
+  // L2 prefetch of the next kernel's weights (the O projection) by the Q-loader warp;
+  // the K/V stream itself is loaded evict-first so it does not push them out.  Null = off.
+  const void* l2_next;
+  long long l2_next_bytes;
+  int kv_evict_first;           // set by the launcher: every K/V tile is read by one CTA only
 };
 
 // stream-K scratch: partials + flags for `ctas` CTAs; carve() points p's sk_* into it

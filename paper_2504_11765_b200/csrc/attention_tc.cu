@@ -443,6 +443,7 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
         for (int h = 0; h < NH; ++h) rows[h] = __shfl_sync(0xffffffffu, my_rows[h], (j - sg.y) & 31);
         if (lane == 0) {
           const int st = it % ST;
+          const uint64_t pol_kv = policy_evict_first();
           TRACE(4, it, 0);
           mbar_wait_sleep(&kv_empty[st], ((it / ST) & 1) ^ 1);
           TRACE(4, it, 1);
@@ -451,15 +452,23 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
           for (int c = 0; c < DH / 64; ++c)
 #pragma unroll
             for (int h = 0; h < NH; ++h)
-              tma_load_2d_nohint(&tmK, &k_full[st], smem + C::OFF_K + st * C::KB + c * (BKV * 128) + h * (HALF * 128),
-                                 c * 64, rows[h]);
+              if (p.kv_evict_first)  // a streamed K/V tile is read once: keep L2 for the prefetched weights
+                tma_load_2d(&tmK, &k_full[st], smem + C::OFF_K + st * C::KB + c * (BKV * 128) + h * (HALF * 128),
+                            c * 64, rows[h], pol_kv);
+              else
+                tma_load_2d_nohint(&tmK, &k_full[st], smem + C::OFF_K + st * C::KB + c * (BKV * 128) + h * (HALF * 128),
+                                   c * 64, rows[h]);
           mbar_arrive_expect_tx(&v_full[st], C::KB);
 #pragma unroll
           for (int c = 0; c < DH / 64; ++c)
 #pragma unroll
             for (int h = 0; h < NH; ++h)
-              tma_load_2d_nohint(&tmV, &v_full[st], smem + C::OFF_V + st * C::KB + c * (BKV * 128) + h * (HALF * 128),
-                                 c * 64, rows[h]);
+              if (p.kv_evict_first)  // a streamed K/V tile is read once: keep L2 for the prefetched weights
+                tma_load_2d(&tmV, &v_full[st], smem + C::OFF_V + st * C::KB + c * (BKV * 128) + h * (HALF * 128),
+                            c * 64, rows[h], pol_kv);
+              else
+                tma_load_2d_nohint(&tmV, &v_full[st], smem + C::OFF_V + st * C::KB + c * (BKV * 128) + h * (HALF * 128),
+                                   c * 64, rows[h]);
           // the smem ring holds only STAGES tiles and a stage is refilled only after its
           // P.V retired: with the KV stream coming from HBM under full load (~4.5k cycles
           // latency measured) the ring alone runs dry, so warm L2 RDKV_ATTN_PF tiles ahead
@@ -530,13 +539,17 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
           const bool more = j + 1 < nt;
           if (!C::ALIAS && more) {  // next S_i while the softmax still works on this tile
             issuer_wait(&k_full[(it + 1) % ST], ((it + 1) / ST) & 1);
+            if (j > 0) TRACE(2 + i, ti, 2);
             issuer_wait(&s_empty[i], ti & 1);
+            if (j > 0) TRACE(2 + i, ti, 3);
             tc_fence_after();
             issue_qk((it + 1) % ST, j + 2 == nt);
             TRACE(2 + i, ti, 0);
           }
           issuer_wait(&v_full[st], (it / ST) & 1);
+          if (j > 0) TRACE(2 + i, ti, 4);
           issuer_wait(&p_full[i], ti & 1);
+          if (j > 0) TRACE(2 + i, ti, 5);
           tc_fence_after();
           const uint32_t va = sb + C::OFF_V + st * C::KB;
 #pragma unroll
@@ -595,6 +608,11 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
         __syncwarp();
         asm volatile("bar.sync %0, %1;" ::"n"(SK_PUB), "n"(NS * 32 + 32) : "memory");
         if (lane == 0) st_release_gpu(p.sk_flag + blockIdx.x, 1);
+      }
+      if (k == 0) {  // Q requested: pull the O projection's weights into L2 meanwhile
+        __syncwarp();
+        l2_prefetch_share(p.l2_next, p.l2_next_bytes, blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z),
+                          gridDim.x * gridDim.y * gridDim.z, lane);
       }
     }
   } else if (warp < NS) {
@@ -934,6 +952,8 @@ int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
   q.kv_splits = 1;
   q.n_seqs = n_seqs;
   q.sk_qblocks = qblocks;
+  // K/V evict-first only alongside the (opt-in) weight prefetch it protects
+  q.kv_evict_first = qblocks == 1 && p.l2_next ? 1 : 0;
   const int ctas = qblocks * p.hkv * n_seqs, sms = num_sms();
   const int max_tiles = (p.max_ctx + C::BKV - 1) / C::BKV;
   // stream-K (opt-in: p.sk_mode) when the unit grid is at least half a wave; measured

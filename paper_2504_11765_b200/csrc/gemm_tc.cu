@@ -191,58 +191,64 @@ __device__ __forceinline__ void epilogue_rows(uint32_t taddr, int row, int nb, i
         st_bf16x32(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + col, w);
       }
     }
-  } else if constexpr (EPI == EPI_QKV && DH == 64) {
-    // dh = 64: each epilogue warpgroup takes one quarter of every head and its RoPE
-    // partner quarter (columns 16h.. and 32+16h..), so both halves do the same work
-    // for any head count per tile (a 256x192 tile has 3 heads), and the (cos, sin)
-    // of this token's 16 frequencies is loaded once for all heads of the tile
+  } else if constexpr (EPI == EPI_QKV && (DH == 64 || DH == 128)) {
+    // each epilogue warpgroup takes a quarter of every head's columns and their RoPE
+    // partners (frequencies [half DH/4, (half+1) DH/4): columns f and f + DH/2), in
+    // chunks of 16 frequencies, so both halves do the same work for any head count per
+    // tile (a 256x384 tile holds 3 heads of 128, a 256x192 one 3 heads of 64) and the
+    // (cos, sin) of this token's 16 frequencies is loaded once per chunk for all heads
     static_assert(BN % DH == 0, "tile must hold whole heads");
     constexpr int HEADS = BN / DH;
+    constexpr int NCH = DH / 64;  // 16-frequency chunks per warpgroup
     const int p = row_ok ? ep.pos[row] : 0;
     const int sl = row_ok ? ep.slot[row] : 0;
-    float2 cs[16];
-    {
-      const float4* src = reinterpret_cast<const float4*>(ep.rope + (long long)p * DH + half * 32);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float4 t = src[i];
-        cs[2 * i] = make_float2(t.x, t.y);
-        cs[2 * i + 1] = make_float2(t.z, t.w);
-      }
-    }
 #pragma unroll 1
-    for (int hh = 0; hh < HEADS; ++hh) {
-      uint32_t ra[16], rb[16];
-      tmem_ld16(taddr + hh * DH + half * 16, ra);
-      tmem_ld16(taddr + hh * DH + 32 + half * 16, rb);
-      tmem_ld_wait();
-      const int g = (nb * BN + hh * DH) / DH;  // global head index in [q | k | v]
-      if (!row_ok || g >= ep.hq + 2 * ep.hkv) continue;
-      uint32_t wa[8], wb[8];
-      if (g < ep.hq + ep.hkv) {
+    for (int ch = 0; ch < NCH; ++ch) {
+      const int f0 = half * (DH / 4) + ch * 16;  // first frequency of this chunk
+      float2 cs[16];
+      {
+        const float4* src = reinterpret_cast<const float4*>(ep.rope + (long long)p * DH + 2 * f0);
 #pragma unroll
-        for (int i = 0; i < 16; i += 2) {
-          const float a0 = rs * __uint_as_float(ra[i]), a1 = rs * __uint_as_float(ra[i + 1]);
-          const float b0 = rs * __uint_as_float(rb[i]), b1 = rs * __uint_as_float(rb[i + 1]);
-          wa[i / 2] = pack_bf16(a0 * cs[i].x - b0 * cs[i].y, a1 * cs[i + 1].x - b1 * cs[i + 1].y);
-          wb[i / 2] = pack_bf16(b0 * cs[i].x + a0 * cs[i].y, b1 * cs[i + 1].x + a1 * cs[i + 1].y);
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; i += 2) {
-          wa[i / 2] = pack_bf16(rs * __uint_as_float(ra[i]), rs * __uint_as_float(ra[i + 1]));
-          wb[i / 2] = pack_bf16(rs * __uint_as_float(rb[i]), rs * __uint_as_float(rb[i + 1]));
+        for (int i = 0; i < 8; ++i) {
+          const float4 t = src[i];
+          cs[2 * i] = make_float2(t.x, t.y);
+          cs[2 * i + 1] = make_float2(t.z, t.w);
         }
       }
-      __nv_bfloat16* dst;
-      if (g < ep.hq)
-        dst = ep.q + (long long)row * ep.ldq + (long long)g * DH;
-      else if (g < ep.hq + ep.hkv)
-        dst = ep.kplane + (long long)(g - ep.hq) * ep.head_stride + (long long)sl * DH;
-      else
-        dst = ep.vplane + (long long)(g - ep.hq - ep.hkv) * ep.head_stride + (long long)sl * DH;
-      st_global_256(dst + half * 16, wa);  // 32-B aligned: head rows are 128 B
-      st_global_256(dst + 32 + half * 16, wb);
+#pragma unroll 1
+      for (int hh = 0; hh < HEADS; ++hh) {
+        uint32_t ra[16], rb[16];
+        tmem_ld16(taddr + hh * DH + f0, ra);
+        tmem_ld16(taddr + hh * DH + DH / 2 + f0, rb);
+        tmem_ld_wait();
+        const int g = (nb * BN + hh * DH) / DH;  // global head index in [q | k | v]
+        if (!row_ok || g >= ep.hq + 2 * ep.hkv) continue;
+        uint32_t wa[8], wb[8];
+        if (g < ep.hq + ep.hkv) {
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            const float a0 = rs * __uint_as_float(ra[i]), a1 = rs * __uint_as_float(ra[i + 1]);
+            const float b0 = rs * __uint_as_float(rb[i]), b1 = rs * __uint_as_float(rb[i + 1]);
+            wa[i / 2] = pack_bf16(a0 * cs[i].x - b0 * cs[i].y, a1 * cs[i + 1].x - b1 * cs[i + 1].y);
+            wb[i / 2] = pack_bf16(b0 * cs[i].x + a0 * cs[i].y, b1 * cs[i + 1].x + a1 * cs[i + 1].y);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            wa[i / 2] = pack_bf16(rs * __uint_as_float(ra[i]), rs * __uint_as_float(ra[i + 1]));
+            wb[i / 2] = pack_bf16(rs * __uint_as_float(rb[i]), rs * __uint_as_float(rb[i + 1]));
+          }
+        }
+        __nv_bfloat16* dst;
+        if (g < ep.hq)
+          dst = ep.q + (long long)row * ep.ldq + (long long)g * DH;
+        else if (g < ep.hq + ep.hkv)
+          dst = ep.kplane + (long long)(g - ep.hq) * ep.head_stride + (long long)sl * DH;
+        else
+          dst = ep.vplane + (long long)(g - ep.hq - ep.hkv) * ep.head_stride + (long long)sl * DH;
+        st_global_256(dst + f0, wa);  // 32-B aligned: f0 is a multiple of 16
+        st_global_256(dst + DH / 2 + f0, wb);
+      }
     }
   } else if constexpr (EPI == EPI_QKV) {
     static_assert(BN % DH == 0, "tile must hold whole heads");
@@ -326,6 +332,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // ---------------- TMA producer
     if (lane == 0) {
       const uint64_t pol_act = policy_evict_last();
+      const uint64_t pol_w = ep.w_policy ? policy_evict_first() : pol_act;
       int stage = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -335,7 +342,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           tma_load_2d(&tmA, &full[stage], sA + stage * C::A_BYTES, kb * BK, mb * BM, pol_act);
-          tma_load_2d_nohint(&tmB, &full[stage], sB + stage * C::B_BYTES, kb * BK, nb * BN);
+          if (ep.w_policy)
+            tma_load_2d(&tmB, &full[stage], sB + stage * C::B_BYTES, kb * BK, nb * BN, pol_w);
+          else
+            tma_load_2d_nohint(&tmB, &full[stage], sB + stage * C::B_BYTES, kb * BK, nb * BN);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -376,6 +386,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (acc == 0) acc_phase ^= 1;
       }
     }
+  } else if (warp == 3) {
+    // idle warp: pull the next kernel's weights into L2 while this GEMM computes
+    l2_prefetch_share(ep.l2_next, ep.l2_next_bytes, blockIdx.x, gridDim.x, lane);
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> registers -> fused op -> global
     const int wq = warp & 3;
@@ -474,6 +487,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol_act = policy_evict_last();
+      const uint64_t pol_w = ep.w_policy ? policy_evict_first() : pol_act;
       int stage = 0;
       uint32_t phase = 0;
       for (int u = pair; u < units; u += npairs) {
@@ -487,11 +501,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             // each CTA holds its N-half of both MMAs: rows [128 r, +128) of the N = 256 one and
             // [256 + 64 r, +64) of the N = 128 one (64-row boxes)
             uint8_t* b = sB + stage * B_BYTES;
-            tma_load_2d_2sm(&tmB, bar, b, kb * BK, nb * BN + (int)rank * 128, pol_act);
-            tma_load_2d_2sm(&tmB, bar, b + 64 * 128, kb * BK, nb * BN + (int)rank * 128 + 64, pol_act);
-            tma_load_2d_2sm(&tmB, bar, b + 128 * 128, kb * BK, nb * BN + 256 + (int)rank * 64, pol_act);
+            tma_load_2d_2sm(&tmB, bar, b, kb * BK, nb * BN + (int)rank * 128, pol_w);
+            tma_load_2d_2sm(&tmB, bar, b + 64 * 128, kb * BK, nb * BN + (int)rank * 128 + 64, pol_w);
+            tma_load_2d_2sm(&tmB, bar, b + 128 * 128, kb * BK, nb * BN + 256 + (int)rank * 64, pol_w);
           } else {
-            tma_load_2d_2sm(&tmB, bar, sB + stage * B_BYTES, kb * BK, nb * BN + (int)rank * (BN / 2), pol_act);
+            tma_load_2d_2sm(&tmB, bar, sB + stage * B_BYTES, kb * BK, nb * BN + (int)rank * (BN / 2), pol_w);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -535,6 +549,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (acc == 0) acc_phase ^= 1;
       }
     }
+  } else if (warp == 3) {
+    // idle warp: pull the next kernel's weights into L2 while this GEMM computes
+    l2_prefetch_share(ep.l2_next, ep.l2_next_bytes, blockIdx.x, gridDim.x, lane);
   } else if (warp >= 4) {
     const int wq = warp & 3;
     int acc = 0;
@@ -1154,7 +1171,21 @@ TilePlan pick_tiles(int M, int N, int K, bool allow192) {
 }
 
 int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long long ldb, int M, int N, int K,
-                int kind, int dh, const GemmEpi& ep, cudaStream_t stream, int bn) {
+                int kind, int dh, const GemmEpi& ep_in, cudaStream_t stream, int bn) {
+  // opt-in A/B knobs, measured no faster inside the C3 step (profiles/r2_l2_prefetch_ab.txt):
+  // RDKV_GEMM_WPOL=1 streams the weights evict-first, RDKV_L2_PREFETCH=1 lets the idle
+  // warp pull the next projection's weights into L2
+  static const int wpol = [] {
+    const char* e = std::getenv("RDKV_GEMM_WPOL");
+    return e && e[0] == '1' ? 1 : 0;
+  }();
+  static const bool l2pf = [] {
+    const char* e = std::getenv("RDKV_L2_PREFETCH");
+    return e && e[0] == '1';
+  }();
+  GemmEpi ep = ep_in;
+  ep.w_policy = wpol;
+  if (!l2pf) ep.l2_next = nullptr;
   if (M <= 0 || N <= 0) return 0;
   if (K <= 0 || K % BK != 0) return set_error(RDKV_ERR_ARG, "gemm: K=%d must be a positive multiple of 64", K);
   if (N % 32 != 0) return set_error(RDKV_ERR_ARG, "gemm: N=%d must be a multiple of 32", N);

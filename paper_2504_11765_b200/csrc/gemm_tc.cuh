@@ -61,6 +61,17 @@ struct GemmEpi {
   const float* ssq_in;
   int ssq_parts;
   int ssq_dim;
+  // L2 prefetch of the NEXT kernel's weights (126 MB of L2: the following projection's
+  // weights are pulled in by this kernel's idle warp while its own tiles compute, so a
+  // single-wave GEMM does not start on a cold weight stream).  Null = off; launch_gemm
+  // clears it unless RDKV_L2_PREFETCH=1 (measured no faster in the C3 step).
+  const void* l2_next;
+  long long l2_next_bytes;
+  // L2 policy of the weight (B) loads: 0 evict-last (like the activations), 1 evict-first
+  // (a weight tile is read by the M tiles of one wave at the same time, then never again
+  // in this kernel: streaming it evict-first keeps the prefetched next weights resident).
+  // Set by launch_gemm (RDKV_GEMM_WPOL, default 0).
+  int w_policy;
 };
 
 // True when launch_gemm will take the split-K path for this shape (small M).

@@ -349,6 +349,15 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
       ap.sk_mode = 1;
       attention_sk_carve(ap, ws.attn_sk, num_sms(), dh);
     }
+    // the attention kernel pulls the O projection's weights into L2 (its K/V stream is evict-first)
+    static const bool attn_l2pf = [] {
+      const char* e = std::getenv("RDKV_L2_PREFETCH");  // opt-in: measured no faster in the C3 step
+      return e && e[0] == '1';
+    }();
+    if (attn_l2pf) {
+      ap.l2_next = W(m, wb + 2);
+      ap.l2_next_bytes = (long long)d.hidden * qd * 2;
+    }
     if (b->layer_ready && b->layer_ready[l])  // layer-wise streaming: this layer's cached KV has landed
       CUDA_TRY(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(b->layer_ready[l]), 0));
     // the tcgen05 kernel is the product path: an unsupported shape is an error, not a
@@ -394,6 +403,11 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     }
     LAUNCH(RDKV_PROF_GU, 4.0 * T * d.ffn * d.hidden, launch_gemm(ssq_path ? ws.x : ws.h, d.hidden, W(m, wb + 4), d.hidden, T, 2 * d.ffn, d.hidden, EPI_SWIGLU, 0, eg, st));
     h_ready = down_fused && l + 1 < d.layers;
+    // the down projection pulls the next layer's QKV weights into L2
+    if (l + 1 < d.layers) {
+      er.l2_next = W(m, wb + RDKV_WEIGHTS_PER_LAYER + 1);
+      er.l2_next_bytes = (long long)qkv_n * d.hidden * 2;
+    }
     er.norm_gain = h_ready ? gain(wb + RDKV_WEIGHTS_PER_LAYER + 0) : nullptr;  // next layer's attention norm
     er.norm_out = h_ready ? ws.h : nullptr;
     if (tp) {

@@ -114,6 +114,26 @@ __device__ __forceinline__ void tma_load_3d_nohint(const CUtensorMap* m, uint64_
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// Bulk L2 prefetch of a global byte range (no smem, no barrier): `bytes` a multiple of 16,
+// `src` 16-B aligned.  Warms L2 for a LATER kernel (the next projection's weights).
+__device__ __forceinline__ void l2_prefetch_bulk(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(src)), "r"(bytes)
+               : "memory");
+}
+// This CTA's share of an L2 prefetch of [base, base + bytes), issued by the 32 lanes of
+// one otherwise idle warp in 64-KiB pieces.
+__device__ __forceinline__ void l2_prefetch_share(const void* base, long long bytes, int cta, int ctas, int lane) {
+  if (!base || bytes <= 0) return;
+  constexpr long long PIECE = 64 << 10;
+  const long long pieces = (bytes + PIECE - 1) / PIECE;
+  const long long p0 = pieces * cta / ctas, p1 = pieces * (cta + 1) / ctas;
+  for (long long q = p0 + lane; q < p1; q += 32) {
+    const long long off = q * PIECE;
+    const long long n = bytes - off < PIECE ? bytes - off : PIECE;
+    l2_prefetch_bulk(static_cast<const uint8_t*>(base) + off, (uint32_t)(n & ~15LL));
+  }
+}
+
 // L2 eviction-priority policies (createpolicy).
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;

@@ -43,5 +43,11 @@ print("producer: tile, before kv_empty wait, after (TMA issued) | iss0 qk(j-1) =
 for j in range(64):
     if not np.isnan(t[4, j, 0]):
         print(f"{j:3d} {t[4, j, 0]:9.0f} {t[4, j, 1]:9.0f}   {t[2, j - 1, 0] if j else float('nan'):9.0f}")
+print("issuer 0 per tile: loop top (prev PV issued) -> k_full(j+1) -> s_empty(j) -> QK(j+1) issued -> v_full(j) -> p_full(j) -> PV(j) issued")
+for j in range(1, 64):
+    r = [t[2, j - 1, 1], t[2, j, 2], t[2, j, 3], t[2, j, 0], t[2, j, 4], t[2, j, 5], t[2, j, 1]]
+    if all(np.isnan(r)):
+        continue
+    print(f"{j:3d} " + " ".join(f"{x:7.0f}" for x in r))
 Path("gpurun_out").mkdir(exist_ok=True)
 Path("gpurun_out/attn_tile_trace.json").write_text(json.dumps({"rows": [[None if np.isnan(x) else x for x in r] for r in rows]}))
