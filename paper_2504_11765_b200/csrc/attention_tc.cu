@@ -70,15 +70,20 @@ namespace {
 constexpr int ROWS = 128;
 constexpr int HALF = 64;  // rows per TMA box (= one KV block of the pool)
 
-template <int DH>
+template <int DH, bool PP = false>
 struct TcCfg {
   // key positions per tile: 128 at dh = 64; 64 at dh = 128, so S_i (BKV columns),
   // O_i (dh) and P_i (BKV / 2) of both Q tiles fit the 512 TMEM columns (448) and
   // Q_i.K^T of the next tile is issued while the softmax still works on this one
   // (with 128-key tiles at dh = 128, P_i had to live over S_i and each Q tile's
-  // S -> P -> P.V -> next S chain serialised: ~4.3k cycles per 128 keys)
-  static constexpr int BKV = DH == 128 ? 64 : 128;
-  static constexpr bool ALIAS = false;  // P_i over S_i (kept for reference; no shape needs it now)
+  // S -> P -> P.V -> next S chain serialised: ~4.3k cycles per 128 keys).
+  // PP (ping-pong, dh = 128): 128-key tiles with P_i over S_i, ONE issuer that interleaves
+  // the Q tiles (P.V_0, Q.K^T_0, P.V_1, Q.K^T_1, ...) so one tile's softmax runs while the
+  // tensor pipe works on the other tile; Q.K^T at N = 128 (N = 64 MMAs run at 2/3 rate,
+  // profiles/r2_l2_prefetch_ab.txt), separate K and V rings (K released after both
+  // Q.K^T, V after both P.V; K loaded two tiles ahead).
+  static constexpr int BKV = PP ? 128 : (DH == 128 ? 64 : 128);
+  static constexpr bool ALIAS = PP;  // P_i over S_i
 #ifndef RDKV_ATTN_ST64
 #define RDKV_ATTN_ST64 5
 #endif
@@ -86,28 +91,34 @@ struct TcCfg {
 #define RDKV_ATTN_ST128 4
 #endif
   static constexpr int STAGES = DH == 64 ? RDKV_ATTN_ST64 : RDKV_ATTN_ST128;
+  static constexpr int KST = PP ? 3 : STAGES;  // K stages (PP: own ring)
+  static constexpr int VST = PP ? 2 : STAGES;  // V stages (PP: own ring)
   static constexpr uint32_t QB = ROWS * DH * 2;    // one Q tile
   static constexpr uint32_t KB = BKV * DH * 2;     // one K (or V) tile
   static constexpr uint32_t OFF_Q = 0;             // [2 Q tiles]
   static constexpr uint32_t OFF_K = OFF_Q + 2 * QB;
-  static constexpr uint32_t OFF_V = OFF_K + STAGES * KB;
-  static constexpr uint32_t OFF_RED = OFF_V + STAGES * KB;  // [2 parity][2 Q tiles][2 halves][128 rows] fp32
-  static constexpr uint32_t OFF_BAR = OFF_RED + 2 * 2 * 2 * ROWS * 4;
-  static constexpr uint32_t OFF_MISC = (OFF_BAR + 8 * (4 + 3 * STAGES + 8) + 15) / 16 * 16;  // TMEM base, segment count, W
+  static constexpr uint32_t OFF_V = OFF_K + KST * KB;
+  // [2 parity][2 Q tiles][2 halves][128 rows] fp32 (SPL = 2 only; PP runs SPL = 1)
+  static constexpr uint32_t OFF_RED = OFF_V + VST * KB;
+  static constexpr uint32_t OFF_BAR = OFF_RED + (PP ? 0 : 2 * 2 * 2 * ROWS * 4);
+  static constexpr uint32_t N_BARS = 4 + 2 * KST + 2 * VST + 8;
+  static constexpr uint32_t OFF_MISC = (OFF_BAR + 8 * N_BARS + 15) / 16 * 16;  // TMEM base, segment count, W
   static constexpr uint32_t OFF_SEG = OFF_MISC + 16;                        // stream-K segments (int4)
   static constexpr uint32_t OFF_SEQ = OFF_SEG + 16 * 512;                   // stream-K: [3][512] seq start/new/cached
   // row sums on the tensor cores (dh = 128, where TMEM has room): L_i += P_i . ones, with a
   // constant [16 x BKV] bf16 ones tile as the K-major B operand (16 columns of L_i, all equal)
   static constexpr bool LSUM = RDKV_ATTN_LSUM && DH == 128 && !ALIAS;
   static constexpr uint32_t OFF_ONES = (OFF_SEQ + 3 * 4 * 512 + 1023) / 1024 * 1024;
-  static constexpr size_t SMEM = LSUM ? OFF_ONES + 16 * 128 : OFF_SEQ + 3 * 4 * 512;
+  static constexpr size_t SMEM = PP ? OFF_MISC + 16 : LSUM ? OFF_ONES + 16 * 128 : OFF_SEQ + 3 * 4 * 512;
+  static_assert(SMEM <= 232448, "attention smem exceeds 227 KB");
   // TMEM columns
-  static constexpr uint32_t COL_S = 0;                          // S_i at 128 i
-  static constexpr uint32_t COL_O = 2 * BKV;                    // O_i at 256 + DH i
-  static constexpr uint32_t COL_P = ALIAS ? 0 : 2 * BKV + 2 * DH;  // P_i at COL_P + (ALIAS ? 128 : 64) i
+  static constexpr uint32_t COL_S = 0;                          // S_i at BKV i
+  static constexpr uint32_t COL_O = 2 * BKV;                    // O_i at 2 BKV + DH i
+  static constexpr uint32_t COL_P = ALIAS ? 0 : 2 * BKV + 2 * DH;  // P_i at COL_P + (ALIAS ? BKV : BKV / 2) i
   static constexpr uint32_t P_STRIDE = ALIAS ? BKV : BKV / 2;
   static constexpr uint32_t COL_L = COL_P + 2 * P_STRIDE;     // L_i at COL_L + 16 i (LSUM)
   static_assert(!LSUM || COL_L + 32 <= 512, "TMEM: L columns do not fit");
+  static_assert(COL_O + 2 * DH <= 512, "TMEM: S and O do not fit");
 };
 
 // SPL softmax warps per query row (each takes BKV / SPL keys of a tile):
@@ -159,6 +170,9 @@ constexpr int EMU_OF_8 = RDKV_ATTN_EMU;  // exp2 of this many of every 8 score g
 
 #ifndef RDKV_ATTN_PF
 #define RDKV_ATTN_PF 0  // TMA producer L2 prefetch distance in tiles (0: off; 2-8 measured no faster)
+#endif
+#ifndef RDKV_ATTN_PPF
+#define RDKV_ATTN_PPF 0  // ping-pong producer: L2 prefetch distance in tiles ahead of the K stream (2-8 slower)
 #endif
 #ifndef RDKV_ATTN_SPIN
 #define RDKV_ATTN_SPIN 1
@@ -232,13 +246,14 @@ __device__ __forceinline__ void st_release_gpu(int* p, int v) {
 // first tiles (SEG_HEAD, always that CTA's last segment): it merges the (m, l, O)
 // partials that the following CTAs wrote as their FIRST segment (SEG_PART, published
 // with a release flag before they do anything else, so the waits cannot deadlock).
-template <int DH, int SPL, bool SK>
+template <int DH, int SPL, bool SK, bool PP = false>
 __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                    const __grid_constant__ CUtensorMap tmQ, AttnParams p) {
-  using C = TcCfg<DH>;
+  using C = TcCfg<DH, PP>;
   using R = Roles<SPL>;
   static_assert(!SK || SPL == 1, "stream-K runs one softmax warp per row");
+  static_assert(!PP || (SPL == 1 && !SK), "ping-pong runs one softmax warp per row, one segment per CTA");
   constexpr int NS = R::NS;
   constexpr int BKV = C::BKV;
   constexpr int NH = BKV / HALF;  // TMA boxes (KV blocks) per tile
@@ -253,10 +268,12 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bars + 0;             // [2] per Q tile: Q_i staged
   uint64_t* q_empty = bars + 2;            // [2] per Q tile: the segment's last Q_i.K^T retired
-  uint64_t* k_full = bars + 4;             // [ST]
-  uint64_t* v_full = k_full + ST;          // [ST]
-  uint64_t* kv_empty = v_full + ST;        // [ST]
-  uint64_t* s_full = kv_empty + ST;        // [2] per Q tile: S_i = Q_i.K^T landed
+  constexpr int KST = C::KST, VST = C::VST;
+  uint64_t* k_full = bars + 4;             // [KST]
+  uint64_t* v_full = k_full + KST;         // [VST]
+  uint64_t* kv_empty = v_full + VST;       // [KST] stage free (PP: K consumed by both Q.K^T)
+  uint64_t* v_empty = kv_empty + KST;      // [VST] PP only: V consumed by both P.V
+  uint64_t* s_full = v_empty + (PP ? VST : 0);  // [2] per Q tile: S_i = Q_i.K^T landed
   uint64_t* s_empty = s_full + 2;          // [2] S_i read into registers
   uint64_t* p_full = s_empty + 2;          // [2] P_i written (and O_i rescaled)
   uint64_t* o_done = p_full + 2;           // [2] O_i += P_i.V retired (P_i free)
@@ -317,10 +334,21 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
         mbar_init(&q_full[i], 1);
         mbar_init(&q_empty[i], 1);
       }
-      for (int i = 0; i < ST; ++i) {
-        mbar_init(&k_full[i], 1);
-        mbar_init(&v_full[i], 1);
-        mbar_init(&kv_empty[i], 2);  // both Q tiles' issuers release every stage
+      if constexpr (PP) {  // one issuer commits each release once
+        for (int i = 0; i < KST; ++i) {
+          mbar_init(&k_full[i], 1);
+          mbar_init(&kv_empty[i], 1);
+        }
+        for (int i = 0; i < VST; ++i) {
+          mbar_init(&v_full[i], 1);
+          mbar_init(&v_empty[i], 1);
+        }
+      } else {
+        for (int i = 0; i < ST; ++i) {
+          mbar_init(&k_full[i], 1);
+          mbar_init(&v_full[i], 1);
+          mbar_init(&kv_empty[i], 2);  // both Q tiles' issuers release every stage
+        }
       }
       for (int i = 0; i < 2; ++i) {
         mbar_init(&s_full[i], 1);
@@ -418,6 +446,98 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
   // the TMA / MMA warpgroup gives its registers up
   if (warp >= NS) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R::REG_AUX) : "memory");
   if (warp == NS) {
+    if constexpr (PP) {
+      // ---------------------------------------------------------- TMA producer (ping-pong)
+      // K runs two tiles ahead of V: order K(0), K(1), then V(j), K(j + 2).  Each stream keeps
+      // a warp-wide cache of 32 tiles' block-table rows (lane l holds tile base + l).
+      const int4 sg = seg0;
+      const Unit u = unit_at(sg.x);
+      const long long row0 = (long long)u.kvh * (p.head_stride / DH);
+      const int* bt = p.block_table + (long long)u.s * p.bt_stride;
+      const uint64_t pol_kv = policy_evict_first();
+      auto fetch = [&](int base, int (&cache)[NH]) {
+        const int j = base + lane;
+        if (j < sg.z) {
+#pragma unroll
+          for (int h = 0; h < NH; ++h) {
+            int pos = j * BKV + h * HALF;
+            if (pos >= u.kv_len) pos = j * BKV;  // masked half: any valid, finite block
+            cache[h] = (int)(row0 + (long long)bt[pos / p.block_size] * p.block_size + pos % p.block_size);
+          }
+        }
+      };
+      int kbase = -64, vbase = -64, kc[NH] = {}, vc[NH] = {};
+      auto load = [&](bool isk, int j) {  // whole warp (uniform j)
+        int& base = isk ? kbase : vbase;
+        int(&cache)[NH] = isk ? kc : vc;
+        if (j < base || j >= base + 32) {
+          base = j;
+          fetch(base, cache);
+        }
+        int rows[NH];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) rows[h] = __shfl_sync(0xffffffffu, cache[h], j - base);
+        if (lane == 0) {
+          const int jl = j - sg.y, ns = isk ? KST : VST, st = jl % ns;
+          mbar_wait_sleep(isk ? &kv_empty[st] : &v_empty[st], ((jl / ns) & 1) ^ 1);
+          uint64_t* bar = isk ? &k_full[st] : &v_full[st];
+          mbar_arrive_expect_tx(bar, C::KB);
+          const CUtensorMap* tm = isk ? &tmK : &tmV;
+          uint8_t* dst = smem + (isk ? C::OFF_K : C::OFF_V) + st * C::KB;
+#pragma unroll
+          for (int c = 0; c < DH / 64; ++c)
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+              if (p.kv_evict_first)
+                tma_load_2d(tm, bar, dst + c * (BKV * 128) + h * (HALF * 128), c * 64, rows[h], pol_kv);
+              else
+                tma_load_2d_nohint(tm, bar, dst + c * (BKV * 128) + h * (HALF * 128), c * 64, rows[h]);
+            }
+        }
+        __syncwarp();
+      };
+      // the K/V stream outruns the smem rings' lead (~5k cycles of DRAM latency under load at
+      // 3 + 2 stages): warm L2 with K and V of tile j + RDKV_ATTN_PPF when K(j) is requested
+      auto prefetch = [&](int j) {
+        if (RDKV_ATTN_PPF <= 0 || j >= sg.z) return;
+        int pcache[NH];
+        // rows of tile j: this lane's cache covers it only if j is in the K window
+        if (j >= kbase && j < kbase + 32) {
+#pragma unroll
+          for (int h = 0; h < NH; ++h) pcache[h] = __shfl_sync(0xffffffffu, kc[h], j - kbase);
+        } else {
+#pragma unroll
+          for (int h = 0; h < NH; ++h) {
+            int pos = j * BKV + h * HALF;
+            if (pos >= u.kv_len) pos = j * BKV;
+            pcache[h] = (int)(row0 + (long long)bt[pos / p.block_size] * p.block_size + pos % p.block_size);
+          }
+        }
+        if (lane == 0) {
+#pragma unroll
+          for (int h = 0; h < NH; ++h) {
+            if (j * BKV + h * HALF >= u.kv_len) continue;
+#pragma unroll
+            for (int c = 0; c < DH / 64; ++c) {
+              tma_prefetch_2d(&tmK, c * 64, pcache[h]);
+              tma_prefetch_2d(&tmV, c * 64, pcache[h]);
+            }
+          }
+        }
+        __syncwarp();
+      };
+      int kj = sg.y;
+      for (int j = sg.y; j < sg.z && j < sg.y + RDKV_ATTN_PPF; ++j) prefetch(j + 2);
+      for (; kj < sg.z && kj < sg.y + 2; ++kj) load(true, kj);
+      for (int j = sg.y; j < sg.z; ++j) {
+        load(false, j);
+        if (kj < sg.z) {
+          load(true, kj);
+          prefetch(kj + RDKV_ATTN_PPF);
+          ++kj;
+        }
+      }
+    } else {
     // ------------------------------------------------------------ TMA producer
     // The whole warp walks the tiles: every 32 tiles each lane resolves one
     // tile's two block-table rows (32 global loads in parallel instead of a
@@ -490,7 +610,67 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
         __syncwarp();
       }
     }
+    }
   } else if (warp == NS + 1 || warp == NS + 2) {
+    if constexpr (PP) {
+      // ---------------------------------------------------------- MMA issuer (ping-pong)
+      // One thread issues for both Q tiles in the order P.V_0(j), Q.K^T_0(j+1), P.V_1(j),
+      // Q.K^T_1(j+1): the tensor pipe executes in issue order, so Q.K^T_i(j+1) overwrites
+      // S_i (= P_i) only after P.V_i(j) has read P_i, and S_i(j+1) landing tells the softmax
+      // that O_i is idle.  While softmax 0 works on S_0(j) the pipe runs tile 1's P.V and
+      // Q.K^T and vice versa.
+      if (warp == NS + 1 && lane == 0) {
+        constexpr uint32_t idesc_qk = idesc_bf16_f32(ROWS, BKV);
+        constexpr uint32_t idesc_pv = idesc_bf16_f32(ROWS, DH) | (1u << 16);  // B (V) is MN-major
+        const int4 sg = seg0;
+        const int nt = sg.z - sg.y;
+        const int nq = unit_at(sg.x).n_q;
+        auto qk = [&](int i, int jl) {  // S_i = Q_i . K(jl)^T
+          const uint32_t qa = sb + C::OFF_Q + i * C::QB;
+          const uint32_t ka = sb + C::OFF_K + (jl % KST) * C::KB;
+          const uint32_t tS = tmem + C::COL_S + i * BKV;
+#pragma unroll
+          for (int kk = 0; kk < DH / 16; ++kk) {
+            const uint32_t sub = (kk & 3) * 32;
+            umma_bf16(tS, desc_k(qa + (kk >> 2) * (ROWS * 128) + sub), desc_k(ka + (kk >> 2) * (BKV * 128) + sub),
+                      idesc_qk, kk > 0 ? 1u : 0u);
+          }
+          umma_commit(&s_full[i]);
+          if (jl + 1 == nt) umma_commit(&q_empty[i]);  // the segment's last Q_i.K^T
+        };
+        if (nt > 0 && nq > 0) {
+          for (int i = 0; i < nq; ++i) issuer_wait(&q_full[i], 0);
+          issuer_wait(&k_full[0], 0);
+          tc_fence_after();
+          for (int i = 0; i < nq; ++i) qk(i, 0);
+          umma_commit(&kv_empty[0]);
+          for (int jl = 0; jl < nt; ++jl) {
+            const int vs = jl % VST;
+            const uint32_t va = sb + C::OFF_V + vs * C::KB;
+            for (int i = 0; i < nq; ++i) {
+              issuer_wait(&p_full[i], jl & 1);
+              if (i == 0) issuer_wait(&v_full[vs], (jl / VST) & 1);
+              TRACE(2 + i, jl, 4);
+              tc_fence_after();
+              const uint32_t tO = tmem + C::COL_O + i * DH, tP = tmem + C::COL_P + i * C::P_STRIDE;
+#pragma unroll
+              for (int kk = 0; kk < BKV / 16; ++kk)  // O_i (+)= P_i . V(jl), P_i (keys 16kk..) at column 8kk
+                umma_bf16_ts(tO, tP + kk * 8, desc_mn(va + kk * 2048, BKV * 128), idesc_pv, (jl > 0 || kk > 0) ? 1u : 0u);
+              umma_commit(&o_done[i]);
+              TRACE(2 + i, jl, 1);
+              if (jl + 1 < nt) {
+                if (i == 0) issuer_wait(&k_full[(jl + 1) % KST], ((jl + 1) / KST) & 1);
+                tc_fence_after();
+                qk(i, jl + 1);
+                TRACE(2 + i, jl, 0);
+              }
+            }
+            umma_commit(&v_empty[vs]);
+            if (jl + 1 < nt) umma_commit(&kv_empty[(jl + 1) % KST]);
+          }
+        }
+      }
+    } else {
     // ------------------------------------------------------------ MMA issuers
     // one issuing thread per Q tile, so neither softmax warpgroup ever waits on
     // the other's progress (their exp2 phases drift apart and overlap)
@@ -576,6 +756,7 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
           }
         }
       }
+    }
     }
   } else if (warp == NS + 3) {
     // ------------------------------------------------------------ Q loader
@@ -673,7 +854,7 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
           tmem_ld_wait();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&s_empty[i]);
+          if (!PP && lane == 0) mbar_arrive(&s_empty[i]);
           const int lim = qpos - (sg.y + j) * BKV - h * KH;  // key e of this half visible iff e <= lim
           if (lim < KH - 1) {
 #pragma unroll
@@ -724,7 +905,7 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
           }
           // P_i (and O_i) are free once P_i.V(j-1) has retired (implied by s_full when P aliases S)
           if (j + 1 < nt) TRACE(i, ti, 3);
-          if (j > 0) {
+          if (!PP && j > 0) {  // PP: S_i(j) landing already implies P.V_i(j-1) retired
             mbar_wait(&o_done[i], (ti - 1) & 1);
             tc_fence_after();
           }
@@ -925,20 +1106,20 @@ __global__ void __launch_bounds__(256) attn_split_combine_kernel(AttnParams p) {
   for (int e = 0; e < PER; ++e) dst[lane + 32 * e] = __float2bfloat16(acc[e] * inv);
 }
 
-template <int DH, int SPL, bool SK>
+template <int DH, int SPL, bool SK, bool PP = false>
 int set_smem_attr() {
   static bool attr = false;
   if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(attn_tc_kernel<DH, SPL, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)TcCfg<DH>::SMEM));
+    CUDA_TRY(cudaFuncSetAttribute(attn_tc_kernel<DH, SPL, SK, PP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)TcCfg<DH, PP>::SMEM));
     attr = true;
   }
   return 0;
 }
 
-template <int DH, int SPL>
+template <int DH, int SPL, bool PP = false>
 int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
-  using C = TcCfg<DH>;
+  using C = TcCfg<DH, PP>;
   // plane view: rows = hkv * slots, cols = dh
   const long long rows = (long long)p.hkv * (p.head_stride / DH);
   CUtensorMap tk, tv;
@@ -958,7 +1139,7 @@ int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
   const int max_tiles = (p.max_ctx + C::BKV - 1) / C::BKV;
   // stream-K (opt-in: p.sk_mode) when the unit grid is at least half a wave; measured
   // slower than one CTA per unit on the C2/C3 shapes (profiles/r1_attn_experiments.md)
-  if constexpr (SPL == 1) {
+  if constexpr (SPL == 1 && !PP) {
     if (p.sk_mode && p.sk_o && p.sk_ctas >= sms && ctas * 2 > sms && ctas <= SK_MAXSEG) {
       RDKV_TRY((set_smem_attr<DH, SPL, true>()));
       CUDA_TRY(launch_k(attn_tc_kernel<DH, SPL, true>, dim3(sms), dim3(Roles<SPL>::THREADS), C::SMEM, st, tk, tv, tq, q));
@@ -983,13 +1164,13 @@ int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
   // unit, measured 77 -> 103 us with 5-tile splits, a 41-tile dh=128 batch 212 -> 189 us)
   if (tail_env && p.split_o && ctas > sms && last > 0.0 && last < 0.9 && s_a >= 1 && s_a < n_seqs &&
       max_tiles >= 8 * KT && (size_t)KT * p.n_tokens * p.hq * (DH * 4 + 8) <= p.split_bytes) {
-    RDKV_TRY((set_smem_attr<DH, SPL, false>()));
+    RDKV_TRY((set_smem_attr<DH, SPL, false, PP>()));
     AttnParams b = q;
     b.seq_off = s_a;
     b.kv_splits = KT;
     b.tail_ctas = s_a * ups;
     const int grid = s_a * ups + (n_seqs - s_a) * ups * KT;
-    CUDA_TRY(launch_k(attn_tc_kernel<DH, SPL, false>, dim3(grid), dim3(Roles<SPL>::THREADS), C::SMEM, st, tk, tv, tq, b));
+    CUDA_TRY(launch_k(attn_tc_kernel<DH, SPL, false, PP>, dim3(grid), dim3(Roles<SPL>::THREADS), C::SMEM, st, tk, tv, tq, b));
     CUDA_TRY(launch_k(attn_split_combine_kernel<DH>, dim3(p.n_tokens, (p.hq + 7) / 8), dim3(256), 0, st, b));
     CUDA_TRY(cudaGetLastError());
     return 0;
@@ -1002,9 +1183,9 @@ int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
     k = k < 16 ? k : 16;
     if (k >= 2 && (size_t)k * p.n_tokens * p.hq * (DH * 4 + 8) <= p.split_bytes) q.kv_splits = k;
   }
-  RDKV_TRY((set_smem_attr<DH, SPL, false>()));
+  RDKV_TRY((set_smem_attr<DH, SPL, false, PP>()));
   dim3 grid(qblocks * q.kv_splits, p.hkv, n_seqs);
-  CUDA_TRY(launch_k(attn_tc_kernel<DH, SPL, false>, grid, dim3(Roles<SPL>::THREADS), C::SMEM, st, tk, tv, tq, q));
+  CUDA_TRY(launch_k(attn_tc_kernel<DH, SPL, false, PP>, grid, dim3(Roles<SPL>::THREADS), C::SMEM, st, tk, tv, tq, q));
   CUDA_TRY(cudaGetLastError());
   if (q.kv_splits > 1) {
     CUDA_TRY(launch_k(attn_split_combine_kernel<DH>, dim3(p.n_tokens, (p.hq + 7) / 8), dim3(256), 0, st, q));
@@ -1039,6 +1220,15 @@ int launch_attention_tc(const AttnParams& p, int head_dim, int n_seqs, int max_n
     return e && e[0] == '2' ? 2 : 1;
   }();
   if (head_dim == 64) return spl == 2 ? launch_tc<64, 2>(p, n_seqs, max_new, st) : launch_tc<64, 1>(p, n_seqs, max_new, st);
+  // RDKV_ATTN_PP=1: the ping-pong schedule (opt-in: measured slower, 102-107 vs 98-99 us at
+  // the C3 shape and 98 vs 93 us with every K/V tile L2-hot — one softmax warp per SMSP at a
+  // time needs ~1510 cycles per 128 keys, profiles/r2_attn_experiments.md)
+  static const bool pp = [] {
+    const char* e = std::getenv("RDKV_ATTN_PP");
+    return e && e[0] == '1';
+  }();
+  // stream-K (opt-in) runs the two-issuer schedule
+  if (pp && !p.sk_mode) return launch_tc<128, 1, true>(p, n_seqs, max_new, st);
   return launch_tc<128, 1>(p, n_seqs, max_new, st);  // 64-key tiles at dh = 128: one softmax warp per row
 }
 

@@ -28,12 +28,16 @@ def main():
     ap.add_argument("--dh", type=int, default=64)
     ap.add_argument("--impl", type=int, default=0)
     ap.add_argument("--reps", type=int, default=50)
+    ap.add_argument("--same-block", action="store_true",
+                    help="timing probe: every KV tile reads block 0 (L2-hot; outputs meaningless)")
     a = ap.parse_args()
     c = _case([a.new] * a.seqs, [a.cached] * a.seqs, a.hq, a.hkv, a.dh, shuffle=True)
     dev = "cuda"
     q, kp, vp = c["q"].to(dev), c["kp"].to(dev), c["vp"].to(dev)
     o = torch.empty_like(q)
     bt = c["bt"].to(dev)
+    if a.same_block:
+        bt.zero_()
     st, nn, nc = c["start"].to(dev), c["n_new"].to(dev), c["n_cached"].to(dev)
     lib = _lib.lib()
     nb = lib.rdkv_attention_scratch_bytes(c["T"], c["hq"], c["dh"])
