@@ -68,6 +68,15 @@ class RuntimeConfig:
     persist: str = "all"                # generated blobs put in the store: "all" prefixes | "composite" | "none"
     token_seed: int = 0
     idle_sleep_s: float = 2e-4
+    # Cost-aware dispatch (opt-in deviation from the reference's "longest cached prefix
+    # wins", sim.py:414-431): a prefix found only on DISK is used only if reading it is
+    # predicted faster than recomputing its tokens; otherwise the next-best non-disk
+    # prefix (or raw prefill) is served and the disk copy is left alone.  On a B200 an
+    # 8B composite of 5120 tokens reads in ~190 ms from a ~3.4 GB/s disk but prefills in
+    # ~55 ms (bench ttft_ms.cold_disk vs full_prefill), so the reference rule loses there.
+    cost_aware: bool = False
+    disk_gbps: float = 3.4              # sustained cold read of the shared store (bench / disk probe)
+    prefill_s_per_token: float = 1.1e-5 # measured full-prefill cost per prefix token on this GPU
 
     def __post_init__(self) -> None:
         if self.persist not in ("all", "composite", "none"):
@@ -310,6 +319,11 @@ class Instance:
             srcs = [self._source(key) for key in keys]
             best = max((j for j, s in enumerate(srcs, 1) if s is not None), default=0)
             source = srcs[best - 1] if best else "miss"
+            if cfg.cost_aware and source == "disk" and self._disk_loses(sum(toks[:best])):
+                self.cp.add(Counter.DISK_SKIPPED)
+                best = max((j for j, s in enumerate(srcs[: best - 1], 1) if s in ("hbm", "peer", "memory")),
+                           default=0)
+                source = srcs[best - 1] if best else "miss"
             q = query_tokens(qid, qn, spec.vocab, cfg.token_seed)
             if source == "peer" and not self._peer_fetch(keys[best - 1]):
                 # the holder evicted it meanwhile: next-best source for the same prefix
@@ -344,6 +358,12 @@ class Instance:
             self.results.append(QueryResult(index, qid, self.rank, arrival, t_dispatch, t_first, best, source,
                                             origins, len(batch), int(tok)))
             self.cp.qstate_cas(index, QState.DISPATCHED, QState.DONE)
+
+    def _disk_loses(self, n_tokens: int) -> bool:
+        """Cost-aware dispatch: is reading ``n_tokens`` of cached KV from disk predicted
+        slower than prefilling them (kv_load vs prefill terms of costs.py:125-144)?"""
+        load = n_tokens * self.eng.spec.kv_bytes_per_token() / (self.cfg.disk_gbps * 1e9)
+        return load > n_tokens * self.cfg.prefill_s_per_token
 
     # ------------------------------------------------------------ queue-time generation
     def _gen_loop(self) -> None:

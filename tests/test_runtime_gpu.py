@@ -49,12 +49,19 @@ def test_single_instance_prefetch_and_reuse():
 
     spec = get_spec("gqa-small-64")
     k = 3
-    eng = Engine(spec, seed=0, pool_tokens=32768, device_cache_bytes=256 << 20)
     items = _items(k=k)
+    cfg = RuntimeConfig(k=k, threshold=0.0, max_batch=4, persist="all")
+    # throwaway pass on its own engine and store: the first launches of every kernel shape
+    # in a fresh process (module load, tensor-map setup) would otherwise delay try 1's
+    # generations past try 2's dispatches on a freshly leased box
+    with tempfile.TemporaryDirectory() as root:
+        warm = Engine(spec, seed=0, pool_tokens=32768, device_cache_bytes=256 << 20)
+        serve(warm, KvStore(root, memory_capacity_bytes=0), cfg, items[:8], rate=400.0, tries=1)
+        del warm
+    eng = Engine(spec, seed=0, pool_tokens=32768, device_cache_bytes=256 << 20)
     expected = _expected_tokens(eng, items, k)
     with tempfile.TemporaryDirectory() as root:
         store = KvStore(root, memory_capacity_bytes=0)
-        cfg = RuntimeConfig(k=k, threshold=0.0, max_batch=4, persist="all")
         out = serve(eng, store, cfg, items, rate=400.0, tries=2)
         rep, res = out["summary"], out["results"]
         assert rep["queries"] == 2 * len(items)
@@ -177,3 +184,39 @@ def test_runtime_store_path_oplog_replays():
         assert all(got[f] == v for f, v in want.items()), (got, want)
         gets = [op for op in store.oplog if op[0] == "get"]
         assert len(gets) >= len(out["access_log"]) > 0
+
+
+@pytest.mark.parametrize("disk_gbps,expect_disk", [(1e-6, False), (1e6, True)])
+def test_cost_aware_dispatch(disk_gbps, expect_disk):
+    """Opt-in cost-aware dispatch: composites that live only on disk are read when the
+    predicted read beats recomputing their tokens, else recomputed (DISK_SKIPPED), and
+    the first tokens are the same either way."""
+    from paper_2504_11765_b200.engine import Engine
+    from paper_2504_11765_b200.generator import KvGenerator
+    from paper_2504_11765_b200.model import get_spec
+    from paper_2504_11765_b200.runtime import RuntimeConfig, serve
+    from paper_2504_11765_b200.store import KvKey, KvStore
+
+    spec = get_spec("gqa-small-64")
+    k = 3
+    eng = Engine(spec, seed=0, pool_tokens=32768, device_cache_bytes=0)
+    items = _items(n=12, k=k)
+    expected = _expected_tokens(eng, items, k)
+    gen = KvGenerator(eng, keep_on_device=False)
+    with tempfile.TemporaryDirectory() as root:
+        store = KvStore(root, memory_capacity_bytes=0)           # disk only (the paper's shared setting)
+        for it in items:
+            key = KvKey(spec.profile().model_hash, tuple(it.doc_ids[:k]))
+            if store.contains(key).name == "ABSENT":
+                store.put(key, gen.generate(it.doc_ids[:k], it.doc_tokens[:k]))
+        cfg = RuntimeConfig(k=k, threshold=10.0, prefetch=False, max_batch=4, cost_aware=True,
+                            disk_gbps=disk_gbps, prefill_s_per_token=1e-5)
+        out = serve(eng, store, cfg, items, rate=200.0, tries=1)
+        rep = out["summary"]
+        assert rep["queries"] == len(items)
+        if expect_disk:
+            assert rep["sources"].get("disk", 0) == len(items) and rep["counters"]["disk_skipped"] == 0
+        else:
+            assert rep["sources"].get("miss", 0) == len(items)
+            assert rep["counters"]["disk_skipped"] == len(items)
+        _check_tokens(out["results"], expected)
