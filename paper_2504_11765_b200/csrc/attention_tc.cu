@@ -98,9 +98,11 @@ struct TcCfg {
   static constexpr uint32_t OFF_Q = 0;             // [2 Q tiles]
   static constexpr uint32_t OFF_K = OFF_Q + 2 * QB;
   static constexpr uint32_t OFF_V = OFF_K + KST * KB;
-  // [2 parity][2 Q tiles][2 halves][128 rows] fp32 (SPL = 2 only; PP runs SPL = 1)
+  // row max / sum exchange of the two halves of a row (SPL = 2): [parity][2 Q tiles][2
+  // halves][128 rows] fp32; PP has room for one parity only (a second barrier orders reuse)
+  static constexpr int RED_PAR = PP ? 1 : 2;
   static constexpr uint32_t OFF_RED = OFF_V + VST * KB;
-  static constexpr uint32_t OFF_BAR = OFF_RED + (PP ? 0 : 2 * 2 * 2 * ROWS * 4);
+  static constexpr uint32_t OFF_BAR = OFF_RED + RED_PAR * 2 * 2 * ROWS * 4;
   static constexpr uint32_t N_BARS = 4 + 2 * KST + 2 * VST + 8;
   static constexpr uint32_t OFF_MISC = (OFF_BAR + 8 * N_BARS + 15) / 16 * 16;  // TMEM base, segment count, W
   static constexpr uint32_t OFF_SEG = OFF_MISC + 16;                        // stream-K segments (int4)
@@ -253,7 +255,7 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
   using C = TcCfg<DH, PP>;
   using R = Roles<SPL>;
   static_assert(!SK || SPL == 1, "stream-K runs one softmax warp per row");
-  static_assert(!PP || (SPL == 1 && !SK), "ping-pong runs one softmax warp per row, one segment per CTA");
+  static_assert(!PP || !SK, "ping-pong runs one segment per CTA");
   constexpr int NS = R::NS;
   constexpr int BKV = C::BKV;
   constexpr int NH = BKV / HALF;  // TMA boxes (KV blocks) per tile
@@ -654,8 +656,10 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
               tc_fence_after();
               const uint32_t tO = tmem + C::COL_O + i * DH, tP = tmem + C::COL_P + i * C::P_STRIDE;
 #pragma unroll
-              for (int kk = 0; kk < BKV / 16; ++kk)  // O_i (+)= P_i . V(jl), P_i (keys 16kk..) at column 8kk
-                umma_bf16_ts(tO, tP + kk * 8, desc_mn(va + kk * 2048, BKV * 128), idesc_pv, (jl > 0 || kk > 0) ? 1u : 0u);
+              for (int kk = 0; kk < BKV / 16; ++kk) {  // O_i (+)= P_i . V(jl); each key half's P inside its S columns
+                const uint32_t pcol = (kk / (KH / 16)) * KH + (kk % (KH / 16)) * 8;
+                umma_bf16_ts(tO, tP + pcol, desc_mn(va + kk * 2048, BKV * 128), idesc_pv, (jl > 0 || kk > 0) ? 1u : 0u);
+              }
               umma_commit(&o_done[i]);
               TRACE(2 + i, jl, 1);
               if (jl + 1 < nt) {
@@ -814,9 +818,11 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
       if constexpr (SPL == 1) {
         return v;
       } else {
-        red[((parity * 2 + i) * 2 + h) * ROWS + r] = v;
+        const int pa = C::RED_PAR == 2 ? parity : 0;
+        red[((pa * 2 + i) * 2 + h) * ROWS + r] = v;
         pair_sync();
-        const float o = red[((parity * 2 + i) * 2 + (h ^ 1)) * ROWS + r];
+        const float o = red[((pa * 2 + i) * 2 + (h ^ 1)) * ROWS + r];
+        if constexpr (C::RED_PAR == 1) pair_sync();  // both read before either writes the slot again
         return use_max ? fmaxf(v, o) : v + o;
       }
     };
@@ -1227,8 +1233,9 @@ int launch_attention_tc(const AttnParams& p, int head_dim, int n_seqs, int max_n
     const char* e = std::getenv("RDKV_ATTN_PP");
     return e && e[0] == '1';
   }();
-  // stream-K (opt-in) runs the two-issuer schedule
-  if (pp && !p.sk_mode) return launch_tc<128, 1, true>(p, n_seqs, max_new, st);
+  // stream-K (opt-in) runs the two-issuer schedule; RDKV_ATTN_SPL=2: two softmax warps per row
+  if (pp && !p.sk_mode) return spl == 2 ? launch_tc<128, 2, true>(p, n_seqs, max_new, st)
+                                        : launch_tc<128, 1, true>(p, n_seqs, max_new, st);
   return launch_tc<128, 1>(p, n_seqs, max_new, st);  // 64-key tiles at dh = 128: one softmax warp per row
 }
 
