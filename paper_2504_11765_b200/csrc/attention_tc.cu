@@ -173,6 +173,9 @@ constexpr int EMU_OF_8 = RDKV_ATTN_EMU;  // exp2 of this many of every 8 score g
 #ifndef RDKV_ATTN_PF
 #define RDKV_ATTN_PF 0  // TMA producer L2 prefetch distance in tiles (0: off; 2-8 measured no faster)
 #endif
+#ifndef RDKV_ATTN_SPLITKV
+#define RDKV_ATTN_SPLITKV 0  // 1: separate K / V stage releases in the two-issuer schedule (measured: C3 98.5 vs 96.3 us, C2 77.5 vs 78.3)
+#endif
 #ifndef RDKV_ATTN_PPF
 #define RDKV_ATTN_PPF 0  // ping-pong producer: L2 prefetch distance in tiles ahead of the K stream (2-8 slower)
 #endif
@@ -271,11 +274,15 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
   uint64_t* q_full = bars + 0;             // [2] per Q tile: Q_i staged
   uint64_t* q_empty = bars + 2;            // [2] per Q tile: the segment's last Q_i.K^T retired
   constexpr int KST = C::KST, VST = C::VST;
+  // separate K and V releases: a K stage frees after both Q.K^T, a V stage after both P.V,
+  // and the producer runs K LEAD tiles ahead of V (stream-K keeps the shared stages)
+  constexpr bool SPLIT = PP || (RDKV_ATTN_SPLITKV && !SK);
+  constexpr int LEAD = PP ? 2 : 1;
   uint64_t* k_full = bars + 4;             // [KST]
   uint64_t* v_full = k_full + KST;         // [VST]
   uint64_t* kv_empty = v_full + VST;       // [KST] stage free (PP: K consumed by both Q.K^T)
   uint64_t* v_empty = kv_empty + KST;      // [VST] PP only: V consumed by both P.V
-  uint64_t* s_full = v_empty + (PP ? VST : 0);  // [2] per Q tile: S_i = Q_i.K^T landed
+  uint64_t* s_full = v_empty + (SPLIT ? VST : 0);  // [2] per Q tile: S_i = Q_i.K^T landed
   uint64_t* s_empty = s_full + 2;          // [2] S_i read into registers
   uint64_t* p_full = s_empty + 2;          // [2] P_i written (and O_i rescaled)
   uint64_t* o_done = p_full + 2;           // [2] O_i += P_i.V retired (P_i free)
@@ -350,6 +357,7 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
           mbar_init(&k_full[i], 1);
           mbar_init(&v_full[i], 1);
           mbar_init(&kv_empty[i], 2);  // both Q tiles' issuers release every stage
+          if constexpr (SPLIT) mbar_init(&v_empty[i], 2);
         }
       }
       for (int i = 0; i < 2; ++i) {
@@ -448,10 +456,10 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
   // the TMA / MMA warpgroup gives its registers up
   if (warp >= NS) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R::REG_AUX) : "memory");
   if (warp == NS) {
-    if constexpr (PP) {
-      // ---------------------------------------------------------- TMA producer (ping-pong)
-      // K runs two tiles ahead of V: order K(0), K(1), then V(j), K(j + 2).  Each stream keeps
-      // a warp-wide cache of 32 tiles' block-table rows (lane l holds tile base + l).
+    if constexpr (SPLIT) {
+      // ---------------------------------------------------------- TMA producer (split K / V rings)
+      // K runs LEAD tiles ahead of V: order K(0..LEAD-1), then V(j), K(j + LEAD).  Each stream
+      // keeps a warp-wide cache of 32 tiles' block-table rows (lane l holds tile base + l).
       const int4 sg = seg0;
       const Unit u = unit_at(sg.x);
       const long long row0 = (long long)u.kvh * (p.head_stride / DH);
@@ -529,8 +537,8 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
         __syncwarp();
       };
       int kj = sg.y;
-      for (int j = sg.y; j < sg.z && j < sg.y + RDKV_ATTN_PPF; ++j) prefetch(j + 2);
-      for (; kj < sg.z && kj < sg.y + 2; ++kj) load(true, kj);
+      for (int j = sg.y; j < sg.z && j < sg.y + RDKV_ATTN_PPF; ++j) prefetch(j + LEAD);
+      for (; kj < sg.z && kj < sg.y + LEAD; ++kj) load(true, kj);
       for (int j = sg.y; j < sg.z; ++j) {
         load(false, j);
         if (kj < sg.z) {
@@ -703,8 +711,15 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
         if (nt == 0) continue;
         if (i >= unit_at(sg.x).n_q) {  // no Q tile i in this unit: release its stages
           for (int j = 0; j < nt; ++j, ++it) {
-            issuer_wait(&v_full[it % ST], (it / ST) & 1);
-            mbar_arrive(&kv_empty[it % ST]);
+            if constexpr (SPLIT) {
+              issuer_wait(&k_full[it % ST], (it / ST) & 1);
+              mbar_arrive(&kv_empty[it % ST]);
+              issuer_wait(&v_full[it % ST], (it / ST) & 1);
+              mbar_arrive(&v_empty[it % ST]);
+            } else {
+              issuer_wait(&v_full[it % ST], (it / ST) & 1);
+              mbar_arrive(&kv_empty[it % ST]);
+            }
           }
           continue;
         }
@@ -718,6 +733,7 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
         TRACE(2 + i, ti, 5);
         tc_fence_after();
         issue_qk(it % ST, nt == 1);
+        if constexpr (SPLIT) umma_commit(&kv_empty[it % ST]);  // K(j) consumed by this Q.K^T
         for (int j = 0; j < nt; ++j, ++it, ++ti) {
           const int st = it % ST;
           const bool more = j + 1 < nt;
@@ -728,6 +744,7 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
             if (j > 0) TRACE(2 + i, ti, 3);
             tc_fence_after();
             issue_qk((it + 1) % ST, j + 2 == nt);
+            if constexpr (SPLIT) umma_commit(&kv_empty[(it + 1) % ST]);
             TRACE(2 + i, ti, 0);
           }
           issuer_wait(&v_full[st], (it / ST) & 1);
@@ -752,7 +769,7 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
           }
           umma_commit(&o_done[i]);
           TRACE(2 + i, ti, 1);
-          umma_commit(&kv_empty[st]);
+          umma_commit(SPLIT ? &v_empty[st] : &kv_empty[st]);
           if (C::ALIAS && more) {  // S_i overwrites P_i only after the P.V above (issue order)
             issuer_wait(&k_full[(it + 1) % ST], ((it + 1) / ST) & 1);
             tc_fence_after();
