@@ -169,6 +169,9 @@ __device__ __forceinline__ long long gtimer() {
 #define RDKV_ATTN_EMU 3
 #endif
 constexpr int EMU_OF_8 = RDKV_ATTN_EMU;  // exp2 of this many of every 8 score groups runs as a polynomial
+#ifndef RDKV_ATTN_SPEC
+#define RDKV_ATTN_SPEC 0  // 1: P at the current reference max while the tile max is taken (redo if it moved); measured slower
+#endif
 
 #ifndef RDKV_ATTN_PF
 #define RDKV_ATTN_PF 0  // TMA producer L2 prefetch distance in tiles (0: off; 2-8 measured no faster)
@@ -265,6 +268,7 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
   constexpr int KH = BKV / SPL;   // keys of a tile per softmax thread
   static_assert(KH % 64 == 0, "a softmax thread stores P in 32-column TMEM chunks");
   constexpr int ST = C::STAGES;
+  constexpr bool SPEC = RDKV_ATTN_SPEC != 0;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   CTA_TRACE(1);
   uint8_t* smem = smem_raw;
@@ -884,48 +888,65 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
             for (int e = 0; e < KH; ++e)
               if (e > lim) sv[e] = __float_as_uint(-INFINITY);
           }
-          float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+          // P = 2^(S*scale - m_used) as bf16 pairs (registers), row sum in fp32; this
+          // overlaps P_i.V(j-1), which still reads the P_i buffer.  With `track`, the
+          // tile's row max is taken in the same pass (speculative: P at the current
+          // reference max, redone below in the rare case that the max moved).
+          float s0, s1, s2, s3;
+          uint32_t pk[KH / 2];
+          float mx4[4];
+          auto exp_pass = [&](float nb, bool track) {
+            s0 = s1 = s2 = s3 = 0.f;
 #pragma unroll
-          for (int e = 0; e < KH; e += 8)
+            for (int e = 0; e < KH; e += 4) {
+              if (track) {
+                mx4[(e / 4) & 3] = fmax3(mx4[(e / 4) & 3], __uint_as_float(sv[e]), __uint_as_float(sv[e + 1]));
+                mx4[(e / 4 + 2) & 3] = fmax3(mx4[(e / 4 + 2) & 3], __uint_as_float(sv[e + 2]), __uint_as_float(sv[e + 3]));
+              }
+              float x0, x1, x2, x3;
+              ffma2(x0, x1, __uint_as_float(sv[e]), __uint_as_float(sv[e + 1]), sl2, sl2, nb, nb);
+              ffma2(x2, x3, __uint_as_float(sv[e + 2]), __uint_as_float(sv[e + 3]), sl2, sl2, nb, nb);
+              if (((e / 4) * 3) % 8 < EMU_OF_8) {  // this group of 4 on the FMA pipe
+                exp2_emu2(x0, x1, x0, x1);
+                exp2_emu2(x2, x3, x2, x3);
+              } else {  // on the MUFU
+                x0 = ex2_approx(x0);
+                x1 = ex2_approx(x1);
+                x2 = ex2_approx(x2);
+                x3 = ex2_approx(x3);
+              }
+              if constexpr (!C::LSUM) {
+                fadd2(s0, s1, s0, s1, x0, x1);
+                fadd2(s2, s3, s2, s3, x2, x3);
+              }
+              pk[e / 2] = pack_bf16(x0, x1);
+              pk[e / 2 + 1] = pack_bf16(x2, x3);
+            }
+          };
+          mx4[0] = mx4[1] = mx4[2] = mx4[3] = -INFINITY;
+          // speculative pass once the reference max is finite (every tile after the first)
+          const bool spec = SPEC && __all_sync(0xffffffffu, m_used != -INFINITY);
+          if (spec) {
+            exp_pass(-m_used, true);
+          } else {
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              mx4[q] = fmax3(mx4[q], __uint_as_float(sv[e + 2 * q]), __uint_as_float(sv[e + 2 * q + 1]));
+            for (int e = 0; e < KH; e += 8)
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                mx4[q] = fmax3(mx4[q], __uint_as_float(sv[e + 2 * q]), __uint_as_float(sv[e + 2 * q + 1]));
+          }
           const float mt = exchange(fmax3(fmaxf(mx4[0], mx4[1]), mx4[2], mx4[3]), ti & 1, true) * sl2;
           // lazy rescale: move the reference max only when it grew by more than 2^8
           const bool need = mt > m_used + RESCALE_LOG2;
-          const bool rescale = __any_sync(0xffffffffu, need) && j > 0;
+          const bool any_need = __any_sync(0xffffffffu, need);
+          const bool rescale = any_need && j > 0;
           float f = 1.f;
           if (need) {
             f = ex2_approx(m_used - mt);  // 0 when m_used = -inf
             l *= f;
             m_used = mt;
           }
-          // P = 2^(S*scale - m_used) as bf16 pairs (registers), row sum in fp32; this
-          // overlaps P_i.V(j-1), which still reads the P_i buffer
-          const float nb = m_used == -INFINITY ? 0.f : -m_used;
-          float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-          uint32_t pk[KH / 2];
-#pragma unroll
-          for (int e = 0; e < KH; e += 4) {
-            float x0, x1, x2, x3;
-            ffma2(x0, x1, __uint_as_float(sv[e]), __uint_as_float(sv[e + 1]), sl2, sl2, nb, nb);
-            ffma2(x2, x3, __uint_as_float(sv[e + 2]), __uint_as_float(sv[e + 3]), sl2, sl2, nb, nb);
-            if (((e / 4) * 3) % 8 < EMU_OF_8) {  // this group of 4 on the FMA pipe
-              exp2_emu2(x0, x1, x0, x1);
-              exp2_emu2(x2, x3, x2, x3);
-            } else {  // on the MUFU
-              x0 = ex2_approx(x0);
-              x1 = ex2_approx(x1);
-              x2 = ex2_approx(x2);
-              x3 = ex2_approx(x3);
-            }
-            if constexpr (!C::LSUM) {
-              fadd2(s0, s1, s0, s1, x0, x1);
-              fadd2(s2, s3, s2, s3, x2, x3);
-            }
-            pk[e / 2] = pack_bf16(x0, x1);
-            pk[e / 2 + 1] = pack_bf16(x2, x3);
-          }
+          if (!spec || any_need) exp_pass(m_used == -INFINITY ? 0.f : -m_used, false);
           // P_i (and O_i) are free once P_i.V(j-1) has retired (implied by s_full when P aliases S)
           if (j + 1 < nt) TRACE(i, ti, 3);
           if (!PP && j > 0) {  // PP: S_i(j) landing already implies P.V_i(j-1) retired
