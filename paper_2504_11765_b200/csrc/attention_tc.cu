@@ -62,6 +62,12 @@ static int make_tmap_q(CUtensorMap* m, const void* q, long long tokens, int hq, 
   return 0;
 }
 
+#ifndef RDKV_ATTN_BYKIND
+#define RDKV_ATTN_BYKIND 1  // MMA issuers by kind and Q tile (Q.K^T_0, Q.K^T_1, P.V_0, P.V_1) instead of one per Q tile
+#endif
+#ifndef RDKV_ATTN_SPLITKV
+#define RDKV_ATTN_SPLITKV 0  // 1: separate K / V stage releases in the two-issuer schedule (measured: C3 98.5 vs 96.3 us, C2 77.5 vs 78.3)
+#endif
 #ifndef RDKV_ATTN_LSUM
 #define RDKV_ATTN_LSUM 0  // 1: dh = 128 row sums on the tensor cores (L += P.ones; measured slower: 111 vs 98 us)
 #endif
@@ -70,7 +76,7 @@ namespace {
 constexpr int ROWS = 128;
 constexpr int HALF = 64;  // rows per TMA box (= one KV block of the pool)
 
-template <int DH, bool PP = false>
+template <int DH, bool PP = false, bool BYK = false>
 struct TcCfg {
   // key positions per tile: 128 at dh = 64; 64 at dh = 128, so S_i (BKV columns),
   // O_i (dh) and P_i (BKV / 2) of both Q tiles fit the 512 TMEM columns (448) and
@@ -90,7 +96,13 @@ struct TcCfg {
 #ifndef RDKV_ATTN_ST128
 #define RDKV_ATTN_ST128 4
 #endif
-  static constexpr int STAGES = DH == 64 ? RDKV_ATTN_ST64 : RDKV_ATTN_ST128;
+#ifndef RDKV_ATTN_ST128_BYK
+#define RDKV_ATTN_ST128_BYK 5
+#endif
+  // BYK (issuers by kind, one segment): no row-exchange / stream-K regions, so dh = 128
+  // affords a fifth K/V stage (the stage of tile j + ST is released only when the later Q
+  // tile's P.V(j) retired; K/V loads under full load take ~3.8k cycles)
+  static constexpr int STAGES = DH == 64 ? RDKV_ATTN_ST64 : BYK ? RDKV_ATTN_ST128_BYK : RDKV_ATTN_ST128;
   static constexpr int KST = PP ? 3 : STAGES;  // K stages (PP: own ring)
   static constexpr int VST = PP ? 2 : STAGES;  // V stages (PP: own ring)
   static constexpr uint32_t QB = ROWS * DH * 2;    // one Q tile
@@ -102,7 +114,7 @@ struct TcCfg {
   // halves][128 rows] fp32; PP has room for one parity only (a second barrier orders reuse)
   static constexpr int RED_PAR = PP ? 1 : 2;
   static constexpr uint32_t OFF_RED = OFF_V + VST * KB;
-  static constexpr uint32_t OFF_BAR = OFF_RED + RED_PAR * 2 * 2 * ROWS * 4;
+  static constexpr uint32_t OFF_BAR = OFF_RED + (BYK ? 0 : RED_PAR * 2 * 2 * ROWS * 4);
   static constexpr uint32_t N_BARS = 4 + 2 * KST + 2 * VST + 8;
   static constexpr uint32_t OFF_MISC = (OFF_BAR + 8 * N_BARS + 15) / 16 * 16;  // TMEM base, segment count, W
   static constexpr uint32_t OFF_SEG = OFF_MISC + 16;                        // stream-K segments (int4)
@@ -111,7 +123,7 @@ struct TcCfg {
   // constant [16 x BKV] bf16 ones tile as the K-major B operand (16 columns of L_i, all equal)
   static constexpr bool LSUM = RDKV_ATTN_LSUM && DH == 128 && !ALIAS;
   static constexpr uint32_t OFF_ONES = (OFF_SEQ + 3 * 4 * 512 + 1023) / 1024 * 1024;
-  static constexpr size_t SMEM = PP ? OFF_MISC + 16 : LSUM ? OFF_ONES + 16 * 128 : OFF_SEQ + 3 * 4 * 512;
+  static constexpr size_t SMEM = PP || BYK ? OFF_MISC + 16 : LSUM ? OFF_ONES + 16 * 128 : OFF_SEQ + 3 * 4 * 512;
   static_assert(SMEM <= 232448, "attention smem exceeds 227 KB");
   // TMEM columns
   static constexpr uint32_t COL_S = 0;                          // S_i at BKV i
@@ -126,7 +138,9 @@ struct TcCfg {
 // SPL softmax warps per query row (each takes BKV / SPL keys of a tile):
 //   warps [0, NS): softmax, NS = 8 * SPL (Q tile i, key half h, TMEM quadrant q);
 //   NS: TMA producer; NS+1 / NS+2: MMA issuers of Q tile 0 / 1; NS+3: Q loader.
-template <int SPL>
+//   BYK (MMA issuers by kind, see ISSUE_BY_KIND): NS+1 / NS+2 issue Q.K^T of Q tile 0 / 1,
+//   NS+3 loads Q then issues P.V of Q tile 0, the TMA producer NS also issues P.V of Q tile 1.
+template <int SPL, bool BYK = false>
 struct Roles {
   static constexpr int NS = 8 * SPL;
   static constexpr int THREADS = 32 * (NS + 4);
@@ -135,6 +149,17 @@ struct Roles {
   static constexpr int REG_SOFTMAX = SPL == 1 ? 224 : 104;
   static constexpr int REG_AUX = SPL == 1 ? 56 : 40;
 };
+// Q.K^T and P.V issued by separate threads, one per (kind, Q tile): single-segment grids
+// with the default TMEM layout (not stream-K, ping-pong or tensor-core row sums)
+// (dh = 128: at dh = 64 the default schedule measured 1% faster)
+template <int DH, int SPL, bool SK, bool PP>
+constexpr bool issue_by_kind() {
+  return RDKV_ATTN_BYKIND && DH == 128 && SPL == 1 && !SK && !PP && !RDKV_ATTN_LSUM && !(RDKV_ATTN_SPLITKV != 0);
+}
+template <int DH, int SPL, bool SK, bool PP>
+using RolesOf = Roles<SPL, issue_by_kind<DH, SPL, SK, PP>()>;
+template <int DH, int SPL, bool SK, bool PP>
+using CfgOf = TcCfg<DH, PP, issue_by_kind<DH, SPL, SK, PP>()>;
 constexpr float RESCALE_LOG2 = 8.f;   // lazy O rescale: keep a stale row max until it is 2^8 too small
 #ifndef RDKV_ATTN_TRACE
 #define RDKV_ATTN_TRACE 0  // 1: per-tile clock64 timeline of CTA 0 (debug builds only)
@@ -175,9 +200,6 @@ constexpr int EMU_OF_8 = RDKV_ATTN_EMU;  // exp2 of this many of every 8 score g
 
 #ifndef RDKV_ATTN_PF
 #define RDKV_ATTN_PF 0  // TMA producer L2 prefetch distance in tiles (0: off; 2-8 measured no faster)
-#endif
-#ifndef RDKV_ATTN_SPLITKV
-#define RDKV_ATTN_SPLITKV 0  // 1: separate K / V stage releases in the two-issuer schedule (measured: C3 98.5 vs 96.3 us, C2 77.5 vs 78.3)
 #endif
 #ifndef RDKV_ATTN_PPF
 #define RDKV_ATTN_PPF 0  // ping-pong producer: L2 prefetch distance in tiles ahead of the K stream (2-8 slower)
@@ -255,11 +277,11 @@ __device__ __forceinline__ void st_release_gpu(int* p, int v) {
 // partials that the following CTAs wrote as their FIRST segment (SEG_PART, published
 // with a release flag before they do anything else, so the waits cannot deadlock).
 template <int DH, int SPL, bool SK, bool PP = false>
-__global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
+__global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                    const __grid_constant__ CUtensorMap tmQ, AttnParams p) {
-  using C = TcCfg<DH, PP>;
-  using R = Roles<SPL>;
+  using C = CfgOf<DH, SPL, SK, PP>;
+  using R = RolesOf<DH, SPL, SK, PP>;
   static_assert(!SK || SPL == 1, "stream-K runs one softmax warp per row");
   static_assert(!PP || !SK, "ping-pong runs one segment per CTA");
   constexpr int NS = R::NS;
@@ -269,6 +291,9 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
   static_assert(KH % 64 == 0, "a softmax thread stores P in 32-column TMEM chunks");
   constexpr int ST = C::STAGES;
   constexpr bool SPEC = RDKV_ATTN_SPEC != 0;
+  // Q.K^T and P.V issued by separate threads (single-segment grids, default two-issuer layout)
+  constexpr bool ISSUE_BY_KIND = issue_by_kind<DH, SPL, SK, PP>();
+  static_assert(!ISSUE_BY_KIND || (!C::LSUM && !C::ALIAS), "issuers by kind need separate S / P buffers");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   CTA_TRACE(1);
   uint8_t* smem = smem_raw;
@@ -360,7 +385,7 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
         for (int i = 0; i < ST; ++i) {
           mbar_init(&k_full[i], 1);
           mbar_init(&v_full[i], 1);
-          mbar_init(&kv_empty[i], 2);  // both Q tiles' issuers release every stage
+          mbar_init(&kv_empty[i], 2);  // both Q tiles' (P.V) issuers release every stage
           if constexpr (SPLIT) mbar_init(&v_empty[i], 2);
         }
       }
@@ -459,6 +484,29 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
   // register budget: the softmax warpgroups hold a 128-score row per thread,
   // the TMA / MMA warpgroup gives its registers up
   if (warp >= NS) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R::REG_AUX) : "memory");
+  // P.V of Q tile i for KV tile j (ISSUE_BY_KIND; lane 0): P.V_i(j) is issued only after the
+  // softmax consumed S_i(j), i.e. after Q.K^T_i(j) retired, so this thread's commit after
+  // P.V_i(j) also covers K(j); each Q tile's P.V issuer releases the stage once (count 2).
+  auto pv_step = [&](int i, int j, bool mine) {
+    constexpr uint32_t idesc_pv = idesc_bf16_f32(ROWS, DH) | (1u << 16);  // B (V) is MN-major
+    const int st = j % ST;
+    issuer_wait(&v_full[st], (j / ST) & 1);
+    if (!mine) {  // no Q tile i in this unit: just release the stage
+      mbar_arrive(&kv_empty[st]);
+      return;
+    }
+    issuer_wait(&p_full[i], j & 1);
+    TRACE(2 + i, j, 5);
+    tc_fence_after();
+    const uint32_t va = sb + C::OFF_V + st * C::KB;
+    const uint32_t tO = tmem + C::COL_O + i * DH, tP = tmem + C::COL_P + i * C::P_STRIDE;
+#pragma unroll
+    for (int kk = 0; kk < BKV / 16; ++kk)  // O_i (+)= P_i . V(j), P_i from TMEM
+      umma_bf16_ts(tO, tP + kk * 8, desc_mn(va + kk * 2048, BKV * 128), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+    umma_commit(&o_done[i]);
+    umma_commit(&kv_empty[st]);
+    TRACE(2 + i, j, 1);
+  };
   if (warp == NS) {
     if constexpr (SPLIT) {
       // ---------------------------------------------------------- TMA producer (split K / V rings)
@@ -550,6 +598,58 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
           prefetch(kj + RDKV_ATTN_PPF);
           ++kj;
         }
+      }
+    } else if constexpr (ISSUE_BY_KIND) {
+      // ---------------------------------------------------------- TMA producer + P.V_1 issuer
+      // The first ST tiles are requested up front; afterwards tile j + ST goes into the stage
+      // that P.V_0(j) and P.V_1(j) release, right after this thread issued P.V_1(j).
+      const int4 sg = seg0;
+      const Unit u = unit_at(sg.x);
+      const int nt = sg.z - sg.y;
+      const bool mine1 = nt > 0 && u.n_q > 1;
+      const long long row0 = (long long)u.kvh * (p.head_stride / DH);
+      const int* bt = p.block_table + (long long)u.s * p.bt_stride;
+      int my_rows[NH] = {};
+      auto produce = [&](int jl) {  // whole warp, jl = 0, 1, 2, ... in order
+        const int j = sg.y + jl;
+        if ((jl & 31) == 0 && j + lane < sg.z) {
+#pragma unroll
+          for (int h = 0; h < NH; ++h) {
+            int pos = (j + lane) * BKV + h * HALF;
+            if (pos >= u.kv_len) pos = (j + lane) * BKV;  // masked half: any valid, finite block
+            my_rows[h] = (int)(row0 + (long long)bt[pos / p.block_size] * p.block_size + pos % p.block_size);
+          }
+        }
+        int rows[NH];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) rows[h] = __shfl_sync(0xffffffffu, my_rows[h], jl & 31);
+        if (lane == 0) {
+          const int st = jl % ST;
+          TRACE(4, jl, 0);
+          issuer_wait(&kv_empty[st], ((jl / ST) & 1) ^ 1);  // prompt: P.V_1 follows on this thread
+          TRACE(4, jl, 1);
+          mbar_arrive_expect_tx(&k_full[st], C::KB);
+#pragma unroll
+          for (int c = 0; c < DH / 64; ++c)
+#pragma unroll
+            for (int h = 0; h < NH; ++h)
+              tma_load_2d_nohint(&tmK, &k_full[st], smem + C::OFF_K + st * C::KB + c * (BKV * 128) + h * (HALF * 128),
+                                 c * 64, rows[h]);
+          mbar_arrive_expect_tx(&v_full[st], C::KB);
+#pragma unroll
+          for (int c = 0; c < DH / 64; ++c)
+#pragma unroll
+            for (int h = 0; h < NH; ++h)
+              tma_load_2d_nohint(&tmV, &v_full[st], smem + C::OFF_V + st * C::KB + c * (BKV * 128) + h * (HALF * 128),
+                                 c * 64, rows[h]);
+        }
+        __syncwarp();
+      };
+      for (int jl = 0; jl < nt && jl < ST; ++jl) produce(jl);
+      for (int j = 0; j < nt; ++j) {
+        if (lane == 0) pv_step(1, j, mine1);
+        __syncwarp();
+        if (j + ST < nt) produce(j + ST);
       }
     } else {
     // ------------------------------------------------------------ TMA producer
@@ -686,6 +786,42 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
           }
         }
       }
+    } else if constexpr (ISSUE_BY_KIND) {
+      // ---------------------------------------------------------- Q.K^T issuers
+      // warp NS+1+i issues Q.K^T_i of every tile; the P.V of both Q tiles is issued by the
+      // Q-loader warp once Q is requested (below).  Separate Q.K^T and P.V streams touch
+      // disjoint TMEM (S vs P / O), so their relative order does not matter: Q.K^T_i(j+1)
+      // goes out as soon as the softmax has read S_i(j), never queued behind the P.V of a
+      // tile whose softmax is still running, and each issuer's barrier-observation latency
+      // (~90 cycles per satisfied try_wait) overlaps the other issuers' MMAs.
+      const int i = warp - NS - 1;
+      if (lane == 0) {
+        constexpr uint32_t idesc_qk = idesc_bf16_f32(ROWS, BKV);
+        const int4 sg = seg0;
+        const int nt = sg.z - sg.y;
+        if (nt > 0 && i < unit_at(sg.x).n_q) {
+          issuer_wait(&q_full[i], 0);
+          const uint32_t qa = sb + C::OFF_Q + i * C::QB;
+          const uint32_t tS = tmem + C::COL_S + i * BKV;
+          for (int j = 0; j < nt; ++j) {
+            const int st = j % ST;
+            issuer_wait(&k_full[st], (j / ST) & 1);
+            if (j > 0) issuer_wait(&s_empty[i], (j - 1) & 1);  // the softmax read S_i(j-1)
+            TRACE(2 + i, j, 2);
+            tc_fence_after();
+            const uint32_t ka = sb + C::OFF_K + st * C::KB;
+#pragma unroll
+            for (int kk = 0; kk < DH / 16; ++kk) {
+              const uint32_t sub = (kk & 3) * 32;
+              umma_bf16(tS, desc_k(qa + (kk >> 2) * (ROWS * 128) + sub), desc_k(ka + (kk >> 2) * (BKV * 128) + sub),
+                        idesc_qk, kk > 0 ? 1u : 0u);
+            }
+            umma_commit(&s_full[i]);
+            if (j + 1 == nt) umma_commit(&q_empty[i]);
+            TRACE(2 + i, j, 0);
+          }
+        }
+      }
     } else {
     // ------------------------------------------------------------ MMA issuers
     // one issuing thread per Q tile, so neither softmax warpgroup ever waits on
@@ -814,6 +950,15 @@ __global__ void __launch_bounds__(Roles<SPL>::THREADS, 1)
         __syncwarp();
         asm volatile("bar.sync %0, %1;" ::"n"(SK_PUB), "n"(NS * 32 + 32) : "memory");
         if (lane == 0) st_release_gpu(p.sk_flag + blockIdx.x, 1);
+      }
+      if constexpr (ISSUE_BY_KIND) {  // then issue P.V of Q tile 0 (the producer: Q tile 1)
+        if (lane == 0) {
+          const int nt = sg.z - sg.y;
+          const bool mine = nt > 0 && unit_at(sg.x).n_q > 0;
+          for (int j = 0; j < nt; ++j) pv_step(0, j, mine);
+        }
+        __syncwarp();
+        continue;
       }
       if (k == 0) {  // Q requested: pull the O projection's weights into L2 meanwhile
         __syncwarp();
@@ -1155,7 +1300,7 @@ int set_smem_attr() {
   static bool attr = false;
   if (!attr) {
     CUDA_TRY(cudaFuncSetAttribute(attn_tc_kernel<DH, SPL, SK, PP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)TcCfg<DH, PP>::SMEM));
+                                  (int)CfgOf<DH, SPL, SK, PP>::SMEM));
     attr = true;
   }
   return 0;
@@ -1163,7 +1308,7 @@ int set_smem_attr() {
 
 template <int DH, int SPL, bool PP = false>
 int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
-  using C = TcCfg<DH, PP>;
+  using C = CfgOf<DH, SPL, false, PP>;
   // plane view: rows = hkv * slots, cols = dh
   const long long rows = (long long)p.hkv * (p.head_stride / DH);
   CUtensorMap tk, tv;
@@ -1186,7 +1331,8 @@ int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
   if constexpr (SPL == 1 && !PP) {
     if (p.sk_mode && p.sk_o && p.sk_ctas >= sms && ctas * 2 > sms && ctas <= SK_MAXSEG) {
       RDKV_TRY((set_smem_attr<DH, SPL, true>()));
-      CUDA_TRY(launch_k(attn_tc_kernel<DH, SPL, true>, dim3(sms), dim3(Roles<SPL>::THREADS), C::SMEM, st, tk, tv, tq, q));
+      CUDA_TRY(launch_k(attn_tc_kernel<DH, SPL, true>, dim3(sms), dim3(RolesOf<DH, SPL, true, false>::THREADS),
+                        CfgOf<DH, SPL, true, false>::SMEM, st, tk, tv, tq, q));
       CUDA_TRY(cudaGetLastError());
       return 0;
     }
@@ -1214,7 +1360,7 @@ int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
     b.kv_splits = KT;
     b.tail_ctas = s_a * ups;
     const int grid = s_a * ups + (n_seqs - s_a) * ups * KT;
-    CUDA_TRY(launch_k(attn_tc_kernel<DH, SPL, false, PP>, dim3(grid), dim3(Roles<SPL>::THREADS), C::SMEM, st, tk, tv, tq, b));
+    CUDA_TRY(launch_k(attn_tc_kernel<DH, SPL, false, PP>, dim3(grid), dim3(RolesOf<DH, SPL, false, PP>::THREADS), C::SMEM, st, tk, tv, tq, b));
     CUDA_TRY(launch_k(attn_split_combine_kernel<DH>, dim3(p.n_tokens, (p.hq + 7) / 8), dim3(256), 0, st, b));
     CUDA_TRY(cudaGetLastError());
     return 0;
@@ -1229,7 +1375,7 @@ int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
   }
   RDKV_TRY((set_smem_attr<DH, SPL, false, PP>()));
   dim3 grid(qblocks * q.kv_splits, p.hkv, n_seqs);
-  CUDA_TRY(launch_k(attn_tc_kernel<DH, SPL, false, PP>, grid, dim3(Roles<SPL>::THREADS), C::SMEM, st, tk, tv, tq, q));
+  CUDA_TRY(launch_k(attn_tc_kernel<DH, SPL, false, PP>, grid, dim3(RolesOf<DH, SPL, false, PP>::THREADS), C::SMEM, st, tk, tv, tq, q));
   CUDA_TRY(cudaGetLastError());
   if (q.kv_splits > 1) {
     CUDA_TRY(launch_k(attn_split_combine_kernel<DH>, dim3(p.n_tokens, (p.hq + 7) / 8), dim3(256), 0, st, q));

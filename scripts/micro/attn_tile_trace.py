@@ -51,3 +51,9 @@ for j in range(1, 64):
     print(f"{j:3d} " + " ".join(f"{x:7.0f}" for x in r))
 Path("gpurun_out").mkdir(exist_ok=True)
 Path("gpurun_out/attn_tile_trace.json").write_text(json.dumps({"rows": [[None if np.isnan(x) else x for x in r] for r in rows]}))
+print("by-kind issuers per tile: [QK0 ready, QK0 issued, PV0 p_full seen, PV0 issued] [same for Q1] | producer tile j: before/after kv_empty wait")
+for j in range(1, 64):
+    r = [t[2, j, 2], t[2, j, 0], t[2, j, 5], t[2, j, 1], t[3, j, 2], t[3, j, 0], t[3, j, 5], t[3, j, 1], t[4, j, 0], t[4, j, 1]]
+    if all(np.isnan(r)):
+        continue
+    print(f"{j:3d} " + " ".join(f"{x:7.0f}" for x in r))
