@@ -65,6 +65,12 @@ static int make_tmap_q(CUtensorMap* m, const void* q, long long tokens, int hq, 
 #ifndef RDKV_ATTN_BYKIND
 #define RDKV_ATTN_BYKIND 1  // MMA issuers by kind and Q tile (Q.K^T_0, Q.K^T_1, P.V_0, P.V_1) instead of one per Q tile
 #endif
+#ifndef RDKV_ATTN_PDB
+#define RDKV_ATTN_PDB 0  // 1: double-buffered P with the issuers by kind (dh = 128)
+#endif
+#ifndef RDKV_ATTN_BYK64
+#define RDKV_ATTN_BYK64 0  // 1: issuers by kind at dh = 64 too
+#endif
 #ifndef RDKV_ATTN_SPLITKV
 #define RDKV_ATTN_SPLITKV 0  // 1: separate K / V stage releases in the two-issuer schedule (measured: C3 98.5 vs 96.3 us, C2 77.5 vs 78.3)
 #endif
@@ -115,7 +121,11 @@ struct TcCfg {
   static constexpr int RED_PAR = PP ? 1 : 2;
   static constexpr uint32_t OFF_RED = OFF_V + VST * KB;
   static constexpr uint32_t OFF_BAR = OFF_RED + (BYK ? 0 : RED_PAR * 2 * 2 * ROWS * 4);
-  static constexpr uint32_t N_BARS = 4 + 2 * KST + 2 * VST + 8;
+  // RDKV_ATTN_PDB (BYK at dh = 128): P double-buffered (TMEM has the room: S 128 + O 256 + P 4 x 32
+  // = 512), so the softmax stores P(j) once P.V(j-2) retired instead of waiting for P.V(j-1).
+  // Correct but measured no faster (C3 attn_perf 92.3 vs 91.7 us): off
+  static constexpr int P_BUFS = RDKV_ATTN_PDB && BYK && DH == 128 ? 2 : 1;
+  static constexpr uint32_t N_BARS = 4 + 2 * KST + 2 * VST + 4 + 4 * P_BUFS;
   static constexpr uint32_t OFF_MISC = (OFF_BAR + 8 * N_BARS + 15) / 16 * 16;  // TMEM base, segment count, W
   static constexpr uint32_t OFF_SEG = OFF_MISC + 16;                        // stream-K segments (int4)
   static constexpr uint32_t OFF_SEQ = OFF_SEG + 16 * 512;                   // stream-K: [3][512] seq start/new/cached
@@ -129,7 +139,8 @@ struct TcCfg {
   static constexpr uint32_t COL_S = 0;                          // S_i at BKV i
   static constexpr uint32_t COL_O = 2 * BKV;                    // O_i at 2 BKV + DH i
   static constexpr uint32_t COL_P = ALIAS ? 0 : 2 * BKV + 2 * DH;  // P_i at COL_P + (ALIAS ? BKV : BKV / 2) i
-  static constexpr uint32_t P_STRIDE = ALIAS ? BKV : BKV / 2;
+  static constexpr uint32_t P_STRIDE = ALIAS ? BKV : P_BUFS * BKV / 2;  // per Q tile (all P buffers)
+  static_assert(COL_P + 2 * P_STRIDE <= 512, "TMEM: P does not fit");
   static constexpr uint32_t COL_L = COL_P + 2 * P_STRIDE;     // L_i at COL_L + 16 i (LSUM)
   static_assert(!LSUM || COL_L + 32 <= 512, "TMEM: L columns do not fit");
   static_assert(COL_O + 2 * DH <= 512, "TMEM: S and O do not fit");
@@ -154,7 +165,7 @@ struct Roles {
 // (dh = 128: at dh = 64 the default schedule measured 1% faster)
 template <int DH, int SPL, bool SK, bool PP>
 constexpr bool issue_by_kind() {
-  return RDKV_ATTN_BYKIND && DH == 128 && SPL == 1 && !SK && !PP && !RDKV_ATTN_LSUM && !(RDKV_ATTN_SPLITKV != 0);
+  return RDKV_ATTN_BYKIND && (DH == 128 || RDKV_ATTN_BYK64) && SPL == 1 && !SK && !PP && !RDKV_ATTN_LSUM && !(RDKV_ATTN_SPLITKV != 0);
 }
 template <int DH, int SPL, bool SK, bool PP>
 using RolesOf = Roles<SPL, issue_by_kind<DH, SPL, SK, PP>()>;
@@ -313,8 +324,14 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
   uint64_t* v_empty = kv_empty + KST;      // [VST] PP only: V consumed by both P.V
   uint64_t* s_full = v_empty + (SPLIT ? VST : 0);  // [2] per Q tile: S_i = Q_i.K^T landed
   uint64_t* s_empty = s_full + 2;          // [2] S_i read into registers
-  uint64_t* p_full = s_empty + 2;          // [2] P_i written (and O_i rescaled)
-  uint64_t* o_done = p_full + 2;           // [2] O_i += P_i.V retired (P_i free)
+  // per P buffer (the softmax runs up to P_BUFS tiles ahead of the P.V issuer, so one barrier
+  // per buffer keeps every parity wait within one phase of the barrier's state)
+  uint64_t* p_full = s_empty + 2;          // [2][P_BUFS] P_i(buffer b) written (and O_i rescaled)
+  uint64_t* o_done = p_full + 2 * C::P_BUFS;  // [2][P_BUFS] O_i += P_i(buffer b).V retired (that P buffer free)
+  // the barriers and parity of tile t of Q tile i: P(t) written, P.V_i(t) retired
+  auto pf = [&](int i, int t) { return &p_full[i * C::P_BUFS + t % C::P_BUFS]; };
+  auto od = [&](int i, int t) { return &o_done[i * C::P_BUFS + t % C::P_BUFS]; };
+  auto od_par = [&](int t) { return (uint32_t)((t / C::P_BUFS) & 1); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_MISC);
   int* nseg_s = reinterpret_cast<int*>(smem + C::OFF_MISC + 4);
   long long* wtot_s = reinterpret_cast<long long*>(smem + C::OFF_MISC + 8);
@@ -392,8 +409,8 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
       for (int i = 0; i < 2; ++i) {
         mbar_init(&s_full[i], 1);
         mbar_init(&s_empty[i], 4 * SPL);
-        mbar_init(&p_full[i], 4 * SPL);
-        mbar_init(&o_done[i], 1);
+        for (int b = 0; b < C::P_BUFS; ++b) mbar_init(&p_full[i * C::P_BUFS + b], 4 * SPL);
+        for (int b = 0; b < C::P_BUFS; ++b) mbar_init(&o_done[i * C::P_BUFS + b], 1);
       }
       fence_barrier_init();
     }
@@ -495,15 +512,16 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
       mbar_arrive(&kv_empty[st]);
       return;
     }
-    issuer_wait(&p_full[i], j & 1);
+    issuer_wait(pf(i, j), od_par(j));
     TRACE(2 + i, j, 5);
     tc_fence_after();
     const uint32_t va = sb + C::OFF_V + st * C::KB;
-    const uint32_t tO = tmem + C::COL_O + i * DH, tP = tmem + C::COL_P + i * C::P_STRIDE;
+    const uint32_t tO = tmem + C::COL_O + i * DH;
+    const uint32_t tP = tmem + C::COL_P + i * C::P_STRIDE + (j % C::P_BUFS) * (BKV / 2);
 #pragma unroll
     for (int kk = 0; kk < BKV / 16; ++kk)  // O_i (+)= P_i . V(j), P_i from TMEM
       umma_bf16_ts(tO, tP + kk * 8, desc_mn(va + kk * 2048, BKV * 128), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
-    umma_commit(&o_done[i]);
+    umma_commit(od(i, j));
     umma_commit(&kv_empty[st]);
     TRACE(2 + i, j, 1);
   };
@@ -762,7 +780,7 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
             const int vs = jl % VST;
             const uint32_t va = sb + C::OFF_V + vs * C::KB;
             for (int i = 0; i < nq; ++i) {
-              issuer_wait(&p_full[i], jl & 1);
+              issuer_wait(pf(i, jl), od_par(jl));
               if (i == 0) issuer_wait(&v_full[vs], (jl / VST) & 1);
               TRACE(2 + i, jl, 4);
               tc_fence_after();
@@ -772,7 +790,7 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
                 const uint32_t pcol = (kk / (KH / 16)) * KH + (kk % (KH / 16)) * 8;
                 umma_bf16_ts(tO, tP + pcol, desc_mn(va + kk * 2048, BKV * 128), idesc_pv, (jl > 0 || kk > 0) ? 1u : 0u);
               }
-              umma_commit(&o_done[i]);
+              umma_commit(od(i, jl));
               TRACE(2 + i, jl, 1);
               if (jl + 1 < nt) {
                 if (i == 0) issuer_wait(&k_full[(jl + 1) % KST], ((jl + 1) / KST) & 1);
@@ -889,7 +907,7 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
           }
           issuer_wait(&v_full[st], (it / ST) & 1);
           if (j > 0) TRACE(2 + i, ti, 4);
-          issuer_wait(&p_full[i], ti & 1);
+          issuer_wait(pf(i, ti), od_par(ti));
           if (j > 0) TRACE(2 + i, ti, 5);
           tc_fence_after();
           const uint32_t va = sb + C::OFF_V + st * C::KB;
@@ -907,7 +925,7 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
               umma_bf16_ts(tmem + C::COL_L + i * 16, tP + kk * 8, desc_k(oa + (kk & 3) * 32), idesc_l,
                            (j > 0 || kk > 0) ? 1u : 0u);
           }
-          umma_commit(&o_done[i]);
+          umma_commit(od(i, ti));
           TRACE(2 + i, ti, 1);
           umma_commit(SPLIT ? &v_empty[st] : &kv_empty[st]);
           if (C::ALIAS && more) {  // S_i overwrites P_i only after the P.V above (issue order)
@@ -1094,13 +1112,18 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
           if (!spec || any_need) exp_pass(m_used == -INFINITY ? 0.f : -m_used, false);
           // P_i (and O_i) are free once P_i.V(j-1) has retired (implied by s_full when P aliases S)
           if (j + 1 < nt) TRACE(i, ti, 3);
-          if (!PP && j > 0) {  // PP: S_i(j) landing already implies P.V_i(j-1) retired
-            mbar_wait(&o_done[i], (ti - 1) & 1);
-            tc_fence_after();
+          // (P double-buffered: P.V_i(j-2) frees this tile's buffer; a rescale of O needs P.V_i(j-1))
+          if (!PP) {  // PP: S_i(j) landing already implies P.V_i(j-1) retired
+            const int tw = rescale ? ti - 1 : ti - C::P_BUFS;
+            if (tw >= ti - j) {  // a P.V of this segment
+              mbar_wait(od(i, tw), od_par(tw));
+              tc_fence_after();
+            }
           }
           if (j + 1 < nt) TRACE(i, ti, 4);
+          const uint32_t tPb = tP + (ti % C::P_BUFS) * (BKV / 2);
 #pragma unroll
-          for (int c = 0; c < KH / 64; ++c) tmem_st32(tP + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[c * 32]));
+          for (int c = 0; c < KH / 64; ++c) tmem_st32(tPb + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[c * 32]));
           l += (s0 + s1) + (s2 + s3);
           if (C::LSUM && rescale) {  // L_i (tensor-core row sums) at the new scale too
             uint32_t lv[16];
@@ -1129,12 +1152,12 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
           tmem_st_wait();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&p_full[i]);
+          if (lane == 0) mbar_arrive(pf(i, ti));
           TRACE(i, ti, 0);
         }
         l = exchange(l, ti & 1, false);  // the parity the last tile did NOT use
         TRACE(i, ti, 1);
-        mbar_wait(&o_done[i], (ti - 1) & 1);
+        mbar_wait(od(i, ti - 1), od_par(ti - 1));
         tc_fence_after();
         if constexpr (C::LSUM) {  // the row sum of the bf16 P the tensor cores multiplied V by
           uint32_t lv[16];

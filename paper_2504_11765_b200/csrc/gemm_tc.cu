@@ -335,10 +335,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint64_t pol_w = ep.w_policy ? policy_evict_first() : pol_act;
       int stage = 0;
       uint32_t phase = 0;
+      const int pf = ep.b_pf;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         int mb, nb, kb0, kb1, sp;
         decode(u, mb, nb, kb0, kb1, sp);
+        // this CTA's share (k-blocks kb with kb % m_tiles == mb) of the B prefetch stream
+        auto prefetch_b = [&](int kb) {
+          if (kb < kb1 && kb % m_tiles == mb) tma_prefetch_2d(&tmB, kb * BK, nb * BN);
+        };
+        if (pf > 0)
+          for (int kb = kb0; kb < kb0 + pf; ++kb) prefetch_b(kb);
         for (int kb = kb0; kb < kb1; ++kb) {
+          if (pf > 0) prefetch_b(kb + pf);
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           tma_load_2d(&tmA, &full[stage], sA + stage * C::A_BYTES, kb * BK, mb * BM, pol_act);
@@ -490,9 +498,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint64_t pol_w = ep.w_policy ? policy_evict_first() : pol_act;
       int stage = 0;
       uint32_t phase = 0;
+      const int pf = ep.b_pf;
       for (int u = pair; u < units; u += npairs) {
         const int mb = u % m_tiles, nb = u / m_tiles;
+        // this CTA's half of B, k-blocks kb with kb % m_tiles == mb (the M tiles sharing the
+        // B tile split the prefetch stream)
+        auto prefetch_b = [&](int kb) {
+          if (kb >= kblocks || kb % m_tiles != mb) return;
+          if constexpr (BN == 384) {
+            tma_prefetch_2d(&tmB, kb * BK, nb * BN + (int)rank * 128);
+            tma_prefetch_2d(&tmB, kb * BK, nb * BN + (int)rank * 128 + 64);
+            tma_prefetch_2d(&tmB, kb * BK, nb * BN + 256 + (int)rank * 64);
+          } else {
+            tma_prefetch_2d(&tmB, kb * BK, nb * BN + (int)rank * (BN / 2));
+          }
+        };
+        if (pf > 0)
+          for (int kb = 0; kb < pf; ++kb) prefetch_b(kb);
         for (int kb = 0; kb < kblocks; ++kb) {
+          if (pf > 0) prefetch_b(kb + pf);
           mbar_wait(&empty[stage], phase ^ 1);
           if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * STAGE);
           const uint32_t bar = mapa_shared(smem_u32(&full[stage]), 0);
@@ -1170,6 +1194,9 @@ TilePlan pick_tiles(int M, int N, int K, bool allow192) {
   return plan;
 }
 
+#ifndef RDKV_GEMM_PF_DEFAULT
+#define RDKV_GEMM_PF_DEFAULT 0
+#endif
 int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long long ldb, int M, int N, int K,
                 int kind, int dh, const GemmEpi& ep_in, cudaStream_t stream, int bn) {
   // opt-in A/B knobs, measured no faster inside the C3 step (profiles/r2_l2_prefetch_ab.txt):
@@ -1183,8 +1210,13 @@ int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, l
     const char* e = std::getenv("RDKV_L2_PREFETCH");
     return e && e[0] == '1';
   }();
+  static const int b_pf = [] {
+    const char* e = std::getenv("RDKV_GEMM_PF");  // weight L2 prefetch distance in k-blocks
+    return e ? std::atoi(e) : RDKV_GEMM_PF_DEFAULT;
+  }();
   GemmEpi ep = ep_in;
   ep.w_policy = wpol;
+  ep.b_pf = b_pf;
   if (!l2pf) ep.l2_next = nullptr;
   if (M <= 0 || N <= 0) return 0;
   if (K <= 0 || K % BK != 0) return set_error(RDKV_ERR_ARG, "gemm: K=%d must be a positive multiple of 64", K);

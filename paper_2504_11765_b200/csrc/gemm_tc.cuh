@@ -72,6 +72,11 @@ struct GemmEpi {
   // in this kernel: streaming it evict-first keeps the prefetched next weights resident).
   // Set by launch_gemm (RDKV_GEMM_WPOL, default 0).
   int w_policy;
+  // L2 prefetch of this GEMM's own weight (B) tiles b_pf k-blocks ahead of the TMA loads
+  // (cp.async.bulk.prefetch.tensor, duty spread over the M tiles sharing a B tile): the
+  // smem ring holds only a few k-blocks, too little to cover DRAM latency when a
+  // single-wave GEMM streams its weights cold.  0 = off.  Set by launch_gemm (RDKV_GEMM_PF).
+  int b_pf;
 };
 
 // True when launch_gemm will take the split-K path for this shape (small M).
