@@ -65,6 +65,9 @@ static int make_tmap_q(CUtensorMap* m, const void* q, long long tokens, int hq, 
 #ifndef RDKV_ATTN_BYKIND
 #define RDKV_ATTN_BYKIND 1  // MMA issuers by kind and Q tile (Q.K^T_0, Q.K^T_1, P.V_0, P.V_1) instead of one per Q tile
 #endif
+#ifndef RDKV_ATTN_QTMEM
+#define RDKV_ATTN_QTMEM 1  // Q tile 0 in TMEM for its Q.K^T (issuers by kind, dh = 128)
+#endif
 #ifndef RDKV_ATTN_PDB
 #define RDKV_ATTN_PDB 0  // 1: double-buffered P with the issuers by kind (dh = 128)
 #endif
@@ -142,6 +145,12 @@ struct TcCfg {
   static constexpr uint32_t P_STRIDE = ALIAS ? BKV : P_BUFS * BKV / 2;  // per Q tile (all P buffers)
   static_assert(COL_P + 2 * P_STRIDE <= 512, "TMEM: P does not fit");
   static constexpr uint32_t COL_L = COL_P + 2 * P_STRIDE;     // L_i at COL_L + 16 i (LSUM)
+  // RDKV_ATTN_QTMEM (BYK, dh = 128, single P buffer): Q tile 0 staged in the last 64 TMEM columns
+  // (tcgen05.cp), so its Q.K^T reads only K from smem: M = 128, N = 64 MMAs are smem-bound at
+  // 48 cycles with both operands in smem (4 KB of Q + 2 KB of K per K = 16 step)
+  static constexpr bool QTMEM = RDKV_ATTN_QTMEM && BYK && DH == 128 && P_BUFS == 1;
+  static constexpr uint32_t COL_Q0 = COL_P + 2 * P_STRIDE;
+  static_assert(!QTMEM || COL_Q0 + DH / 2 <= 512, "TMEM: Q tile 0 does not fit");
   static_assert(!LSUM || COL_L + 32 <= 512, "TMEM: L columns do not fit");
   static_assert(COL_O + 2 * DH <= 512, "TMEM: S and O do not fit");
 };
@@ -821,6 +830,13 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
           issuer_wait(&q_full[i], 0);
           const uint32_t qa = sb + C::OFF_Q + i * C::QB;
           const uint32_t tS = tmem + C::COL_S + i * BKV;
+          const bool q_in_tmem = C::QTMEM && i == 0;
+          if (q_in_tmem) {  // stage Q_0 in TMEM: one 128 x 16 slice per K = 16 step, same descriptors as the MMA
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < DH / 16; ++kk)
+              tmem_cp_128x256b(tmem + C::COL_Q0 + kk * 8, desc_k(qa + (kk >> 2) * (ROWS * 128) + (kk & 3) * 32));
+          }
           for (int j = 0; j < nt; ++j) {
             const int st = j % ST;
             issuer_wait(&k_full[st], (j / ST) & 1);
@@ -828,11 +844,18 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
             TRACE(2 + i, j, 2);
             tc_fence_after();
             const uint32_t ka = sb + C::OFF_K + st * C::KB;
+            if (q_in_tmem) {
 #pragma unroll
-            for (int kk = 0; kk < DH / 16; ++kk) {
-              const uint32_t sub = (kk & 3) * 32;
-              umma_bf16(tS, desc_k(qa + (kk >> 2) * (ROWS * 128) + sub), desc_k(ka + (kk >> 2) * (BKV * 128) + sub),
-                        idesc_qk, kk > 0 ? 1u : 0u);
+              for (int kk = 0; kk < DH / 16; ++kk)
+                umma_bf16_ts(tS, tmem + C::COL_Q0 + kk * 8, desc_k(ka + (kk >> 2) * (BKV * 128) + (kk & 3) * 32),
+                             idesc_qk, kk > 0 ? 1u : 0u);
+            } else {
+#pragma unroll
+              for (int kk = 0; kk < DH / 16; ++kk) {
+                const uint32_t sub = (kk & 3) * 32;
+                umma_bf16(tS, desc_k(qa + (kk >> 2) * (ROWS * 128) + sub), desc_k(ka + (kk >> 2) * (BKV * 128) + sub),
+                          idesc_qk, kk > 0 ? 1u : 0u);
+              }
             }
             umma_commit(&s_full[i]);
             if (j + 1 == nt) umma_commit(&q_empty[i]);

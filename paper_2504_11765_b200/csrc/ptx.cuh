@@ -243,6 +243,14 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, u
       : "memory");
 }
 
+// smem -> TMEM copy of one 128-row x 256-bit (16 bf16 of K) operand slice described by a
+// shared-memory matrix descriptor (same layout rules as an MMA operand), e.g. to stage an
+// A operand in TMEM for tcgen05.mma [d], [a_tmem], b_desc.  Ordered with this thread's
+// later tcgen05.mma (both run in the tensor pipe in issue order).
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t tmem_dst, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(tmem_dst), "l"(sdesc) : "memory");
+}
+
 // Packed fp32 pair ops (FFMA2 / FADD2 / FMUL2): two lanes of fp32 math per issue slot.
 __device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1, float c0,
                                       float c1) {
