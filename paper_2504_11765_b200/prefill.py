@@ -37,27 +37,43 @@ class PrefillRequest:
 
 
 @dataclass
+class LiveSequence:
+    """A prefilled sequence kept alive for decoding (``prefill_batch(keep=True)``): its pool
+    blocks hold the KV of positions [0, n_ctx); ``owned`` are the blocks it allocated
+    (released by ``decode.retire``), ``pinned`` the HBM-tier entry whose blocks it shares."""
+    blocks: list
+    owned: list
+    n_ctx: int
+    pinned: KvKey | None = None
+
+
+@dataclass
 class PrefillResult:
     ttft: float
     breakdown: TtftBreakdown
     logits: torch.Tensor              # [S, V] fp32 on the device
     next_token: torch.Tensor          # [S] int32 on the device
+    sequences: list | None = None     # LiveSequence per request when keep=True
 
 
 def prefill_batch(engine: Engine, requests: Sequence[PrefillRequest], timed: bool = True,
                   unpack_events: list | None = None, use_graph: bool = True,
-                  stream_layers: bool = True) -> PrefillResult:
+                  stream_layers: bool = True, keep: bool = False) -> PrefillResult:
     """Serve a batch of queries on one engine; kv_load / prefill are the
     device-measured durations of the whole batch's load and prefill phases.
     ``unpack_events`` collects (start, end) CUDA events around the K3 launch.
     Untimed calls replay a per-shape CUDA graph (``Engine.graphs``); its output
-    tensors are reused by the next call of the same shape."""
+    tensors are reused by the next call of the same shape.  ``keep`` hands every
+    sequence's pool blocks (and its HBM-tier pin) to the caller as
+    ``result.sequences`` for decoding (``decode.py``) instead of releasing them."""
     pool = engine.pool
     main = torch.cuda.current_stream(engine.device)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if timed else None
     if timed:
         ev[0].record(main)
     seqs, owned, jobs, staged, pending_h2d, pinned = [], [], [], [], [], []
+    pin_of: dict[int, KvKey] = {}
+    kept = False
     bs = pool.block_size
     # staging buffers are allocated on `main`; the copy stream must not write
     # them before main's earlier users of that memory are done
@@ -70,6 +86,7 @@ def prefill_batch(engine: Engine, requests: Sequence[PrefillRequest], timed: boo
             entry = engine.resident.acquire(r.key) if hit and r.key is not None else None
             if entry is not None:
                 pinned.append(r.key)
+                pin_of[i] = r.key
             if hit and r.lookup.blob is None and entry is None:
                 raise ValueError(f"request {i}: an HBM-tier hit needs the prefix resident in the pool")
             n_cached = (entry.n_tokens if r.lookup.blob is None else int(r.lookup.blob.header.token_count)) \
@@ -163,12 +180,18 @@ def prefill_batch(engine: Engine, requests: Sequence[PrefillRequest], timed: boo
         for d in staged:  # keep staging buffers alive until the stream has consumed them
             d.record_stream(main)
         bd = TtftBreakdown(kv_load, prefill)
-        return PrefillResult(bd.total, bd, logits, nxt)
+        live = None
+        if keep:
+            live = [LiveSequence(list(sp.blocks), list(own), int(sp.n_cached + len(sp.tokens)), pin_of.get(i))
+                    for i, (sp, own) in enumerate(zip(seqs, owned))]
+            kept = True
+        return PrefillResult(bd.total, bd, logits, nxt, live)
     finally:
-        for b in owned:
-            pool.release(b)
-        for k in pinned:
-            engine.resident.unpin(k)
+        if not kept:
+            for b in owned:
+                pool.release(b)
+            for k in pinned:
+                engine.resident.unpin(k)
 
 
 def prefill_with_cached_prefix(engine: Engine, lookup: LookupResult, prefix_tokens, new_tokens,
