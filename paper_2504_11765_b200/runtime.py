@@ -52,6 +52,7 @@ from .generator import KvGenerator
 from .model import combo_tokens, query_tokens
 from .multi import owner_rank
 from .prefetch import PendingQuery, scan
+from . import decode
 from .prefill import PrefillRequest, prefill_batch
 from .store import CacheTier, KvKey, KvStore, LookupResult, Outcome
 
@@ -77,6 +78,11 @@ class RuntimeConfig:
     cost_aware: bool = False
     disk_gbps: float = 3.4              # sustained cold read of the shared store (bench / disk probe)
     prefill_s_per_token: float = 1.1e-5 # measured full-prefill cost per prefix token on this GPU
+    # Decode after the first token (decode.py; the reference's decode_tokens, sim.py:572-573):
+    # every query generates this many more tokens greedily; the instance batches them
+    # continuously (new queries' prefills join between decode steps, finished ones leave).
+    # A query is DONE when its last token is out; TTFT stays the first token's.
+    decode_tokens: int = 0
 
     def __post_init__(self) -> None:
         if self.persist not in ("all", "composite", "none"):
@@ -96,6 +102,9 @@ class QueryResult:
     origins: tuple              # per prefix j: generated | hbm | peer | memory | disk | miss_raw
     batch: int                  # queries in the serving batch
     token: int                  # first token
+    done: float = 0.0           # last token out (decode_tokens > 0; = first_token otherwise)
+    n_tokens: int = 1           # tokens generated, the first one included
+    tokens: tuple = ()          # every generated token (decode_tokens > 0)
 
     @property
     def latency(self) -> float:
@@ -172,6 +181,7 @@ class Instance:
         self.generated: list[tuple[int, tuple]] = []     # (requesting query index, prefix ids) per key made here
         self._gen_for: dict[tuple, int] = {}             # prefix ids -> query index that triggered it
         self._unpins: list = []                           # (event, key): peer pins to drop once copies land
+        self._live: list = []                             # (decode.DecodeSeq, result index) being decoded
         self._writer = _Writer(store, cp)
         self._threads: list[threading.Thread] = []
         self.errors: list = []
@@ -283,20 +293,45 @@ class Instance:
     # ------------------------------------------------------------ serving
     def _serve_loop(self) -> None:
         with torch.cuda.stream(self.serve_stream):
-            while not self.stopping():
-                self._drain_unpins()
-                batch = self._take_batch()
-                if not batch:
-                    time.sleep(self.cfg.idle_sleep_s)
-                    continue
-                self._serve(batch)
+            try:
+                while not self.stopping():
+                    self._drain_unpins()
+                    room = self.cfg.max_batch - len(self._live)
+                    batch = self._take_batch(room) if room > 0 else []
+                    if batch:
+                        self._serve(batch)
+                    if self._live:
+                        self._decode_step()
+                    elif not batch:
+                        time.sleep(self.cfg.idle_sleep_s)
+            finally:
+                for seq, _ in self._live:
+                    decode.retire(self.eng, seq)
+                self._live = []
 
-    def _take_batch(self) -> list:
+    def _decode_step(self) -> None:
+        """One decode step for every live sequence (continuous batching); finished
+        sequences leave the batch, their queries become DONE."""
+        decode.step(self.eng, [s for s, _ in self._live])
+        now = time.monotonic()
+        keep = []
+        for seq, ri in self._live:
+            if seq.done:
+                res = self.results[ri]
+                res.done, res.n_tokens, res.tokens = now, len(seq.tokens), tuple(seq.tokens)
+                decode.retire(self.eng, seq)
+                self.cp.qstate_cas(res.index, QState.DISPATCHED, QState.DONE)
+            else:
+                keep.append((seq, ri))
+        self._live = keep
+
+    def _take_batch(self, limit: int | None = None) -> list:
         """An idle instance takes the oldest waiting queries (up to max_batch /
         max_batch_tokens new tokens; the reference dispatches one query per idle
         instance, sim.py:403-409 — batching only groups what already waits)."""
         out, tokens = [], 0
-        while len(out) < self.cfg.max_batch:
+        limit = self.cfg.max_batch if limit is None else limit
+        while len(out) < limit:
             q = self.cp.pop_query()
             if q is None:
                 break
@@ -351,13 +386,18 @@ class Instance:
                             else ("miss_raw" if s is None else s) for j, s in enumerate(srcs, 1))
             reqs.append(req)
             meta.append((index, qid, arrival, best, source, origins))
-        r = prefill_batch(self.eng, reqs, timed=False, use_graph=False)
+        dec = cfg.decode_tokens > 0
+        r = prefill_batch(self.eng, reqs, timed=False, use_graph=False, keep=dec)
         first = r.next_token.cpu()  # D2H of the first tokens: the batch's TTFT point
         t_first = time.monotonic()
-        for (index, qid, arrival, best, source, origins), tok in zip(meta, first.tolist()):
+        for i, ((index, qid, arrival, best, source, origins), tok) in enumerate(zip(meta, first.tolist())):
             self.results.append(QueryResult(index, qid, self.rank, arrival, t_dispatch, t_first, best, source,
-                                            origins, len(batch), int(tok)))
-            self.cp.qstate_cas(index, QState.DISPATCHED, QState.DONE)
+                                            origins, len(batch), int(tok), t_first))
+            if dec:  # keeps its KV: decoded by the next steps, DONE with its last token
+                self._live.append((decode.DecodeSeq(r.sequences[i], int(tok), cfg.decode_tokens + 1, [int(tok)]),
+                                   len(self.results) - 1))
+            else:
+                self.cp.qstate_cas(index, QState.DISPATCHED, QState.DONE)
 
     def _disk_loses(self, n_tokens: int) -> bool:
         """Cost-aware dispatch: is reading ``n_tokens`` of cached KV from disk predicted
@@ -528,7 +568,9 @@ def summarize(results: Sequence[QueryResult], tries: Sequence[Sequence[QueryResu
     lat = np.array([r.latency for r in results])
     ttft = np.array([r.ttft for r in results])
     groups = tries if tries is not None else [results]
-    spans = [max(r.first_token for r in g) - min(r.arrival for r in g) for g in groups if g]
+    # a try ends with its last token out (the first token unless queries decode: the reference
+    # adds decode time to the batch span, sim.py:572-573)
+    spans = [max(max(r.first_token, r.done) for r in g) - min(r.arrival for r in g) for g in groups if g]
     origins: dict[str, int] = {}
     sources: dict[str, int] = {}
     for r in results:
@@ -543,7 +585,20 @@ def summarize(results: Sequence[QueryResult], tries: Sequence[Sequence[QueryResu
         "latency_ms": pct(lat), "ttft_ms": pct(ttft),
         "mean_batch": float(np.mean([r.batch for r in results])),
         "sources": dict(sorted(sources.items())), "origins": dict(sorted(origins.items())),
+        **_decode_summary(results, spans),
     }
+
+
+def _decode_summary(results: Sequence[QueryResult], spans) -> dict:
+    dec = [r for r in results if r.n_tokens > 1]
+    if not dec:
+        return {}
+    tpot = np.array([(r.done - r.first_token) / (r.n_tokens - 1) for r in dec])
+    toks = sum(r.n_tokens for r in results)
+    return {"decode": {"queries": len(dec), "tokens": int(toks),
+                       "tokens_per_s": toks / sum(spans) if sum(spans) > 0 else 0.0,
+                       "tpot_ms": {"p50": float(np.percentile(tpot, 50) * 1e3),
+                                   "p99": float(np.percentile(tpot, 99) * 1e3)}}}
 
 
 def arrivals_for_try(items: Sequence, rate: float, seed: int, try_index: int) -> list[tuple[float, object]]:

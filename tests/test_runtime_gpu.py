@@ -224,3 +224,61 @@ def test_cost_aware_dispatch(disk_gbps, expect_disk):
             assert rep["sources"].get("miss", 0) == len(items)
             assert rep["counters"]["disk_skipped"] == len(items)
         _check_tokens(out["results"], expected)
+
+
+def test_runtime_continuous_batching_decode():
+    """decode_tokens > 0: every query generates more tokens after its first one while new
+    queries' prefills join the running batch between decode steps.  Each query's tokens
+    equal a stand-alone greedy decode of its full prompt where the margins are clear, all
+    pool blocks come back, and the summary reports decode throughput / TPOT."""
+    from paper_2504_11765_b200 import decode
+    from paper_2504_11765_b200.engine import Engine
+    from paper_2504_11765_b200.model import combo_tokens, get_spec, query_tokens
+    from paper_2504_11765_b200.prefill import PrefillRequest
+    from paper_2504_11765_b200.runtime import RuntimeConfig, serve
+    from paper_2504_11765_b200.store import KvStore, LookupResult, Outcome
+
+    spec = get_spec("gqa-small-128")
+    k, n_dec = 3, 6
+    eng = Engine(spec, seed=0, pool_tokens=32768, device_cache_bytes=64 << 20)
+    items = _items(n=12, k=k)
+    # reference: each full prompt decoded alone (miss path), with the top-2 margin of every step
+    ref = {}
+    for it in items:
+        toks = np.concatenate([combo_tokens(it.doc_ids[:k], it.doc_tokens[:k], spec.vocab),
+                               query_tokens(it.query_id, it.q_tokens, spec.vocab)])
+        seqs = decode.start(eng, [PrefillRequest(LookupResult(Outcome.MISS), toks[:0], toks)], n_dec + 1)
+        margins = []
+        try:
+            while not seqs[0].done:
+                decode.step(eng, seqs)
+                top = torch.topk(eng._decode_step.logits[0].float(), 2).values
+                margins.append(float(top[0] - top[1]))
+            ref[it.query_id] = (list(seqs[0].tokens), margins)
+        finally:
+            decode.retire(eng, seqs[0])
+    free0 = eng.pool.free_blocks
+    with tempfile.TemporaryDirectory() as root:
+        cfg = RuntimeConfig(k=k, threshold=0.0, max_batch=4, persist="all", decode_tokens=n_dec)
+        out = serve(eng, KvStore(root, memory_capacity_bytes=0), cfg, items, rate=400.0, tries=1)
+    rep = out["summary"]
+    assert rep["queries"] == len(items)
+    assert rep["decode"]["queries"] == len(items) and rep["decode"]["tokens"] == len(items) * (n_dec + 1)
+    assert rep["decode"]["tpot_ms"]["p50"] > 0 and rep["decode"]["tokens_per_s"] > 0
+    compared = 0
+    for r in out["results"]:
+        assert r.n_tokens == n_dec + 1 and len(r.tokens) == n_dec + 1 and r.done >= r.first_token
+        assert r.tokens[0] == r.token
+        toks, margins = ref[r.query_id]
+        # same greedy continuation until a near-tie step (margin < 0.05) lets bf16 noise pick
+        # the other token; the first token is covered by _check_tokens' rule
+        if r.token != toks[0]:
+            continue
+        for j in range(1, n_dec + 1):
+            if margins[j - 1] < 0.05:
+                break
+            assert r.tokens[j] == toks[j], (r.query_id, j, r.tokens, toks)
+            compared += 1
+    assert compared >= len(items)
+    eng.resident.clear()
+    assert eng.pool.free_blocks == free0
