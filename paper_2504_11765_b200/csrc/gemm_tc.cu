@@ -685,20 +685,36 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_trigger();
-  pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol_act = policy_evict_last();
-      int stage = 0;
+      // The weights are never written by the preceding kernels: the first unit's first
+      // STAGES weight tiles are requested BEFORE griddepcontrol.wait, so their cold DRAM
+      // latency overlaps the predecessor's tail (programmatic dependent launch); the
+      // activation tiles (the predecessor's output) follow once it has completed.
+      int pre = 0;
+      if (blockIdx.x < units) {
+        const int wt = blockIdx.x / splits, sp = blockIdx.x % splits;
+        const int kb0 = sp * kb_per, kb1 = min(kb0 + kb_per, kblocks);
+        pre = min(STAGES, kb1 - kb0);
+        for (int s = 0; s < pre; ++s) {
+          mbar_arrive_expect_tx(&full[s], STAGE);
+          tma_load_2d_nohint(&tmW, &full[s], sW + s * W_BYTES, (kb0 + s) * BK, wt * 128);
+        }
+      }
+      pdl_wait();
+      int stage = 0, n = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const int wt = u / splits, sp = u % splits;
         const int kb0 = sp * kb_per, kb1 = min(kb0 + kb_per, kblocks);
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], STAGE);
-          tma_load_2d_nohint(&tmW, &full[stage], sW + stage * W_BYTES, kb * BK, wt * 128);
+        for (int kb = kb0; kb < kb1; ++kb, ++n) {
+          if (n >= pre) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], STAGE);
+            tma_load_2d_nohint(&tmW, &full[stage], sW + stage * W_BYTES, kb * BK, wt * 128);
+          }
           tma_load_2d(&tmX, &full[stage], sX + stage * X_BYTES, kb * BK, 0, pol_act);
           if (++stage == STAGES) {
             stage = 0;
@@ -737,6 +753,7 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {
+    pdl_wait();  // the split-K scratch may still be read by the predecessor's finalize
     const int wq = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -798,8 +815,10 @@ __global__ void __launch_bounds__(256) splitk_finalize_kernel(const float* __res
   const int row = blockIdx.x;
   const long long slab = (long long)M * N;
   const float* pr = part + (long long)row * N;
+  // splits summed in order (deterministic); unrolled so the partial loads are in flight together
   auto sum4 = [&](int col) {
     float4 s = *reinterpret_cast<const float4*>(pr + col);
+#pragma unroll 4
     for (int k = 1; k < splits; ++k) {
       const float4 t = *reinterpret_cast<const float4*>(pr + k * slab + col);
       s.x += t.x;
@@ -821,6 +840,7 @@ __global__ void __launch_bounds__(256) splitk_finalize_kernel(const float* __res
     for (int k = 0; k < PER; ++k) {
       const int col = g * DH + lane + 32 * k;
       float t = pr[col];
+#pragma unroll 4
       for (int q = 1; q < splits; ++q) t += pr[q * slab + col];
       v[k] = t;
     }
@@ -882,33 +902,55 @@ __global__ void __launch_bounds__(256) splitk_finalize_kernel(const float* __res
 
 // RESID finalize with the following RMSNorm fused in (one CTA per row, N <= 8192):
 // x = resid + sum(partials) -> bf16 -> out; h = x * rsqrt(mean(x^2) + eps) * gain -> norm_out.
-__global__ void __launch_bounds__(256) splitk_resid_norm_kernel(const float* __restrict__ part, int splits, int M,
-                                                                int N, GemmEpi ep) {
-  constexpr int MAXC = 8;
+// 1024 threads x <= 2 float4 chunks; every split's partial of a chunk is requested before
+// any is summed (a decode step has only M = 16 rows = 16 CTAs: the kernel is latency-bound,
+// so the loads must all be in flight at once), summed in split order (deterministic).
+constexpr int RN_THREADS = 1024, RN_MAXC = 2, RN_G = 4;
+__global__ void __launch_bounds__(RN_THREADS) splitk_resid_norm_kernel(const float* __restrict__ part, int splits,
+                                                                       int M, int N, GemmEpi ep) {
   pdl_trigger();
   pdl_wait();
   const int row = blockIdx.x;
   const long long slab = (long long)M * N;
   const float* pr = part + (long long)row * N;
-  float xs[MAXC][4];
+  float xs[RN_MAXC][4];
   float ss = 0.f;
+  float4 t[RN_MAXC];
+  uint2 rr[RN_MAXC];
 #pragma unroll
-  for (int c = 0; c < MAXC; ++c) {
-    const int j = (c * 256 + threadIdx.x) * 4;
+  for (int c = 0; c < RN_MAXC; ++c) {
+    const int j = (c * RN_THREADS + threadIdx.x) * 4;
+    t[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (j < N) rr[c] = *reinterpret_cast<const uint2*>(ep.resid + (long long)row * ep.ldr + j);
+  }
+  for (int k0 = 0; k0 < splits; k0 += RN_G) {  // RN_G splits x every chunk in flight per round
+    float4 u[RN_MAXC][RN_G];
+#pragma unroll
+    for (int c = 0; c < RN_MAXC; ++c) {
+      const int j = (c * RN_THREADS + threadIdx.x) * 4;
+#pragma unroll
+      for (int g = 0; g < RN_G; ++g)
+        if (j < N && k0 + g < splits) u[c][g] = __ldcg(reinterpret_cast<const float4*>(pr + (k0 + g) * slab + j));
+    }
+#pragma unroll
+    for (int c = 0; c < RN_MAXC; ++c)
+#pragma unroll
+      for (int g = 0; g < RN_G; ++g)
+        if (k0 + g < splits) {  // split order: bit-identical to a serial sum
+          t[c].x += u[c][g].x;
+          t[c].y += u[c][g].y;
+          t[c].z += u[c][g].z;
+          t[c].w += u[c][g].w;
+        }
+  }
+#pragma unroll
+  for (int c = 0; c < RN_MAXC; ++c) {
+    const int j = (c * RN_THREADS + threadIdx.x) * 4;
     if (j < N) {
-      float4 t = *reinterpret_cast<const float4*>(pr + j);
-      for (int k = 1; k < splits; ++k) {
-        const float4 u = *reinterpret_cast<const float4*>(pr + k * slab + j);
-        t.x += u.x;
-        t.y += u.y;
-        t.z += u.z;
-        t.w += u.w;
-      }
-      const uint2 r = *reinterpret_cast<const uint2*>(ep.resid + (long long)row * ep.ldr + j);
-      const float2 a = unpack_bf16(r.x), b = unpack_bf16(r.y);
+      const float2 a = unpack_bf16(rr[c].x), b = unpack_bf16(rr[c].y);
       uint2 w;
-      w.x = pack_bf16(t.x + a.x, t.y + a.y);
-      w.y = pack_bf16(t.z + b.x, t.w + b.y);
+      w.x = pack_bf16(t[c].x + a.x, t[c].y + a.y);
+      w.y = pack_bf16(t[c].z + b.x, t[c].w + b.y);
       *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + j) = w;
       const float2 p0 = unpack_bf16(w.x), p1 = unpack_bf16(w.y);  // normalise the rounded residual
       xs[c][0] = p0.x;
@@ -918,17 +960,17 @@ __global__ void __launch_bounds__(256) splitk_resid_norm_kernel(const float* __r
       ss += p0.x * p0.x + p0.y * p0.y + p1.x * p1.x + p1.y * p1.y;
     }
   }
-  __shared__ float red[8];
+  __shared__ float red[RN_THREADS / 32];
   for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
   float tot = 0.f;
 #pragma unroll
-  for (int w = 0; w < 8; ++w) tot += red[w];
+  for (int w = 0; w < RN_THREADS / 32; ++w) tot += red[w];
   const float inv = rsqrtf(tot / (float)N + ep.norm_eps);
 #pragma unroll
-  for (int c = 0; c < MAXC; ++c) {
-    const int j = (c * 256 + threadIdx.x) * 4;
+  for (int c = 0; c < RN_MAXC; ++c) {
+    const int j = (c * RN_THREADS + threadIdx.x) * 4;
     if (j < N) {
       const float4 g = *reinterpret_cast<const float4*>(ep.norm_gain + j);
       uint2 w;
@@ -1058,8 +1100,9 @@ int finalize(int kind, int dh, const float* part, int splits, int M, int N, cons
     case EPI_STORE_F32: return launch_finalize<EPI_STORE_F32, 0>(part, splits, M, N, ep, stream);
     case EPI_RESID:
       if (ep.norm_out) {
-        if (N > 8192 || N % 4) return set_error(RDKV_ERR_ARG, "resid+norm finalize: N must be <= 8192, %% 4");
-        CUDA_TRY(launch_k(splitk_resid_norm_kernel, dim3(M), dim3(256), 0, stream, part, splits, M, N, ep));
+        if (N > RN_THREADS * RN_MAXC * 4 || N % 4)
+          return set_error(RDKV_ERR_ARG, "resid+norm finalize: N must be <= 8192, %% 4");
+        CUDA_TRY(launch_k(splitk_resid_norm_kernel, dim3(M), dim3(RN_THREADS), 0, stream, part, splits, M, N, ep));
         return 0;
       }
       return launch_finalize<EPI_RESID, 0>(part, splits, M, N, ep, stream);
