@@ -1321,11 +1321,15 @@ __global__ void __launch_bounds__(256) attn_split_combine_kernel(AttnParams p) {
   pdl_wait();
   const int t = blockIdx.x, head = blockIdx.y * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (head >= p.hq || t < p.seq_start[p.seq_off]) return;  // tokens of this launch's sequences only
+  // (split loops unrolled: the partials' loads are in flight together — a single-query
+  // combine is latency-bound; summation order unchanged, so results are bit-identical)
   float M = -INFINITY;
+#pragma unroll 8
   for (int k = 0; k < p.kv_splits; ++k) M = fmaxf(M, p.split_ml[((long long)k * p.n_tokens + t) * p.hq + head].x);
   constexpr int PER = DH / 32;
   float acc[PER] = {};
   float L = 0.f;
+#pragma unroll 4
   for (int k = 0; k < p.kv_splits; ++k) {
     const float2 ml = p.split_ml[((long long)k * p.n_tokens + t) * p.hq + head];
     if (ml.x == -INFINITY) continue;

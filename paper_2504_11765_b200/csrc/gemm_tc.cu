@@ -828,6 +828,23 @@ __global__ void __launch_bounds__(256) splitk_finalize_kernel(const float* __res
     }
     return s;
   };
+  // RMSNorm fused across GEMMs (QKV / SwiGLU consumers): this row's rsqrt, reduced once per
+  // CTA from the producer's per-chunk sums of squares (fixed order: deterministic)
+  float rs = 1.f;
+  if constexpr (EPI == EPI_QKV || EPI == EPI_SWIGLU) {
+    if (ep.ssq_in) {
+      __shared__ float red[8];
+      float v = 0.f;
+      for (int c = threadIdx.x; c < ep.ssq_parts; c += blockDim.x) v += ep.ssq_in[(long long)c * M + row];
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+      __syncthreads();
+      float t = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) t += red[w];
+      rs = rsqrtf(t / (float)ep.ssq_dim + ep.norm_eps);
+    }
+  }
   if constexpr (EPI == EPI_QKV) {
     // one warp per head (8 heads per CTA); lane owns elements lane + 32k, so RoPE
     // pairs (i, i + DH/2) stay in-lane
@@ -842,7 +859,7 @@ __global__ void __launch_bounds__(256) splitk_finalize_kernel(const float* __res
       float t = pr[col];
 #pragma unroll 4
       for (int q = 1; q < splits; ++q) t += pr[q * slab + col];
-      v[k] = t;
+      v[k] = t * rs;
     }
     if (g < ep.hq + ep.hkv) {
       const float2* cs = reinterpret_cast<const float2*>(ep.rope) + (long long)p * (DH / 2);
@@ -867,15 +884,19 @@ __global__ void __launch_bounds__(256) splitk_finalize_kernel(const float* __res
     const int j = (blockIdx.y * 256 + threadIdx.x) * 4;  // 4 outputs inside one 64-block
     if (j >= N / 2) return;
     const int gc = (j / 64) * 128 + (j % 64);
-    const float4 g = sum4(gc), u = sum4(gc + 64);
+    float4 g = sum4(gc), u = sum4(gc + 64);
+    if (ep.ssq_in) {
+      g = make_float4(g.x * rs, g.y * rs, g.z * rs, g.w * rs);
+      u = make_float4(u.x * rs, u.y * rs, u.z * rs, u.w * rs);
+    }
     uint2 w;
     w.x = pack_bf16(silu(g.x) * u.x, silu(g.y) * u.y);
     w.y = pack_bf16(silu(g.z) * u.z, silu(g.w) * u.w);
     *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + j) = w;
   } else {
     const int j = (blockIdx.y * 256 + threadIdx.x) * 4;
-    if (j >= N) return;
-    float4 s = sum4(j);
+    if (EPI != EPI_RESID && j >= N) return;  // RESID: every lane joins the chunk sums below
+    float4 s = j < N ? sum4(j) : make_float4(0.f, 0.f, 0.f, 0.f);
     if constexpr (EPI == EPI_STORE_F32) {
       *reinterpret_cast<float4*>(static_cast<float*>(ep.out) + (long long)row * ep.ldo + j) = s;
     } else {
@@ -894,7 +915,17 @@ __global__ void __launch_bounds__(256) splitk_finalize_kernel(const float* __res
         for (int p = 0; p < ep.npush; ++p) *reinterpret_cast<uint2*>(ep.push[p] + (long long)row * ep.ldo + j) = w;
         __threadfence_system();
       } else {
-        *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + j) = w;
+        if (j < N) *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(ep.out) + (long long)row * ep.ldo + j) = w;
+        if constexpr (EPI == EPI_RESID) {
+          if (ep.ssq_out) {  // the next RMSNorm's statistics: per 32-column chunk (8 lanes), bf16 outputs
+            const float2 p0 = unpack_bf16(w.x), p1 = unpack_bf16(w.y);
+            float ss = j < N ? (p0.x * p0.x + p0.y * p0.y) + (p1.x * p1.x + p1.y * p1.y) : 0.f;
+            ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+            ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+            ss += __shfl_xor_sync(0xffffffffu, ss, 4);
+            if ((threadIdx.x & 7) == 0 && j < N) ep.ssq_out[(long long)(j >> 5) * M + row] = ss;
+          }
+        }
       }
     }
   }
