@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 #include "common.cuh"
 #include "gemm_tc.cuh"
 #include "pdl.cuh"
@@ -642,10 +643,17 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int 
 // unit (128 weight rows, K split) writes fp32 partial rows part[split][m][n]
 // (thread = weight row n, so a warp writes 32 consecutive n per token: coalesced);
 // splitk_finalize applies the fused epilogue.
-template <int NT>
+//
+// EPI != EPI_PARTIAL (fused small-M path): no finalize kernel.  With one split the epilogue
+// warps apply the epilogue straight from TMEM; otherwise every split's CTA writes its partial,
+// and the CTA whose atomic ticket on the weight tile comes last (after a __threadfence)
+// sums the partials in split order (deterministic) and applies the epilogue for that tile's
+// 128 output columns.  Norms use the per-chunk sum-of-squares scheme (ep.ssq_out / ssq_in).
+template <int NT, int EPI = EPI_PARTIAL, int DH = 0>
 __global__ void __launch_bounds__(256, 1)
     gemm_swapab_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, int M, int N,
-                       int K, int splits, float* __restrict__ part) {
+                       int K, int splits, float* __restrict__ part, GemmEpi ep) {
+  constexpr bool FUSED = EPI != EPI_PARTIAL;
   constexpr int STAGES = NT >= 128 ? 6 : 8;
   constexpr uint32_t W_BYTES = 128 * BK * 2, X_BYTES = NT * BK * 2, STAGE = W_BYTES + X_BYTES;
   constexpr uint32_t ACC = NT < 32 ? 32 : NT;  // accumulator column stride (tcgen05.ld reads 32 columns)
@@ -755,24 +763,165 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp >= 4) {
     pdl_wait();  // the split-K scratch may still be read by the predecessor's finalize
     const int wq = warp & 3;
+    const int r = wq * 32 + lane;  // weight row within the tile == output column offset
     int acc = 0;
     uint32_t acc_phase = 0;
+    // fused epilogue scratch (after the stage ring): RoPE / SwiGLU partner exchange [32][128] fp32,
+    // per-row RMSNorm scales [128], the last-split flag
+    float* xs = reinterpret_cast<float*>(smem + STAGES * STAGE + 1024);
+    float* rs_s = xs + 32 * 128;
+    int* last_s = reinterpret_cast<int*>(rs_s + 128);
+    auto epi_bar = [&]() { asm volatile("bar.sync 1, 128;" ::: "memory"); };
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int wt = u / splits, sp = u % splits;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int n = wt * 128 + wq * 32 + lane;  // weight row == output column
+      const int n = wt * 128 + r;  // weight row == output column
       const uint32_t taddr = tmem_base + acc * ACC + ((uint32_t)(wq * 32) << 16);
       float* dst = part + (long long)sp * M * N + n;
+      bool direct = false;  // fused, one split: epilogue straight from TMEM
+      if constexpr (FUSED) direct = splits == 1;
+      if (!direct) {
 #pragma unroll
-      for (int c = 0; c < (NT + 31) / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(taddr + c * 32, r);
-        tmem_ld_wait();
-        if (n < N) {
+        for (int c = 0; c < (NT + 31) / 32; ++c) {
+          uint32_t rr[32];
+          tmem_ld32(taddr + c * 32, rr);
+          tmem_ld_wait();
+          if (n < N) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (c * 32 + i < M) dst[(long long)(c * 32 + i) * N] = __uint_as_float(r[i]);
+            for (int i = 0; i < 32; ++i)
+              if (c * 32 + i < M) dst[(long long)(c * 32 + i) * N] = __uint_as_float(rr[i]);
+          }
+        }
+      }
+      if constexpr (FUSED) {
+        bool mine = direct;
+        if (!direct) {  // last split of this weight tile does the epilogue
+          __threadfence();
+          epi_bar();
+          if (r == 0) *last_s = atomicAdd(&ep.counters[wt], 1) == splits - 1;
+          epi_bar();
+          mine = *last_s != 0;
+          if (mine) __threadfence();
+        }
+        if (mine) {
+          if (ep.ssq_in && (EPI == EPI_QKV || EPI == EPI_SWIGLU)) {  // per-row RMSNorm scales
+            if (r < M) {
+              float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
+              const float* p = ep.ssq_in + r;
+              int c = 0;
+              for (; c + 4 <= ep.ssq_parts; c += 4) {
+                v0 += p[(long long)c * M];
+                v1 += p[(long long)(c + 1) * M];
+                v2 += p[(long long)(c + 2) * M];
+                v3 += p[(long long)(c + 3) * M];
+              }
+              for (; c < ep.ssq_parts; ++c) v0 += p[(long long)c * M];
+              rs_s[r] = rsqrtf(((v0 + v1) + (v2 + v3)) / (float)ep.ssq_dim + ep.norm_eps);
+            }
+            epi_bar();
+          }
+#pragma unroll 1
+          for (int c = 0; c < (M + 31) / 32; ++c) {
+            float v[32];
+            if (direct) {
+              uint32_t rr[32];
+              tmem_ld32(taddr + c * 32, rr);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(rr[i]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = 0.f;
+              for (int k = 0; k < splits; ++k) {  // split order: deterministic
+                const float* src = part + (long long)k * M * N + n;
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (c * 32 + i < M && n < N) v[i] += __ldcg(src + (long long)(c * 32 + i) * N);
+              }
+            }
+            if constexpr (EPI == EPI_QKV || EPI == EPI_SWIGLU) {
+              if (ep.ssq_in) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] *= rs_s[min(c * 32 + i, 127)];
+              }
+            }
+            if constexpr (EPI == EPI_STORE_F32 || EPI == EPI_STORE || EPI == EPI_RESID) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const int m = c * 32 + i;
+                float y = v[i];
+                if (m < M && n < N) {
+                  if constexpr (EPI == EPI_STORE_F32) {
+                    static_cast<float*>(ep.out)[(long long)m * ep.ldo + n] = y;
+                  } else {
+                    if constexpr (EPI == EPI_RESID) y += __bfloat162float(ep.resid[(long long)m * ep.ldr + n]);
+                    const __nv_bfloat16 yb = __float2bfloat16(y);
+                    static_cast<__nv_bfloat16*>(ep.out)[(long long)m * ep.ldo + n] = yb;
+                    y = __bfloat162float(yb);
+                  }
+                } else {
+                  y = 0.f;
+                }
+                if constexpr (EPI == EPI_RESID) {
+                  if (ep.ssq_out) {  // the next RMSNorm's statistics: this warp's 32 columns = one chunk
+                    float q = y * y;
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+                    if (lane == 0 && m < M) ep.ssq_out[(long long)(n >> 5) * M + m] = q;
+                  }
+                }
+              }
+            } else if constexpr (EPI == EPI_SWIGLU) {
+              // weight rows [0, 64) of the tile are gate, [64, 128) up, for output columns wt*64 + r % 64
+              if (r >= 64) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) xs[i * 128 + r] = v[i];
+              }
+              epi_bar();
+              if (r < 64) {
+                const int o = wt * 64 + r;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  const int m = c * 32 + i;
+                  if (m < M && o < N / 2)
+                    static_cast<__nv_bfloat16*>(ep.out)[(long long)m * ep.ldo + o] =
+                        __float2bfloat16(silu(v[i]) * xs[i * 128 + r + 64]);
+                }
+              }
+              epi_bar();
+            } else if constexpr (EPI == EPI_QKV) {
+              // DH = 128: the tile is one head; DH = 64: two.  RoPE pairs (d, d + DH/2) within a head.
+#pragma unroll
+              for (int i = 0; i < 32; ++i) xs[i * 128 + r] = v[i];
+              epi_bar();
+              const int g = (wt * 128 + r) / DH, d = r % DH;
+              const bool rot = g < ep.hq + ep.hkv;
+#pragma unroll 4
+              for (int i = 0; i < 32; ++i) {
+                const int m = c * 32 + i;
+                if (m >= M || n >= N) continue;
+                float y = v[i];
+                if (rot) {
+                  const int p = ep.pos[m];
+                  const float2 cs = reinterpret_cast<const float2*>(ep.rope)[(long long)p * (DH / 2) + (d % (DH / 2))];
+                  const int base = r - d;  // this head's first row in the tile
+                  y = d < DH / 2 ? v[i] * cs.x - xs[i * 128 + base + d + DH / 2] * cs.y
+                                 : v[i] * cs.x + xs[i * 128 + base + d - DH / 2] * cs.y;
+                }
+                __nv_bfloat16* o;
+                if (g < ep.hq)
+                  o = ep.q + (long long)m * ep.ldq + (long long)g * DH + d;
+                else if (g < ep.hq + ep.hkv)
+                  o = ep.kplane + (long long)(g - ep.hq) * ep.head_stride + (long long)ep.slot[m] * DH + d;
+                else
+                  o = ep.vplane + (long long)(g - ep.hq - ep.hkv) * ep.head_stride + (long long)ep.slot[m] * DH + d;
+                *o = __float2bfloat16(y);
+              }
+              epi_bar();
+            }
+          }
+          if (!direct && r == 0) ep.counters[wt] = 0;  // ticket reset for the next launch
         }
       }
       tc_fence_before();
@@ -789,18 +938,21 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
-template <int NT>
+template <int NT, int EPI = EPI_PARTIAL, int DH = 0>
 int launch_swapab(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K, int splits, float* part,
-                  cudaStream_t stream) {
-  constexpr size_t SMEM = 1024 + (NT >= 128 ? 6 : 8) * ((size_t)128 * BK * 2 + (size_t)NT * BK * 2) + 256;
+                  const GemmEpi& ep, cudaStream_t stream) {
+  // stage ring + the fused epilogue's exchange [32][128] fp32, row scales [128], flag
+  constexpr size_t SMEM = 1024 + (NT >= 128 ? 6 : 8) * ((size_t)128 * BK * 2 + (size_t)NT * BK * 2) + 256 +
+                          (EPI != EPI_PARTIAL ? 1024 + 32 * 128 * 4 + 128 * 4 + 16 : 0);
   static bool attr_set = false;
+  auto kern = gemm_swapab_kernel<NT, EPI, DH>;
   if (!attr_set) {
-    CUDA_TRY(cudaFuncSetAttribute(gemm_swapab_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
     attr_set = true;
   }
   const int units = ((N + 127) / 128) * splits;
   const int grid = units < num_sms() ? units : num_sms();
-  CUDA_TRY(launch_k(gemm_swapab_kernel<NT>, dim3(grid), dim3(256), SMEM, stream, tw, tx, M, N, K, splits, part));
+  CUDA_TRY(launch_k(kern, dim3(grid), dim3(256), SMEM, stream, tw, tx, M, N, K, splits, part, ep));
   return 0;
 }
 
@@ -1153,11 +1305,37 @@ int launch_small_m(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B
   RDKV_TRY(make_tmap(&tw, B, N, K, ldb, 128));
   RDKV_TRY(make_tmap(&tx, A, M, K, lda, sp.nt));
   auto* part = static_cast<float*>(ep.splitk_ws);
+  // fused split-K (no finalize kernel) for every epilogue that works per 128-column tile: not
+  // the row-wide resid+norm finalize (norm_out) nor the tensor-parallel push
+  const int w_tiles = (N + 127) / 128;
+  const bool fuse = ep.counters && w_tiles <= ep.n_counters && !(kind == EPI_RESID && ep.norm_out) &&
+                    kind != EPI_PUSH && (kind != EPI_QKV || dh == 64 || dh == 128);
+  if (fuse) {
+    auto go = [&](auto nt) -> int {
+      constexpr int NT = decltype(nt)::value;
+      switch (kind) {
+        case EPI_STORE: return launch_swapab<NT, EPI_STORE, 0>(tw, tx, M, N, K, sp.splits, part, ep, stream);
+        case EPI_STORE_F32: return launch_swapab<NT, EPI_STORE_F32, 0>(tw, tx, M, N, K, sp.splits, part, ep, stream);
+        case EPI_RESID: return launch_swapab<NT, EPI_RESID, 0>(tw, tx, M, N, K, sp.splits, part, ep, stream);
+        case EPI_SWIGLU: return launch_swapab<NT, EPI_SWIGLU, 0>(tw, tx, M, N, K, sp.splits, part, ep, stream);
+        case EPI_QKV:
+          if (dh == 64) return launch_swapab<NT, EPI_QKV, 64>(tw, tx, M, N, K, sp.splits, part, ep, stream);
+          return launch_swapab<NT, EPI_QKV, 128>(tw, tx, M, N, K, sp.splits, part, ep, stream);
+        default: return set_error(RDKV_ERR_ARG, "gemm: unknown epilogue %d", kind);
+      }
+    };
+    switch (sp.nt) {
+      case 16: return go(std::integral_constant<int, 16>{});
+      case 32: return go(std::integral_constant<int, 32>{});
+      case 64: return go(std::integral_constant<int, 64>{});
+      default: return go(std::integral_constant<int, 128>{});
+    }
+  }
   switch (sp.nt) {
-    case 16: RDKV_TRY(launch_swapab<16>(tw, tx, M, N, K, sp.splits, part, stream)); break;
-    case 32: RDKV_TRY(launch_swapab<32>(tw, tx, M, N, K, sp.splits, part, stream)); break;
-    case 64: RDKV_TRY(launch_swapab<64>(tw, tx, M, N, K, sp.splits, part, stream)); break;
-    default: RDKV_TRY(launch_swapab<128>(tw, tx, M, N, K, sp.splits, part, stream)); break;
+    case 16: RDKV_TRY(launch_swapab<16>(tw, tx, M, N, K, sp.splits, part, ep, stream)); break;
+    case 32: RDKV_TRY(launch_swapab<32>(tw, tx, M, N, K, sp.splits, part, ep, stream)); break;
+    case 64: RDKV_TRY(launch_swapab<64>(tw, tx, M, N, K, sp.splits, part, ep, stream)); break;
+    default: RDKV_TRY(launch_swapab<128>(tw, tx, M, N, K, sp.splits, part, ep, stream)); break;
   }
   return finalize(kind, dh, part, sp.splits, M, N, ep, stream);
 }

@@ -77,6 +77,11 @@ struct GemmEpi {
   // smem ring holds only a few k-blocks, too little to cover DRAM latency when a
   // single-wave GEMM streams its weights cold.  0 = off.  Set by launch_gemm (RDKV_GEMM_PF).
   int b_pf;
+  // Small-M fused split-K (swap-AB GEMM, no finalize kernel): one ticket counter per 128-column
+  // weight tile, zero before the launch and left zero by it (the last split resets it).
+  // Null = the split-K partials go through a separate finalize kernel.
+  int* counters;
+  int n_counters;
 };
 
 // True when launch_gemm will take the split-K path for this shape (small M).

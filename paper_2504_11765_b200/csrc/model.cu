@@ -95,7 +95,9 @@ struct Ws {
   size_t attn_split_bytes;
   void* attn_sk;  // stream-K attention partials + flags (num_sms() CTAs)
   void* argmax;
+  int* counters;  // fused small-M split-K tickets (zeroed at the start of every forward)
 };
+constexpr int N_SPLITK_COUNTERS = 2048;
 
 size_t ws_layout(const rdkv_model_desc& d, int T, int S, Ws* ws, void* base) {
   const size_t qd = (size_t)d.n_heads * d.head_dim;
@@ -121,7 +123,9 @@ size_t ws_layout(const rdkv_model_desc& d, int T, int S, Ws* ws, void* base) {
   const size_t osk_attn = take(attention_sk_scratch_bytes(num_sms(), d.head_dim));
   const size_t oam = take(argmax_scratch_bytes(S));
   const size_t ossq = take((size_t)(d.hidden / 32) * T * sizeof(float));
+  const size_t octr = take((size_t)N_SPLITK_COUNTERS * sizeof(int));
   if (ws && base) {
+    ws->counters = reinterpret_cast<int*>(static_cast<uint8_t*>(base) + octr);
     ws->ssq = reinterpret_cast<float*>(static_cast<uint8_t*>(base) + ossq);
     ws->argmax = static_cast<uint8_t*>(base) + oam;
     ws->attn_split = ask ? static_cast<uint8_t*>(base) + oask : nullptr;
@@ -275,13 +279,23 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     const char* e = std::getenv("RDKV_FUSED_NORM");  // "0": rmsnorm launches instead (A/B)
     return !(e && e[0] == '0');
   }();
-  // (RDKV_SMALLM_SSQ=1: small batches too — the split-K finalizes emit / apply the same
-  // per-chunk statistics instead of the row-wide resid+norm finalize; correct, measured no
-  // faster: decode step 5.20 vs 5.20 ms, single-query TTFT 4.52 vs 4.51 ms; off)
-  static const bool small_ssq_env = [] {
-    const char* e = std::getenv("RDKV_SMALLM_SSQ");
+  // RDKV_SMALLM_FUSED=1: the swap-AB split-K GEMMs reduce their partials in-kernel (the last
+  // split of each weight tile applies the epilogue: no finalize launches) and the norms use the
+  // per-chunk statistics of large batches.  Correct (tests pass with it on) but slower: only the
+  // w_tiles last CTAs do the whole epilogue (single-query TTFT 4.50 -> 9.94 ms, decode step
+  // 5.22 -> 6.89 ms); the finalize kernels spread it over rows x column chunks.  Off.
+  // (RDKV_SMALLM_SSQ=1 with the finalize kernels: correct, measured no faster — decode step
+  // 5.20 vs 5.20 ms, single-query TTFT 4.52 vs 4.51 ms.)
+  static const bool small_fused_env = [] {
+    const char* e = std::getenv("RDKV_SMALLM_FUSED");
     return e && e[0] == '1';
   }();
+  static const bool small_ssq_env = [] {
+    const char* e = std::getenv("RDKV_SMALLM_SSQ");
+    return (e && e[0] == '1') || small_fused_env;
+  }();
+  int* counters = small_fused_env && !tp ? ws.counters : nullptr;
+  if (counters) CUDA_TRY(cudaMemsetAsync(counters, 0, N_SPLITK_COUNTERS * sizeof(int), st));
   const bool split_any = o_fused || down_fused || gemm_splits(T, qkv_n, d.hidden, ws.splitk_bytes) ||
                          gemm_splits(T, 2 * d.ffn, d.hidden, ws.splitk_bytes);
   const bool ssq_path = fuse_norm_env && folded && !tp && d.hidden % 256 == 0 && (small_ssq_env || !split_any);
@@ -297,6 +311,8 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     if (!h_ready && !ssq_path)
       LAUNCH(RDKV_PROF_MISC, 0.0, launch_rmsnorm(ws.x, d.hidden, nullptr, gain(wb + 0), ws.h, d.hidden, T, d.hidden, d.norm_eps, st));
     GemmEpi eq{};
+    eq.counters = counters;
+    eq.n_counters = N_SPLITK_COUNTERS;
     eq.splitk_ws = ws.splitk;  // small M: split-K (the finalize handles the norm statistics)
     eq.splitk_bytes = ws.splitk_bytes;
     if (ssq_path) {
@@ -374,6 +390,8 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     else
       LAUNCH(RDKV_PROF_ATTN, 0.0, launch_attention(ap, dh, S, b->max_new, st));
     GemmEpi er{};
+    er.counters = counters;
+    er.n_counters = N_SPLITK_COUNTERS;
     er.splitk_ws = ws.splitk;  // small M: split-K (the finalize handles the norm statistics)
     er.splitk_bytes = ws.splitk_bytes;
     er.out = ws.x;
@@ -398,6 +416,8 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     if (!o_fused && !ssq_path)
       LAUNCH(RDKV_PROF_MISC, 0.0, launch_rmsnorm(ws.x, d.hidden, nullptr, gain(wb + 3), ws.h, d.hidden, T, d.hidden, d.norm_eps, st));
     GemmEpi eg{};
+    eg.counters = counters;
+    eg.n_counters = N_SPLITK_COUNTERS;
     eg.splitk_ws = ws.splitk;  // small M: split-K (the finalize handles the norm statistics)
     eg.splitk_bytes = ws.splitk_bytes;
     eg.out = ws.a;
@@ -431,6 +451,8 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     const int fn = 1 + RDKV_WEIGHTS_PER_LAYER * d.layers;
     LAUNCH(RDKV_PROF_HEAD, 0.0, launch_rmsnorm(ws.x, d.hidden, b->last_row, G(m, fn), ws.hl, d.hidden, S, d.hidden, d.norm_eps, st));
     GemmEpi el{};
+    el.counters = counters;
+    el.n_counters = N_SPLITK_COUNTERS;
     el.splitk_ws = ws.splitk;
     el.splitk_bytes = ws.splitk_bytes;
     el.out = b->logits;
