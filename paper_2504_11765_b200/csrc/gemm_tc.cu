@@ -1501,6 +1501,24 @@ int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, l
       if (tp.bn == 128) return dispatch_pair<128>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
       if (tp.bn == 192) return dispatch_pair<192>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
       if (tp.bn == 384) return dispatch_pair<384>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
+      // RDKV_GEMM_TAIL=1: a last round that holds only the final column of 256-wide tiles
+      // (gate/up at M = 1024: 448 tiles on 74 pairs, the 7th round has 4) runs as its own launch
+      // of 256 x 128 tiles.  Correct, measured slower (gate/up 169.8 -> 175.1 us alone, 6.03 ->
+      // 6.29 ms per C3 step: the second launch's ramp costs more than the half round it saves).
+      static const bool tail_env = [] {
+        const char* e = std::getenv("RDKV_GEMM_TAIL");
+        return e && e[0] == '1';
+      }();
+      const int m_t = (M + 255) / 256, n_t = N / 256, npairs = num_sms() / 2;
+      const int units = m_t * n_t, rem = units % npairs;
+      if (tail_env && (kind == EPI_SWIGLU || kind == EPI_STORE) && N % 256 == 0 && units > npairs && rem > 0 &&
+          rem <= m_t && (units - m_t) % npairs == 0) {
+        const int n_main = N - 256;
+        RDKV_TRY(dispatch_pair<256>(A, lda, B, ldb, M, n_main, K, kind, dh, ep, stream));
+        GemmEpi et = ep;  // the last 256 output columns (128 for SwiGLU): shifted B rows and output
+        et.out = static_cast<__nv_bfloat16*>(ep.out) + (kind == EPI_SWIGLU ? n_main / 2 : n_main);
+        return dispatch_pair<128>(A, lda, B + (long long)n_main * ldb, ldb, M, 256, K, kind, dh, et, stream);
+      }
       return dispatch_pair<256>(A, lda, B, ldb, M, N, K, kind, dh, ep, stream);
     }
     bn = tp.bn;

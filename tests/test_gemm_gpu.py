@@ -112,3 +112,23 @@ def test_bad_k_rejected():
     D = torch.empty(128, 128, device="cuda", dtype=torch.bfloat16)
     with pytest.raises(_lib.NativeError):
         _gemm(A, B, D, _lib.EPI_STORE)
+
+
+@pytest.mark.parametrize("epi", [_lib.EPI_STORE, _lib.EPI_SWIGLU])
+def test_last_round_tail_tiles(epi):
+    """M = 1024, N = 28672 (the C3 gate/up shape): 448 tiles of 256 x 256 on 74 CTA pairs
+    leave a 7th round of 4 tiles (with RDKV_GEMM_TAIL=1 the last 256 columns run as a second
+    launch of 256 x 128 tiles).  Every column, the last tile column included, matches."""
+    M, N, K = 1024, 28672, 256
+    A, B = _inputs(M, N, K, seed=5)
+    n_out = N // 2 if epi == _lib.EPI_SWIGLU else N
+    D = torch.full((M, n_out), float("nan"), device="cuda", dtype=torch.bfloat16)
+    _gemm(A, B, D, epi)
+    torch.cuda.synchronize()
+    full = A.float() @ B.float().T
+    if epi == _lib.EPI_SWIGLU:
+        f = full.view(M, N // 128, 2, 64)
+        ref = (torch.nn.functional.silu(f[:, :, 0]) * f[:, :, 1]).reshape(M, n_out)
+    else:
+        ref = full
+    torch.testing.assert_close(D.float(), ref, atol=2e-2, rtol=1e-2)
