@@ -1,5 +1,6 @@
-"""Break a cold-disk TTFT (C2 composite, page cache dropped) into its parts:
-pinned-buffer allocation, the parallel read, the GPU checksum, and the prefill."""
+"""Break a cold-disk TTFT (page cache dropped) into its parts: pinned-buffer allocation,
+the parallel read, the GPU checksum, and the prefill.
+    python scripts/micro/cold_path.py [model (llama-3.2-1b)] [docs (5)]   # C3: llama-3-8b 10"""
 import json, sys, tempfile, time
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
@@ -11,11 +12,12 @@ from paper_2504_11765_b200.model import get_spec, query_tokens
 from paper_2504_11765_b200.prefill import PrefillRequest, prefill_batch
 from paper_2504_11765_b200.store import GpuVerifier, KvKey, KvStore, read_blob_file
 
-spec = get_spec("llama-3.2-1b")
+spec = get_spec(sys.argv[1] if len(sys.argv) > 1 else "llama-3.2-1b")
+nd = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 eng = Engine(spec, seed=0, pool_tokens=16384, device_cache_bytes=1 << 30)
 gen = KvGenerator(eng)
-docs = (11, 22, 33, 44, 55)
-blob = gen.generate(docs, (512,) * 5)
+docs = tuple(11 * (i + 1) for i in range(nd))
+blob = gen.generate(docs, (512,) * nd)
 root = Path(tempfile.mkdtemp(prefix="rdkv_cold_"))
 store = KvStore(root, 0, verifier=GpuVerifier("cuda"))
 key = KvKey(spec.profile().model_hash, docs)
