@@ -1329,7 +1329,7 @@ __global__ void __launch_bounds__(256) attn_split_combine_kernel(AttnParams p) {
   constexpr int PER = DH / 32;
   float acc[PER] = {};
   float L = 0.f;
-#pragma unroll 4
+#pragma unroll 4  // (8 / 16 measured slower: 14.9 vs 10.0 us per single-query layer)
   for (int k = 0; k < p.kv_splits; ++k) {
     const float2 ml = p.split_ml[((long long)k * p.n_tokens + t) * p.hq + head];
     if (ml.x == -INFINITY) continue;

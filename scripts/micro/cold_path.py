@@ -26,7 +26,20 @@ path = store.path_of(key)
 L = _lib.lib()
 qt = query_tokens(3, 64, spec.vocab)
 rows = []
+# "distinct": like the bench's cold leg, four freshly written composites, flushed, each read once
+distinct = len(sys.argv) > 3 and sys.argv[3] == "distinct"
+paths = [path]
+if distinct:
+    import os
+    keys = [KvKey(spec.profile().model_hash, tuple(d + 1000 * j for d in docs)) for j in range(1, 5)]
+    for k2 in keys:
+        store.put(k2, gen.generate(k2.doc_ids, (512,) * nd))
+    os.sync()
+    paths = [store.path_of(k2) for k2 in keys]
 for it in range(8):
+    if distinct:
+        key = keys[it % 4]
+        path = paths[it % 4]
     L.rdkv_drop_page_cache(str(path).encode())
     torch.cuda.synchronize()
     t0 = time.perf_counter()
