@@ -993,6 +993,10 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
         if (lane == 0) st_release_gpu(p.sk_flag + blockIdx.x, 1);
       }
       if constexpr (ISSUE_BY_KIND) {  // then issue P.V of Q tile 0 (the producer: Q tile 1)
+        // this CTA's share of the next projection's weights into L2 first (a few bulk prefetches)
+        __syncwarp();
+        l2_prefetch_share(p.l2_next, p.l2_next_bytes, blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z),
+                          gridDim.x * gridDim.y * gridDim.z, lane);
         if (lane == 0) {
           const int nt = sg.z - sg.y;
           const bool mine = nt > 0 && unit_at(sg.x).n_q > 0;

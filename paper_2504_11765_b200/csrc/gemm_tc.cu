@@ -760,6 +760,10 @@ __global__ void __launch_bounds__(256, 1)
         if (acc == 0) acc_phase ^= 1;
       }
     }
+  } else if (warp == 3) {
+    // idle warp: this CTA's share of the next kernel's weights into L2 (weights are never
+    // written by a predecessor: no griddepcontrol.wait needed)
+    l2_prefetch_share(ep.l2_next, ep.l2_next_bytes, blockIdx.x, gridDim.x, lane);
   } else if (warp >= 4) {
     pdl_wait();  // the split-K scratch may still be read by the predecessor's finalize
     const int wq = warp & 3;
@@ -1469,7 +1473,15 @@ int launch_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, l
   GemmEpi ep = ep_in;
   ep.w_policy = wpol;
   ep.b_pf = b_pf;
-  if (!l2pf) ep.l2_next = nullptr;
+  // RDKV_SMALLM_L2PF=all: on the small-M (split-K swap-AB) path the idle warp pulls the next
+  // projection's weights into L2 (gate/up -> w_down, down -> next w_qkv).  Measured slower
+  // (single-query TTFT 4.50 -> 5.09 ms, decode step 5.20 -> 5.68 ms: the prefetch competes with
+  // the weight stream it is meant to hide); off.  Large M only with RDKV_L2_PREFETCH=1.
+  static const bool small_l2pf = [] {
+    const char* e = std::getenv("RDKV_SMALLM_L2PF");
+    return e && e[0] == 'a';
+  }();
+  if (!l2pf && !(small_l2pf && M <= 128)) ep.l2_next = nullptr;
   if (M <= 0 || N <= 0) return 0;
   if (K <= 0 || K % BK != 0) return set_error(RDKV_ERR_ARG, "gemm: K=%d must be a positive multiple of 64", K);
   if (N % 32 != 0) return set_error(RDKV_ERR_ARG, "gemm: N=%d must be a multiple of 32", N);

@@ -377,7 +377,11 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
       const char* e = std::getenv("RDKV_L2_PREFETCH");  // opt-in: measured no faster in the C3 step
       return e && e[0] == '1';
     }();
-    if (attn_l2pf) {
+    static const bool small_l2pf = [] {  // RDKV_SMALLM_L2PF=attn|all: small batches pull w_o while attending
+      const char* e = std::getenv("RDKV_SMALLM_L2PF");
+      return e && (e[0] == 'a');
+    }();
+    if (attn_l2pf || (small_l2pf && T <= 128)) {
       ap.l2_next = W(m, wb + 2);
       ap.l2_next_bytes = (long long)d.hidden * qd * 2;
     }
@@ -428,6 +432,8 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
       eg.ssq_dim = d.hidden;
       eg.norm_eps = d.norm_eps;
     }
+    eg.l2_next = W(m, wb + 5);  // the down projection's weights (kept only on the small-M path)
+    eg.l2_next_bytes = (long long)d.ffn * d.hidden * 2;
     LAUNCH(RDKV_PROF_GU, 4.0 * T * d.ffn * d.hidden, launch_gemm(ssq_path ? ws.x : ws.h, d.hidden, W(m, wb + 4), d.hidden, T, 2 * d.ffn, d.hidden, EPI_SWIGLU, 0, eg, st));
     h_ready = down_fused && !ssq_path && l + 1 < d.layers;
     // the down projection pulls the next layer's QKV weights into L2
