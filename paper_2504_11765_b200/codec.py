@@ -120,6 +120,24 @@ def fnv1a64_device(data, seed: int = FNV_OFFSET, stream=None) -> int:
     return int(out.item()) & _U64
 
 
+def fnv1a64_device_async(data, seed: int = FNV_OFFSET, stream=None):
+    """fnv1a64_device without the host synchronisation: returns a 1-element int64 CUDA
+    tensor that holds the checksum once ``stream`` reaches this point."""
+    import torch
+
+    L = _lib.lib()
+    raw = data.reshape(-1).view(torch.uint8) if data.dtype != torch.uint8 else data.reshape(-1)
+    n = raw.numel()
+    need = int(L.rdkv_fnv1a64_device_scratch(n))
+    st = stream if stream is not None else torch.cuda.current_stream(raw.device)
+    with torch.cuda.stream(st):
+        ws = torch.empty(need, dtype=torch.uint8, device=raw.device)
+        out = torch.empty(1, dtype=torch.int64, device=raw.device)
+    _lib.check(L.rdkv_fnv1a64_device(raw.data_ptr(), n, seed & _U64, ws.data_ptr(), need, out.data_ptr(),
+                                     st.cuda_stream))
+    return out
+
+
 def fnv1a64_many(buffers: Sequence, threads: int = 8) -> list[int]:
     """FNV-1a of several independent buffers in parallel (one chain per buffer)."""
     n = len(buffers)

@@ -21,7 +21,7 @@ from typing import Callable, Sequence
 import numpy as np
 import torch
 
-from .codec import KvBlob, fnv1a64_device, make_header
+from .codec import KvBlob, fnv1a64_device, fnv1a64_device_async, make_header
 from .engine import Engine
 from .model import combo_tokens
 from .store import KvKey
@@ -66,6 +66,49 @@ class KvGenerator:
         if self.keep_on_device:
             eng.make_resident(KvKey(self.profile.model_hash, ids), kv, n)
         return KvBlob.trusted(make_header(self.profile, ids, n, checksum), host)
+
+    def generate_many(self, combos: Sequence[tuple[Sequence[int], Sequence[int]]],
+                      hosts: Sequence[torch.Tensor] | None = None) -> list[KvBlob]:
+        """``generate`` for several combinations as one pipeline: composite i's D2H into the
+        host tier (copy engine) runs while composite i+1 is prefilled, and the checksums stay
+        on the device until the end — no host synchronisation between composites.  Each blob
+        is byte-identical to ``generate`` of the same combination.  ``hosts``: optional
+        pinned uint8 buffers (one per combination, at least the payload size) to copy into."""
+        eng = self.engine
+        out = []
+        with torch.cuda.device(eng.device):
+            main = torch.cuda.current_stream(eng.device)
+            cs = self.copy_stream
+            # the checksum of composite i runs on a low-priority stream beside the prefill of
+            # composite i+1 (it takes the SMs the prefill's kernels leave idle)
+            if getattr(self, "_fnv_stream", None) is None:
+                lo, _ = torch.cuda.Stream.priority_range()
+                self._fnv_stream = torch.cuda.Stream(device=eng.device, priority=lo)
+            fs = self._fnv_stream
+            pending = []
+            for ci, (doc_ids, counts) in enumerate(combos):
+                ids = tuple(int(d) for d in doc_ids)
+                toks = self.tokens(ids, counts)
+                kv = eng.generate_doc_kv(toks)
+                raw = kv.view(torch.uint8)
+                fs.wait_stream(main)
+                csum = fnv1a64_device_async(raw, stream=fs)
+                raw.record_stream(fs)
+                host = hosts[ci][: raw.numel()] if hosts is not None else \
+                    torch.empty(raw.numel(), dtype=torch.uint8, pin_memory=True)
+                cs.wait_stream(main)
+                with torch.cuda.stream(cs):
+                    host.copy_(raw, non_blocking=True)
+                raw.record_stream(cs)
+                if self.keep_on_device:
+                    eng.make_resident(KvKey(self.profile.model_hash, ids), kv, len(toks))
+                pending.append((ids, len(toks), csum, host))
+            cs.synchronize()
+            fs.synchronize()
+            main.synchronize()
+            for ids, n, csum, host in pending:
+                out.append(KvBlob.trusted(make_header(self.profile, ids, n, int(csum.item()) & ((1 << 64) - 1)), host))
+        return out
 
     def slice_prefix(self, full: torch.Tensor, n_full: int, n: int) -> torch.Tensor:
         """Payload of the first n tokens of a combination's payload [L][2][Hkv][n_full][dh]

@@ -301,3 +301,18 @@ def test_layer_stream_native_chain_matches_unpack():
     torch.cuda.synchronize()
     assert torch.equal(staging, payload.view(torch.uint8))
     assert torch.equal(pool.gather(blocks_b, n), pool.gather(blocks_a, n))
+
+
+def test_generate_many_pipeline_equals_generate(setup):
+    """KvGenerator.generate_many (D2H under the next prefill, checksums left on the device)
+    returns blobs byte-identical to generate() of each combination."""
+    from paper_2504_11765_b200.generator import KvGenerator
+
+    spec, eng, orc = setup
+    gen = KvGenerator(eng, keep_on_device=False)
+    combos = [((3, 5), (128, 61)), ((7,), (200,)), ((3, 5, 9), (128, 61, 64))]
+    many = gen.generate_many(combos)
+    for (ids, counts), b in zip(combos, many):
+        ref = gen.generate(ids, counts)
+        assert b.header == ref.header
+        assert torch.equal(b.payload_tensor(), ref.payload_tensor())
