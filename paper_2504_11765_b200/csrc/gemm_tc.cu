@@ -649,12 +649,22 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int 
 // and the CTA whose atomic ticket on the weight tile comes last (after a __threadfence)
 // sums the partials in split order (deterministic) and applies the epilogue for that tile's
 // 128 output columns.  Norms use the per-chunk sum-of-squares scheme (ep.ssq_out / ssq_in).
+// Token tiles of <= 32 rows (decode steps): two CTAs per SM (RDKV_SWAPAB_2CTA), each with a
+// shallower ring, so one CTA's prologue / epilogue overlaps the other's weight stream.
+#ifndef RDKV_SWAPAB_2CTA
+#define RDKV_SWAPAB_2CTA 1
+#endif
+template <int NT>
+struct SwapCfg {
+  static constexpr int CTAS_PER_SM = (RDKV_SWAPAB_2CTA && NT <= 32) ? 2 : 1;
+  static constexpr int STAGES = NT >= 128 ? 6 : CTAS_PER_SM == 2 ? 5 : 8;
+};
 template <int NT, int EPI = EPI_PARTIAL, int DH = 0>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, SwapCfg<NT>::CTAS_PER_SM)
     gemm_swapab_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, int M, int N,
                        int K, int splits, float* __restrict__ part, GemmEpi ep) {
   constexpr bool FUSED = EPI != EPI_PARTIAL;
-  constexpr int STAGES = NT >= 128 ? 6 : 8;
+  constexpr int STAGES = SwapCfg<NT>::STAGES;
   constexpr uint32_t W_BYTES = 128 * BK * 2, X_BYTES = NT * BK * 2, STAGE = W_BYTES + X_BYTES;
   constexpr uint32_t ACC = NT < 32 ? 32 : NT;  // accumulator column stride (tcgen05.ld reads 32 columns)
   constexpr uint32_t TMEM_COLS = 2 * ACC;
@@ -946,7 +956,7 @@ template <int NT, int EPI = EPI_PARTIAL, int DH = 0>
 int launch_swapab(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K, int splits, float* part,
                   const GemmEpi& ep, cudaStream_t stream) {
   // stage ring + the fused epilogue's exchange [32][128] fp32, row scales [128], flag
-  constexpr size_t SMEM = 1024 + (NT >= 128 ? 6 : 8) * ((size_t)128 * BK * 2 + (size_t)NT * BK * 2) + 256 +
+  constexpr size_t SMEM = 1024 + SwapCfg<NT>::STAGES * ((size_t)128 * BK * 2 + (size_t)NT * BK * 2) + 256 +
                           (EPI != EPI_PARTIAL ? 1024 + 32 * 128 * 4 + 128 * 4 + 16 : 0);
   static bool attr_set = false;
   auto kern = gemm_swapab_kernel<NT, EPI, DH>;
@@ -954,8 +964,8 @@ int launch_swapab(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, in
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
     attr_set = true;
   }
-  const int units = ((N + 127) / 128) * splits;
-  const int grid = units < num_sms() ? units : num_sms();
+  const int units = ((N + 127) / 128) * splits, slots = num_sms() * SwapCfg<NT>::CTAS_PER_SM;
+  const int grid = units < slots ? units : slots;
   CUDA_TRY(launch_k(kern, dim3(grid), dim3(256), SMEM, stream, tw, tx, M, N, K, splits, part, ep));
   return 0;
 }
@@ -1260,7 +1270,7 @@ struct SplitPlan {
 SplitPlan pick_split_plan(int M, int N, int K) {
   if (M > 128 || K % BK) return {0, 1};
   const int nt = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : 128;
-  const int sms = num_sms(), kblocks = K / BK, w_tiles = (N + 127) / 128;
+  const int sms = num_sms() * ((RDKV_SWAPAB_2CTA && nt <= 32) ? 2 : 1), kblocks = K / BK, w_tiles = (N + 127) / 128;
   int s = w_tiles >= sms ? 1 : sms / w_tiles;
   s = s < kblocks / 4 ? s : kblocks / 4;
   if (s < 1) s = 1;
