@@ -649,15 +649,18 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int 
 // and the CTA whose atomic ticket on the weight tile comes last (after a __threadfence)
 // sums the partials in split order (deterministic) and applies the epilogue for that tile's
 // 128 output columns.  Norms use the per-chunk sum-of-squares scheme (ep.ssq_out / ssq_in).
-// Token tiles of <= 32 rows (decode steps): two CTAs per SM (RDKV_SWAPAB_2CTA), each with a
+// Token tiles of <= 64 rows (decode steps, single queries): two CTAs per SM (RDKV_SWAPAB_2CTA), each with a
 // shallower ring, so one CTA's prologue / epilogue overlaps the other's weight stream.
 #ifndef RDKV_SWAPAB_2CTA
 #define RDKV_SWAPAB_2CTA 1
 #endif
+#ifndef RDKV_SWAPAB_2CTA_MAXNT
+#define RDKV_SWAPAB_2CTA_MAXNT 64
+#endif
 template <int NT>
 struct SwapCfg {
-  static constexpr int CTAS_PER_SM = (RDKV_SWAPAB_2CTA && NT <= 32) ? 2 : 1;
-  static constexpr int STAGES = NT >= 128 ? 6 : CTAS_PER_SM == 2 ? 5 : 8;
+  static constexpr int CTAS_PER_SM = (RDKV_SWAPAB_2CTA && NT <= RDKV_SWAPAB_2CTA_MAXNT) ? 2 : 1;
+  static constexpr int STAGES = NT >= 128 ? 6 : CTAS_PER_SM == 2 ? (NT >= 64 ? 4 : 5) : 8;
 };
 template <int NT, int EPI = EPI_PARTIAL, int DH = 0>
 __global__ void __launch_bounds__(256, SwapCfg<NT>::CTAS_PER_SM)
@@ -1270,7 +1273,8 @@ struct SplitPlan {
 SplitPlan pick_split_plan(int M, int N, int K) {
   if (M > 128 || K % BK) return {0, 1};
   const int nt = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : 128;
-  const int sms = num_sms() * ((RDKV_SWAPAB_2CTA && nt <= 32) ? 2 : 1), kblocks = K / BK, w_tiles = (N + 127) / 128;
+  const int sms = num_sms() * ((RDKV_SWAPAB_2CTA && nt <= RDKV_SWAPAB_2CTA_MAXNT) ? 2 : 1), kblocks = K / BK,
+            w_tiles = (N + 127) / 128;
   int s = w_tiles >= sms ? 1 : sms / w_tiles;
   s = s < kblocks / 4 ? s : kblocks / 4;
   if (s < 1) s = 1;
