@@ -122,6 +122,29 @@ def step(engine: Engine, seqs: Sequence[DecodeSeq], sync: bool = True,
     return nxt
 
 
+def extend(engine: Engine, parts: Sequence[tuple[LiveSequence, np.ndarray]]) -> torch.Tensor:
+    """One forward that appends ``tokens`` to each live sequence — a decode step's single
+    token, or the next chunk of a prompt being prefilled in chunks (chunked prefill: long
+    prompts share forwards with the running decodes) — over the sequences' paged contexts.
+    Returns the [S] int32 argmax after each sequence's last appended token (device)."""
+    pool = engine.pool
+    bs = pool.block_size
+    plans = []
+    for lv, toks in parts:
+        need = (lv.n_ctx + len(toks) + bs - 1) // bs
+        if need > len(lv.blocks):
+            nb = pool.alloc_blocks(need - len(lv.blocks))
+            lv.blocks.extend(nb)
+            lv.owned.extend(nb)
+        plans.append(SeqPlan(np.asarray(toks, np.int32), lv.n_ctx, lv.blocks))
+    plan = BatchPlan(plans, bs, engine.device)
+    logits, nxt = _steps(engine).buffers(len(parts))
+    engine.model.forward(plan, pool.data.data_ptr(), pool.slots, logits, nxt)
+    for lv, toks in parts:
+        lv.n_ctx += len(toks)
+    return nxt
+
+
 def retire(engine: Engine, seq: DecodeSeq) -> None:
     """Release a finished (or abandoned) sequence's blocks and its HBM-tier pin."""
     lv = seq.live

@@ -83,6 +83,12 @@ class RuntimeConfig:
     # continuously (new queries' prefills join between decode steps, finished ones leave).
     # A query is DONE when its last token is out; TTFT stays the first token's.
     decode_tokens: int = 0
+    # Chunked prefill (with decode_tokens > 0): at most this many prompt tokens per forward,
+    # shared first-come-first-served by the prompts still being prefilled, each forward also
+    # carrying one decode token per running query (decode.extend) — a long miss prefill no longer
+    # stalls every decoding query for its whole duration (TPOT) at the cost of the chunked
+    # prompts' own TTFT.  0 = whole prompts at once.
+    prefill_chunk: int = 0
 
     def __post_init__(self) -> None:
         if self.persist not in ("all", "composite", "none"):
@@ -182,6 +188,7 @@ class Instance:
         self._gen_for: dict[tuple, int] = {}             # prefix ids -> query index that triggered it
         self._unpins: list = []                           # (event, key): peer pins to drop once copies land
         self._live: list = []                             # (decode.DecodeSeq, result index) being decoded
+        self._filling: list = []                          # [LiveSequence, remaining tokens, meta, t_dispatch, batch]
         self._writer = _Writer(store, cp)
         self._threads: list[threading.Thread] = []
         self.errors: list = []
@@ -296,18 +303,71 @@ class Instance:
             try:
                 while not self.stopping():
                     self._drain_unpins()
-                    room = self.cfg.max_batch - len(self._live)
+                    room = self.cfg.max_batch - len(self._live) - len(self._filling)
                     batch = self._take_batch(room) if room > 0 else []
                     if batch:
                         self._serve(batch)
-                    if self._live:
+                    if self._filling:
+                        self._mixed_step()
+                    elif self._live:
                         self._decode_step()
                     elif not batch:
                         time.sleep(self.cfg.idle_sleep_s)
             finally:
                 for seq, _ in self._live:
                     decode.retire(self.eng, seq)
+                for lv, *_ in self._filling:
+                    decode.retire(self.eng, decode.DecodeSeq(lv, 0, 1))
                 self._live = []
+                self._filling = []
+
+    def _mixed_step(self) -> None:
+        """One forward: a decode token for every live sequence plus the next chunk of every
+        prompt being prefilled in chunks; a prompt whose last chunk ran yields its first token
+        (TTFT) and starts decoding."""
+        cfg = self.cfg
+        dec = [(s, ri) for s, ri in self._live if not s.done]
+        parts = [(s.live, np.array([s.last], np.int32)) for s, _ in dec]
+        budget = cfg.prefill_chunk
+        fed = []
+        for f in self._filling:  # first come, first served
+            if budget <= 0:
+                break
+            chunk, f[1] = f[1][:budget], f[1][budget:]
+            budget -= len(chunk)
+            fed.append(f)
+            parts.append((f[0], chunk))
+        nxt = decode.extend(self.eng, parts).cpu().tolist() if parts else []
+        now = time.monotonic()
+        for (s, _), t in zip(dec, nxt[: len(dec)]):
+            s.last = int(t)
+            s.tokens.append(int(t))
+        done = set()
+        for f, t in zip(fed, nxt[len(dec):]):
+            lv, rest, meta, t_dispatch, nb = f
+            if not len(rest):
+                self._first_token(lv, int(t), meta, t_dispatch, now, nb)
+                done.add(id(f))
+        self._filling = [f for f in self._filling if id(f) not in done]
+        self._retire_done(now)
+
+    def _first_token(self, lv, tok: int, meta, t_dispatch: float, t_first: float, batch_n: int) -> None:
+        index, qid, arrival, best, source, origins = meta
+        self.results.append(QueryResult(index, qid, self.rank, arrival, t_dispatch, t_first, best, source,
+                                        origins, batch_n, tok, t_first))
+        self._live.append((decode.DecodeSeq(lv, tok, self.cfg.decode_tokens + 1, [tok]), len(self.results) - 1))
+
+    def _retire_done(self, now: float) -> None:
+        keep = []
+        for seq, ri in self._live:
+            if seq.done:
+                res = self.results[ri]
+                res.done, res.n_tokens, res.tokens = now, len(seq.tokens), tuple(seq.tokens)
+                decode.retire(self.eng, seq)
+                self.cp.qstate_cas(res.index, QState.DISPATCHED, QState.DONE)
+            else:
+                keep.append((seq, ri))
+        self._live = keep
 
     def _decode_step(self) -> None:
         """One decode step for every live sequence (continuous batching); finished
@@ -387,9 +447,29 @@ class Instance:
             reqs.append(req)
             meta.append((index, qid, arrival, best, source, origins))
         dec = cfg.decode_tokens > 0
+        rests = [np.zeros(0, np.int32)] * len(reqs)
+        if dec and cfg.prefill_chunk > 0:  # chunked prefill: a share of the budget now, the rest in mixed steps
+            share = max(1, cfg.prefill_chunk // len(reqs))
+            for i, req in enumerate(reqs):
+                whole = np.asarray(req.new_tokens, np.int32) if req.lookup.outcome is not Outcome.MISS else \
+                    np.concatenate([np.asarray(req.prefix_tokens, np.int32), np.asarray(req.new_tokens, np.int32)])
+                if len(whole) > share:
+                    head, rests[i] = whole[:share], whole[share:]
+                    reqs[i] = PrefillRequest(req.lookup, head[:0], head, req.key) \
+                        if req.lookup.outcome is not Outcome.MISS else PrefillRequest(req.lookup, head, head[:0], None)
         r = prefill_batch(self.eng, reqs, timed=False, use_graph=False, keep=dec)
         first = r.next_token.cpu()  # D2H of the first tokens: the batch's TTFT point
         t_first = time.monotonic()
+        if any(len(x) for x in rests):
+            keep_meta, keep_first = [], []
+            for i, m in enumerate(meta):
+                if len(rests[i]):
+                    self._filling.append([r.sequences[i], rests[i], m, t_dispatch, len(batch)])
+                else:
+                    keep_meta.append((i, m))
+            for i, m in keep_meta:
+                self._first_token(r.sequences[i], int(first[i]), m, t_dispatch, t_first, len(batch))
+            return
         for i, ((index, qid, arrival, best, source, origins), tok) in enumerate(zip(meta, first.tolist())):
             self.results.append(QueryResult(index, qid, self.rank, arrival, t_dispatch, t_first, best, source,
                                             origins, len(batch), int(tok), t_first))

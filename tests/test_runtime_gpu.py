@@ -226,11 +226,13 @@ def test_cost_aware_dispatch(disk_gbps, expect_disk):
         _check_tokens(out["results"], expected)
 
 
-def test_runtime_continuous_batching_decode():
+@pytest.mark.parametrize("chunk", [0, 96], ids=["whole-prompts", "chunked-prefill"])
+def test_runtime_continuous_batching_decode(chunk):
     """decode_tokens > 0: every query generates more tokens after its first one while new
-    queries' prefills join the running batch between decode steps.  Each query's tokens
-    equal a stand-alone greedy decode of its full prompt where the margins are clear, all
-    pool blocks come back, and the summary reports decode throughput / TPOT."""
+    queries' prefills join the running batch between decode steps (chunked: prompts enter
+    96 tokens per forward, sharing forwards with the decodes).  Each query's tokens equal a
+    stand-alone greedy decode of its full prompt where the margins are clear, all pool
+    blocks come back, and the summary reports decode throughput / TPOT."""
     from paper_2504_11765_b200 import decode
     from paper_2504_11765_b200.engine import Engine
     from paper_2504_11765_b200.model import combo_tokens, get_spec, query_tokens
@@ -259,7 +261,8 @@ def test_runtime_continuous_batching_decode():
             decode.retire(eng, seqs[0])
     free0 = eng.pool.free_blocks
     with tempfile.TemporaryDirectory() as root:
-        cfg = RuntimeConfig(k=k, threshold=0.0, max_batch=4, persist="all", decode_tokens=n_dec)
+        cfg = RuntimeConfig(k=k, threshold=0.0, max_batch=4, persist="all", decode_tokens=n_dec,
+                            prefill_chunk=chunk)
         out = serve(eng, KvStore(root, memory_capacity_bytes=0), cfg, items, rate=400.0, tries=1)
     rep = out["summary"]
     assert rep["queries"] == len(items)
