@@ -38,6 +38,13 @@ def test_concurrent_oplog_replays_into_the_store_law(tmp_path):
     ths += [threading.Thread(target=reader, args=(s,)) for s in range(4)]
     [t.start() for t in ths]
     [t.join() for t in ths]
+    # a deterministic tail after the concurrent phase so every outcome is exercised whatever the
+    # interleaving was (readers can finish before the writers reach most keys): the oldest keys
+    # were evicted from the memory tier (disk hits), the newest are resident, one key is absent
+    store.put(keys[0], blobs[keys[0]])
+    for k in keys:
+        store.get(k)
+    store.get(KvKey(P.model_hash, (999,)))
     got = asdict(store.stats())
     want = replay(store.oplog, cap)
     for f, v in want.items():
