@@ -107,6 +107,30 @@ for name, req, reps in (("warm_hbm", hbm, 10), ("warm_host", host, 6), ("full_pr
     torch.cuda.empty_cache()
 same = len({res[k]["first_token"] for k in res}) == 1
 
+# ---- greedy decode after the first token (decode.py): the HBM-tier query, 32 steps
+from paper_2504_11765_b200 import decode as _decode
+
+dec = None
+try:
+    seqs = _decode.start(eng, [hbm], 40)
+    _decode.step(eng, seqs)
+    prev = torch.tensor([s.last for s in seqs], dtype=torch.int32, device=eng.device)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(32):
+        prev = _decode.step(eng, seqs, sync=False, dev_tokens=prev).clone()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / 32
+    step_bytes = 2 * (spec.nonembedding_params() + spec.vocab * spec.hidden) + kvb * (n_ctx + 17)
+    dec = {"batch": 1, "ms_per_token": ms, "tokens_per_s": 1e3 / ms, "bytes_per_step": step_bytes,
+           "frac_of_hbm": step_bytes / ms / 1e6 / peaks["hbm_gbs"]}
+    for s_ in seqs:
+        _decode.retire(eng, s_)
+except Exception as exc:  # the measurements above stand on their own
+    dec = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+torch.cuda.empty_cache()
+
 # ---- K3 sweep: cached tokens 1..20 documents, staged payload -> pool (HBM-bound)
 rows = []
 dev_payload = eng.stage(blob.payload_tensor())
@@ -141,7 +165,7 @@ print(json.dumps({
     "generation": {"tokens": len(toks), "device_ms": gen_ms, "tflops": gen_flops / gen_ms / 1e9,
                    "frac_of_burst": gen_flops / gen_ms / 1e9 / peaks["bf16_tflops"],
                    "wall_ms_with_fnv_d2h": gen_wall * 1e3},
-    "ttft_ms": res, "same_first_token": same,
+    "ttft_ms": res, "same_first_token": same, "decode": dec,
     "speedup_vs_full_prefill": {k: res["full_prefill"]["wall_ms_p50"] / res[k]["wall_ms_p50"]
                                 for k in ("warm_hbm", "warm_host")},
     "k3_sweep": rows, "hbm_peak_gbs": peaks["hbm_gbs"],
