@@ -68,6 +68,9 @@ static int make_tmap_q(CUtensorMap* m, const void* q, long long tokens, int hq, 
 #ifndef RDKV_ATTN_QTMEM
 #define RDKV_ATTN_QTMEM 1  // Q tile 0 in TMEM for its Q.K^T (issuers by kind, dh = 128)
 #endif
+#ifndef RDKV_ATTN_ONES
+#define RDKV_ATTN_ONES 0  // 1: row sums through a ones column in V (issuers by kind, dh = 128)
+#endif
 #ifndef RDKV_ATTN_PDB
 #define RDKV_ATTN_PDB 0  // 1: double-buffered P with the issuers by kind (dh = 128)
 #endif
@@ -111,7 +114,7 @@ struct TcCfg {
   // BYK (issuers by kind, one segment): no row-exchange / stream-K regions, so dh = 128
   // affords a fifth K/V stage (the stage of tile j + ST is released only when the later Q
   // tile's P.V(j) retired; K/V loads under full load take ~3.8k cycles)
-  static constexpr int STAGES = DH == 64 ? RDKV_ATTN_ST64 : BYK ? RDKV_ATTN_ST128_BYK : RDKV_ATTN_ST128;
+  static constexpr int STAGES = DH == 64 ? RDKV_ATTN_ST64 : BYK ? (RDKV_ATTN_ONES ? 4 : RDKV_ATTN_ST128_BYK) : RDKV_ATTN_ST128;
   static constexpr int KST = PP ? 3 : STAGES;  // K stages (PP: own ring)
   static constexpr int VST = PP ? 2 : STAGES;  // V stages (PP: own ring)
   static constexpr uint32_t QB = ROWS * DH * 2;    // one Q tile
@@ -119,10 +122,16 @@ struct TcCfg {
   static constexpr uint32_t OFF_Q = 0;             // [2 Q tiles]
   static constexpr uint32_t OFF_K = OFF_Q + 2 * QB;
   static constexpr uint32_t OFF_V = OFF_K + KST * KB;
+  // RDKV_ATTN_ONES (BYK, dh = 128): each V stage carries a third 64-column chunk of bf16 ones
+  // (written once), so P.V runs at N = DH + 16 and O's extra columns accumulate the row sums
+  // of the bf16 P the tensor cores multiplied (no FADD2 row sum in the softmax)
+  static constexpr bool ONES = RDKV_ATTN_ONES && BYK && DH == 128 && !PP;
+  static constexpr uint32_t VKB = KB + (ONES ? BKV * 128 : 0);  // V stage stride
+  static constexpr uint32_t OW = DH + (ONES ? 16 : 0);          // O columns per Q tile
   // row max / sum exchange of the two halves of a row (SPL = 2): [parity][2 Q tiles][2
   // halves][128 rows] fp32; PP has room for one parity only (a second barrier orders reuse)
   static constexpr int RED_PAR = PP ? 1 : 2;
-  static constexpr uint32_t OFF_RED = OFF_V + VST * KB;
+  static constexpr uint32_t OFF_RED = OFF_V + VST * VKB;
   static constexpr uint32_t OFF_BAR = OFF_RED + (BYK ? 0 : RED_PAR * 2 * 2 * ROWS * 4);
   // RDKV_ATTN_PDB (BYK at dh = 128): P double-buffered (TMEM has the room: S 128 + O 256 + P 4 x 32
   // = 512), so the softmax stores P(j) once P.V(j-2) retired instead of waiting for P.V(j-1).
@@ -140,19 +149,20 @@ struct TcCfg {
   static_assert(SMEM <= 232448, "attention smem exceeds 227 KB");
   // TMEM columns
   static constexpr uint32_t COL_S = 0;                          // S_i at BKV i
-  static constexpr uint32_t COL_O = 2 * BKV;                    // O_i at 2 BKV + DH i
-  static constexpr uint32_t COL_P = ALIAS ? 0 : 2 * BKV + 2 * DH;  // P_i at COL_P + (ALIAS ? BKV : BKV / 2) i
+  static constexpr uint32_t COL_O = 2 * BKV;                    // O_i at 2 BKV + OW i
+  static constexpr uint32_t COL_P = ALIAS ? 0 : 2 * BKV + 2 * OW;  // P_i at COL_P + (ALIAS ? BKV : BKV / 2) i
   static constexpr uint32_t P_STRIDE = ALIAS ? BKV : P_BUFS * BKV / 2;  // per Q tile (all P buffers)
   static_assert(COL_P + 2 * P_STRIDE <= 512, "TMEM: P does not fit");
   static constexpr uint32_t COL_L = COL_P + 2 * P_STRIDE;     // L_i at COL_L + 16 i (LSUM)
   // RDKV_ATTN_QTMEM (BYK, dh = 128, single P buffer): Q tile 0 staged in the last 64 TMEM columns
   // (tcgen05.cp), so its Q.K^T reads only K from smem: M = 128, N = 64 MMAs are smem-bound at
   // 48 cycles with both operands in smem (4 KB of Q + 2 KB of K per K = 16 step)
-  static constexpr bool QTMEM = RDKV_ATTN_QTMEM && BYK && DH == 128 && P_BUFS == 1;
+  static constexpr bool QTMEM = RDKV_ATTN_QTMEM && BYK && DH == 128 && P_BUFS == 1 && !ONES;
   static constexpr uint32_t COL_Q0 = COL_P + 2 * P_STRIDE;
   static_assert(!QTMEM || COL_Q0 + DH / 2 <= 512, "TMEM: Q tile 0 does not fit");
   static_assert(!LSUM || COL_L + 32 <= 512, "TMEM: L columns do not fit");
-  static_assert(COL_O + 2 * DH <= 512, "TMEM: S and O do not fit");
+  static_assert(COL_O + 2 * OW <= 512, "TMEM: S and O do not fit");
+  static_assert(!ONES || P_BUFS == 1, "ones-column row sums with a single P buffer");
 };
 
 // SPL softmax warps per query row (each takes BKV / SPL keys of a tile):
@@ -480,6 +490,15 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
     }
   }
   if (warp == NS + 1) tmem_alloc(tmem_slot, 512);
+  if constexpr (C::ONES) {
+    if (warp == NS + 3) {  // every V stage's third chunk: bf16 1.0 (never written by the TMA)
+      for (int st2 = 0; st2 < C::VST; ++st2) {
+        uint32_t* ones = reinterpret_cast<uint32_t*>(smem + C::OFF_V + st2 * C::VKB + C::KB);
+        for (int w = lane; w < BKV * 128 / 4; w += 32) ones[w] = 0x3F803F80u;
+      }
+      fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core (async proxy)
+    }
+  }
   if constexpr (C::LSUM) {
     if (warp == NS + 3) {  // constant B operand of the row-sum MMA: bf16 1.0 everywhere
       uint32_t* ones = reinterpret_cast<uint32_t*>(smem + C::OFF_ONES);
@@ -511,7 +530,7 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
   // softmax consumed S_i(j), i.e. after Q.K^T_i(j) retired, so this thread's commit after
   // P.V_i(j) also covers K(j); each Q tile's P.V issuer releases the stage once (count 2).
   auto pv_step = [&](int i, int j, bool mine) {
-    constexpr uint32_t idesc_pv = idesc_bf16_f32(ROWS, DH) | (1u << 16);  // B (V) is MN-major
+    constexpr uint32_t idesc_pv = idesc_bf16_f32(ROWS, C::OW) | (1u << 16);  // B (V) is MN-major
     const int st = j % ST;
     issuer_wait(&v_full[st], (j / ST) & 1);
     if (!mine) {  // no Q tile i in this unit: just release the stage
@@ -521,8 +540,8 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
     issuer_wait(pf(i, j), od_par(j));
     TRACE(2 + i, j, 5);
     tc_fence_after();
-    const uint32_t va = sb + C::OFF_V + st * C::KB;
-    const uint32_t tO = tmem + C::COL_O + i * DH;
+    const uint32_t va = sb + C::OFF_V + st * C::VKB;
+    const uint32_t tO = tmem + C::COL_O + i * C::OW;
     const uint32_t tP = tmem + C::COL_P + i * C::P_STRIDE + (j % C::P_BUFS) * (BKV / 2);
 #pragma unroll
     for (int kk = 0; kk < BKV / 16; ++kk)  // O_i (+)= P_i . V(j), P_i from TMEM
@@ -569,7 +588,7 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
           uint64_t* bar = isk ? &k_full[st] : &v_full[st];
           mbar_arrive_expect_tx(bar, C::KB);
           const CUtensorMap* tm = isk ? &tmK : &tmV;
-          uint8_t* dst = smem + (isk ? C::OFF_K : C::OFF_V) + st * C::KB;
+          uint8_t* dst = smem + (isk ? C::OFF_K + st * C::KB : C::OFF_V + st * C::VKB);
 #pragma unroll
           for (int c = 0; c < DH / 64; ++c)
 #pragma unroll
@@ -664,7 +683,7 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
           for (int c = 0; c < DH / 64; ++c)
 #pragma unroll
             for (int h = 0; h < NH; ++h)
-              tma_load_2d_nohint(&tmV, &v_full[st], smem + C::OFF_V + st * C::KB + c * (BKV * 128) + h * (HALF * 128),
+              tma_load_2d_nohint(&tmV, &v_full[st], smem + C::OFF_V + st * C::VKB + c * (BKV * 128) + h * (HALF * 128),
                                  c * 64, rows[h]);
         }
         __syncwarp();
@@ -722,10 +741,10 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
 #pragma unroll
             for (int h = 0; h < NH; ++h)
               if (p.kv_evict_first)  // a streamed K/V tile is read once: keep L2 for the prefetched weights
-                tma_load_2d(&tmV, &v_full[st], smem + C::OFF_V + st * C::KB + c * (BKV * 128) + h * (HALF * 128),
+                tma_load_2d(&tmV, &v_full[st], smem + C::OFF_V + st * C::VKB + c * (BKV * 128) + h * (HALF * 128),
                             c * 64, rows[h], pol_kv);
               else
-                tma_load_2d_nohint(&tmV, &v_full[st], smem + C::OFF_V + st * C::KB + c * (BKV * 128) + h * (HALF * 128),
+                tma_load_2d_nohint(&tmV, &v_full[st], smem + C::OFF_V + st * C::VKB + c * (BKV * 128) + h * (HALF * 128),
                                    c * 64, rows[h]);
           // the smem ring holds only STAGES tiles and a stage is refilled only after its
           // P.V retired: with the KV stream coming from HBM under full load (~4.5k cycles
@@ -784,13 +803,13 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
           umma_commit(&kv_empty[0]);
           for (int jl = 0; jl < nt; ++jl) {
             const int vs = jl % VST;
-            const uint32_t va = sb + C::OFF_V + vs * C::KB;
+            const uint32_t va = sb + C::OFF_V + vs * C::VKB;
             for (int i = 0; i < nq; ++i) {
               issuer_wait(pf(i, jl), od_par(jl));
               if (i == 0) issuer_wait(&v_full[vs], (jl / VST) & 1);
               TRACE(2 + i, jl, 4);
               tc_fence_after();
-              const uint32_t tO = tmem + C::COL_O + i * DH, tP = tmem + C::COL_P + i * C::P_STRIDE;
+              const uint32_t tO = tmem + C::COL_O + i * C::OW, tP = tmem + C::COL_P + i * C::P_STRIDE;
 #pragma unroll
               for (int kk = 0; kk < BKV / 16; ++kk) {  // O_i (+)= P_i . V(jl); each key half's P inside its S columns
                 const uint32_t pcol = (kk / (KH / 16)) * KH + (kk % (KH / 16)) * 8;
@@ -869,7 +888,7 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
       constexpr uint32_t idesc_qk = idesc_bf16_f32(ROWS, BKV);
       constexpr uint32_t idesc_pv = idesc_bf16_f32(ROWS, DH) | (1u << 16);  // B (V) is MN-major
       const uint32_t qa = sb + C::OFF_Q + i * C::QB;
-      const uint32_t tS = tmem + C::COL_S + i * BKV, tO = tmem + C::COL_O + i * DH;
+      const uint32_t tS = tmem + C::COL_S + i * BKV, tO = tmem + C::COL_O + i * C::OW;
       const uint32_t tP = tmem + C::COL_P + i * C::P_STRIDE;
       auto issue_qk = [&](int stg, bool last) {  // S_i = Q_i . K^T of the tile in stage stg
         const uint32_t ka = sb + C::OFF_K + stg * C::KB;
@@ -930,7 +949,7 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
           issuer_wait(pf(i, ti), od_par(ti));
           if (j > 0) TRACE(2 + i, ti, 5);
           tc_fence_after();
-          const uint32_t va = sb + C::OFF_V + st * C::KB;
+          const uint32_t va = sb + C::OFF_V + st * C::VKB;
 #pragma unroll
           for (int kk = 0; kk < BKV / 16; ++kk) {  // O_i (+)= P_i . V(j), P_i from TMEM
             // P of keys [16kk, 16kk+16): with P over S each half writes inside its own S columns
@@ -1037,7 +1056,7 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
     auto softmax_bar = [&]() { asm volatile("bar.sync %0, %1;" ::"n"(SK_BAR), "n"(NS * 32) : "memory"); };
     constexpr int OH = DH / SPL;  // O columns of this half
     const uint32_t tS = tmem + C::COL_S + i * BKV + h * KH + lane_off;
-    const uint32_t tO = tmem + C::COL_O + i * DH + h * OH + lane_off;
+    const uint32_t tO = tmem + C::COL_O + i * C::OW + h * OH + lane_off;
     // P columns of this half: inside its own S columns when P is written over S
     const uint32_t tP = tmem + C::COL_P + i * C::P_STRIDE + h * (C::ALIAS ? KH : KH / 2) + lane_off;
     const float sl2 = p.scale_log2;
@@ -1102,7 +1121,7 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
                 x2 = ex2_approx(x2);
                 x3 = ex2_approx(x3);
               }
-              if constexpr (!C::LSUM) {
+              if constexpr (!C::LSUM && !C::ONES) {
                 fadd2(s0, s1, s0, s1, x0, x1);
                 fadd2(s2, s3, s2, s3, x2, x3);
               }
@@ -1157,6 +1176,14 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
             for (int e = 0; e < 16; ++e) lv[e] = __float_as_uint(__uint_as_float(lv[e]) * f);
             tmem_st16(tmem + C::COL_L + i * 16 + lane_off, lv);
           }
+          if (C::ONES && rescale) {  // the ones-column row sums at the new scale too
+            uint32_t lv[16];
+            tmem_ld16(tO + DH, lv);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) lv[e] = __float_as_uint(__uint_as_float(lv[e]) * f);
+            tmem_st16(tO + DH, lv);
+          }
           if (rescale) {  // this half of the O_i row *= f before P_i.V(j) accumulates into it
 #pragma unroll
             for (int c = 0; c < OH / 32; ++c) {
@@ -1186,6 +1213,12 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
         if constexpr (C::LSUM) {  // the row sum of the bf16 P the tensor cores multiplied V by
           uint32_t lv[16];
           tmem_ld16(tmem + C::COL_L + i * 16 + lane_off, lv);
+          tmem_ld_wait();
+          l = __uint_as_float(lv[0]);
+        }
+        if constexpr (C::ONES) {  // the ones columns of O_i: the row sum of the bf16 P
+          uint32_t lv[16];
+          tmem_ld16(tO + DH, lv);
           tmem_ld_wait();
           l = __uint_as_float(lv[0]);
         }
