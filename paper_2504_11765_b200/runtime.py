@@ -373,17 +373,7 @@ class Instance:
         """One decode step for every live sequence (continuous batching); finished
         sequences leave the batch, their queries become DONE."""
         decode.step(self.eng, [s for s, _ in self._live])
-        now = time.monotonic()
-        keep = []
-        for seq, ri in self._live:
-            if seq.done:
-                res = self.results[ri]
-                res.done, res.n_tokens, res.tokens = now, len(seq.tokens), tuple(seq.tokens)
-                decode.retire(self.eng, seq)
-                self.cp.qstate_cas(res.index, QState.DISPATCHED, QState.DONE)
-            else:
-                keep.append((seq, ri))
-        self._live = keep
+        self._retire_done(time.monotonic())
 
     def _take_batch(self, limit: int | None = None) -> list:
         """An idle instance takes the oldest waiting queries (up to max_batch /
