@@ -234,6 +234,12 @@ constexpr int EMU_OF_8 = RDKV_ATTN_EMU;  // exp2 of this many of every 8 score g
 #ifndef RDKV_ATTN_PPF
 #define RDKV_ATTN_PPF 0  // ping-pong producer: L2 prefetch distance in tiles ahead of the K stream (2-8 slower)
 #endif
+#ifndef RDKV_ATTN_IDLE
+#define RDKV_ATTN_IDLE 0  // 1: softmax warps with no real query row skip the exp work (decode: G valid
+                          // rows of 128); measured no faster — decode attention is HBM-bound (5.15-5.19
+                          // vs 5.16-5.22 ms per C3 decode step, identical tokens)
+#endif
+constexpr bool IDLE_SKIP = RDKV_ATTN_IDLE != 0;
 #ifndef RDKV_ATTN_SPIN
 #define RDKV_ATTN_SPIN 1
 #endif
@@ -1075,10 +1081,28 @@ __global__ void __launch_bounds__(RolesOf<DH, SPL, SK, PP>::THREADS, 1)
       if (act) {
         // padded rows pretend to be the last valid position so no row is fully masked
         const int qpos = ok ? u.pos0 + i * TPT + r / G : u.kv_len - 1;
+        // a warp none of whose rows is a real query row (decode: G valid rows of 128) only
+        // keeps the handshakes: its P rows feed O rows that are never stored
+        const bool idle = IDLE_SKIP && !PP && SPL == 1 && !C::LSUM && !C::ONES && !__any_sync(0xffffffffu, ok);
         TRACE(i, ti, 6);
         for (int j = 0; j < nt; ++j, ++ti) {
           mbar_wait(&s_full[i], ti & 1);
           tc_fence_after();
+          if (idle) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[i]);
+            // as below: no p_full arrival for tile ti before P.V(ti - P_BUFS) retired, or the
+            // early arrival would complete the previous tile's phase
+            const int tw = ti - C::P_BUFS;
+            if (!PP && tw >= ti - j) {
+              mbar_wait(od(i, tw), od_par(tw));
+              tc_fence_after();
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(pf(i, ti));
+            continue;
+          }
           if (j == 0) TRACE(i, ti, 7);
           if (j + 1 < nt) TRACE(i, ti, 2);
           uint32_t sv[KH];
