@@ -1460,8 +1460,12 @@ int launch_tc(const AttnParams& p, int n_seqs, int max_new, cudaStream_t st) {
   // (only when a split keeps >= 8 KV tiles: a CTA's fixed cost — TMEM / barrier setup,
   // pipeline fill, the O store — is several tiles' worth; the C2 batch, 21 tiles per
   // unit, measured 77 -> 103 us with 5-tile splits, a 41-tile dh=128 batch 212 -> 189 us)
+  static const int tail_min = [] {  // KV tiles a split must keep (RDKV_ATTN_TAIL_MIN, A/B)
+    const char* e = std::getenv("RDKV_ATTN_TAIL_MIN");
+    return e ? std::atoi(e) : 8;
+  }();
   if (tail_env && p.split_o && ctas > sms && last > 0.0 && last < 0.9 && s_a >= 1 && s_a < n_seqs &&
-      max_tiles >= 8 * KT && (size_t)KT * p.n_tokens * p.hq * (DH * 4 + 8) <= p.split_bytes) {
+      max_tiles >= tail_min * KT && (size_t)KT * p.n_tokens * p.hq * (DH * 4 + 8) <= p.split_bytes) {
     RDKV_TRY((set_smem_attr<DH, SPL, false, PP>()));
     AttnParams b = q;
     b.seq_off = s_a;
