@@ -119,7 +119,11 @@ RDKV_API int64_t rdkv_file_size(const char* path);
 
 /* Read a whole blob file into `buf` (capacity `cap`, normally pinned host
  * memory) placing the payload at an `align`-byte boundary (payload offset in
- * the file is 46+8k, never aligned).  With verify != 0 it runs the same
+ * the file is 46+8k, never aligned), with parallel buffered preads.  align = 0:
+ * O_DIRECT reads instead (page cache bypassed, block-aligned requests on up to
+ * 8 threads): the file's first byte lands on a 4096-byte boundary, `cap` must
+ * cover that pad plus the size rounded up to 4096, and file systems that refuse
+ * O_DIRECT fall back to buffered reads.  With verify != 0 it runs the same
  * validation as rdkv_blob_check (KvStore.get disk path: store.py:266-267).
  * On success *file_off is where the file's first byte landed in `buf` and
  * *payload_off where the payload starts. */

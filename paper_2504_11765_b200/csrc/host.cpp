@@ -171,6 +171,50 @@ int read_all(int fd, void* p, size_t n) {
   return 0;
 }
 
+// O_DIRECT whole-file read into a 4096-aligned `p` (page cache bypassed): the same
+// 2-MiB pieces on up to 8 threads; every request is block-aligned (the last one is
+// rounded up and comes back short at EOF).  Returns 0, -1 (I/O error: errno), or
+// -3 when the file system refuses O_DIRECT (caller falls back to buffered reads).
+int read_all_direct(int fd, void* p, size_t n) {
+  constexpr size_t kPiece = 2u << 20, kBlk = 4096;
+  const size_t pieces = (n + kPiece - 1) / kPiece;
+  const int threads = (int)std::min<size_t>(8, std::max<size_t>(1, pieces));
+  const size_t per = (pieces + threads - 1) / threads * kPiece;
+  std::vector<std::thread> pool;
+  std::vector<int> rc(threads, 0);
+  for (int t = 0; t < threads; ++t) {
+    const size_t a = (size_t)t * per, b = std::min(n, a + per);
+    if (a >= b) break;
+    pool.emplace_back([&, t, a, b] {
+      uint8_t* dst = static_cast<uint8_t*>(p) + a;
+      size_t off = a;
+      const size_t end = (b + kBlk - 1) / kBlk * kBlk;  // block-rounded request end
+      while (off < b) {
+        ssize_t r = ::pread(fd, dst, end - off, (off_t)off);
+        if (r < 0) {
+          if (errno == EINTR) continue;
+          rc[t] = errno == EINVAL ? -3 : -1;
+          return;
+        }
+        if (r == 0) {  // EOF before b: the file shrank under us
+          rc[t] = -1;
+          return;
+        }
+        dst += r;
+        off += (size_t)r;
+        if ((size_t)r % kBlk && off < b) {  // a short unaligned read before the end: cannot continue direct
+          rc[t] = -3;
+          return;
+        }
+      }
+    });
+  }
+  for (auto& th : pool) th.join();
+  for (int r : rc)
+    if (r) return r;
+  return 0;
+}
+
 }  // namespace
 }  // namespace rdkv
 
@@ -257,7 +301,8 @@ int64_t rdkv_file_size(const char* path) {
 
 int rdkv_blob_read(const char* path, void* buf, size_t cap, size_t align, int verify, rdkv_header* h,
                    uint64_t* ids, size_t ids_cap, size_t* file_off, size_t* payload_off) {
-  if (align == 0 || (align & (align - 1))) return set_error(RDKV_ERR_ARG, "align must be a power of two");
+  if (align & (align - 1)) return set_error(RDKV_ERR_ARG, "align must be a power of two (or 0: O_DIRECT)");
+  const bool direct = align == 0;
   int fd = ::open(path, O_RDONLY | O_CLOEXEC);
   if (fd < 0) return set_error(RDKV_ERR_IO, "open %s: %s", path, strerror(errno));
   struct stat st;
@@ -276,14 +321,26 @@ int rdkv_blob_read(const char* path, void* buf, size_t cap, size_t align, int ve
     }
     hl = kFixed + 8 * (size_t)load_le<uint16_t>(head + 14) + kTail;
   }
-  // pad so that the payload lands on an absolute `align` boundary
-  const size_t pad = (align - ((reinterpret_cast<uintptr_t>(buf) + hl) % align)) % align;
-  if (cap < pad + size) {
+  // pad so that the payload lands on an absolute `align` boundary; O_DIRECT (align 0):
+  // the file's first byte on a 4096-byte boundary instead (block-aligned DMA targets)
+  constexpr size_t kBlk = 4096;
+  const uintptr_t b0 = reinterpret_cast<uintptr_t>(buf);
+  const size_t pad = direct ? (kBlk - b0 % kBlk) % kBlk : (align - ((b0 + hl) % align)) % align;
+  const size_t need = pad + (direct ? (size + kBlk - 1) / kBlk * kBlk : size);
+  if (cap < need) {
     ::close(fd);
-    return set_error(RDKV_ERR_ARG, "buffer too small for %s (%zu < %zu)", path, cap, pad + size);
+    return set_error(RDKV_ERR_ARG, "buffer too small for %s (%zu < %zu)", path, cap, need);
   }
   uint8_t* dst = static_cast<uint8_t*>(buf) + pad;
-  const int r = read_all(fd, dst, size);
+  int r = -3;
+  if (direct) {
+    const int dfd = ::open(path, O_RDONLY | O_CLOEXEC | O_DIRECT);
+    if (dfd >= 0) {
+      r = read_all_direct(dfd, dst, size);
+      ::close(dfd);
+    }
+  }
+  if (r == -3) r = read_all(fd, dst, size);  // buffered (or O_DIRECT refused by the file system)
   ::close(fd);
   if (r != 0) return set_error(RDKV_ERR_IO, "read %s failed", path);
   size_t poff = 0;

@@ -66,13 +66,23 @@ def test_memory_vs_disk_hit(tmp_path):
     assert r.outcome is Outcome.DISK_HIT and r.blob == b and r.load_cost_bytes == size
 
 
-def test_disk_hit_payload_is_aligned_tensor(tmp_path):
+@pytest.mark.parametrize("direct", ["0", "1"])
+def test_disk_hit_payload_is_aligned_tensor(tmp_path, monkeypatch, direct):
+    """Buffered reads put the payload on a 256-B boundary; O_DIRECT reads (the default)
+    put the file's first byte on a 4096-B boundary.  Same bytes either way, for a blob
+    smaller than one block and one that ends mid-block."""
+    monkeypatch.setenv("RDKV_ODIRECT", direct)
     st = KvStore(tmp_path)
-    st.put(key_for(PROFILE, [5, 6]), blob([5, 6], tokens=3))
-    r = KvStore(tmp_path).get(key_for(PROFILE, [5, 6]))
-    assert r.outcome is Outcome.DISK_HIT
-    assert r.blob.payload.data_ptr() % 256 == 0
-    assert r.blob.payload_bytes() == blob([5, 6], tokens=3).payload
+    for ids, tokens in (([5, 6], 3), ([7], 2900)):
+        st.put(key_for(PROFILE, ids), blob(ids, tokens=tokens))
+        r = KvStore(tmp_path).get(key_for(PROFILE, ids))
+        assert r.outcome is Outcome.DISK_HIT
+        hl = 46 + 8 * len(ids)
+        if direct == "0":
+            assert r.blob.payload.data_ptr() % 256 == 0
+        else:
+            assert (r.blob.payload.data_ptr() - hl) % 4096 == 0
+        assert r.blob.payload_bytes() == blob(ids, tokens=tokens).payload
 
 
 def test_immutability_and_noop_reput(tmp_path):
@@ -157,7 +167,9 @@ def test_reference_store_reads_our_files(tmp_path):
         assert r.blob.payload == blob(ids, tokens=len(ids)).payload
 
 
-def test_large_blob_file_roundtrip_parallel_read(tmp_path):
+@pytest.mark.parametrize("direct", ["0", "1"])
+def test_large_blob_file_roundtrip_parallel_read(tmp_path, monkeypatch, direct):
+    monkeypatch.setenv("RDKV_ODIRECT", direct)
     # > 2 MiB files are read by several threads; sizes just past a piece boundary
     # must still include the tail bytes (header + payload + checksum verify)
     from paper_2504_11765_b200.codec import ModelProfile, synth_blob
