@@ -10,6 +10,7 @@
 #include <cerrno>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -175,10 +176,19 @@ int read_all(int fd, void* p, size_t n) {
 // 2-MiB pieces on up to 8 threads; every request is block-aligned (the last one is
 // rounded up and comes back short at EOF).  Returns 0, -1 (I/O error: errno), or
 // -3 when the file system refuses O_DIRECT (caller falls back to buffered reads).
+int io_threads() {
+  static const int t = [] {
+    const char* e = std::getenv("RDKV_IO_THREADS");  // A/B knob (default 8)
+    const int v = e ? std::atoi(e) : 8;
+    return v < 1 ? 1 : v > 64 ? 64 : v;
+  }();
+  return t;
+}
+
 int read_all_direct(int fd, void* p, size_t n) {
   constexpr size_t kPiece = 2u << 20, kBlk = 4096;
   const size_t pieces = (n + kPiece - 1) / kPiece;
-  const int threads = (int)std::min<size_t>(8, std::max<size_t>(1, pieces));
+  const int threads = (int)std::min<size_t>((size_t)io_threads(), std::max<size_t>(1, pieces));
   const size_t per = (pieces + threads - 1) / threads * kPiece;
   std::vector<std::thread> pool;
   std::vector<int> rc(threads, 0);
