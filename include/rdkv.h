@@ -71,6 +71,14 @@ RDKV_API void rdkv_fnv1a64_many(const void* const* bufs, const size_t* lens, siz
 RDKV_API size_t rdkv_fnv1a64_device_scratch(size_t len);
 RDKV_API int rdkv_fnv1a64_device(const void* data, size_t len, uint64_t seed, void* scratch, size_t scratch_bytes,
                                  uint64_t* out_dev, void* stream);
+/* The same in two steps for a payload still arriving (streamed disk hit): the
+ * per-chunk automaton pass over the whole chunks of bytes [0, ready), from chunk
+ * `chunk_begin` on — returns the next chunk to run (pass ready = len for the
+ * rest) — then the stitch / affine / combine passes.  Same scratch, same result. */
+RDKV_API int64_t rdkv_fnv1a64_device_partial(const void* data, size_t len, size_t ready, int64_t chunk_begin,
+                                             void* scratch, size_t scratch_bytes, void* stream);
+RDKV_API int rdkv_fnv1a64_device_finish(const void* data, size_t len, uint64_t seed, void* scratch,
+                                        size_t scratch_bytes, uint64_t* out_dev, void* stream);
 
 /* Fixed-width view of the .rdkv header (codec.py:8-13, 35-36, 110-137). */
 typedef struct rdkv_header {
@@ -130,6 +138,14 @@ RDKV_API int64_t rdkv_file_size(const char* path);
 RDKV_API int rdkv_blob_read(const char* path, void* buf, size_t cap, size_t align, int verify,
                    rdkv_header* h, uint64_t* doc_ids, size_t ids_cap, size_t* file_off,
                    size_t* payload_off);
+
+/* Read file bytes [off, off + len) into `dst` (the part of a blob file a
+ * streamed disk hit has not read yet; store.read_blob_file overlaps each
+ * segment's H2D copy with the next segment's read).  direct != 0: O_DIRECT,
+ * `dst` and `off` 4096-aligned, `cap` >= len rounded up to 4096 (buffered
+ * fallback where the file system refuses O_DIRECT).  Returns the bytes read
+ * (short only at end of file), or < 0. */
+RDKV_API int64_t rdkv_file_read_range(const char* path, void* dst, size_t cap, uint64_t off, size_t len, int direct);
 
 /* Drop a file's pages from the OS page cache (cold-read benchmarking). */
 RDKV_API int rdkv_drop_page_cache(const char* path);

@@ -70,10 +70,13 @@ SIGNATURES: dict[str, tuple] = {
     "rdkv_file_size": (_i64, [_cp]),
     "rdkv_blob_read": (_i32, [_cp, _vp, _sz, _sz, _i32, C.POINTER(RdkvHeader), C.POINTER(_u64), _sz,
                               C.POINTER(_sz), C.POINTER(_sz)]),
+    "rdkv_file_read_range": (_i64, [_cp, _vp, _sz, _u64, _sz, _i32]),
     "rdkv_drop_page_cache": (_i32, [_cp]),
     "rdkv_gemm_bf16": (_i32, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _i32, _i32, _vp]),
     "rdkv_fnv1a64_device_scratch": (_sz, [_sz]),
     "rdkv_fnv1a64_device": (_i32, [_vp, _sz, _u64, _vp, _sz, _vp, _vp]),
+    "rdkv_fnv1a64_device_partial": (_i64, [_vp, _sz, _sz, _i64, _vp, _sz, _vp]),
+    "rdkv_fnv1a64_device_finish": (_i32, [_vp, _sz, _u64, _vp, _sz, _vp, _vp]),
     "rdkv_attention": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32,
                               _i32, _i32, _i32, _i32, _i32, _vp, _sz, _vp]),
     "rdkv_attention_scratch_bytes": (_sz, [_i32, _i32, _i32]),

@@ -138,6 +138,41 @@ def fnv1a64_device_async(data, seed: int = FNV_OFFSET, stream=None):
     return out
 
 
+class StreamingFnv:
+    """Device FNV-1a of a CUDA uint8 buffer that fills front to back (a streamed disk
+    hit): ``advance(ready)`` runs the per-chunk automaton pass over the newly complete
+    16-KiB chunks on ``stream``; ``result()`` runs the rest and returns the checksum —
+    equal to fnv1a64_device of the whole buffer."""
+
+    def __init__(self, data, seed: int = FNV_OFFSET, stream=None) -> None:
+        import torch
+
+        self.raw = data.reshape(-1)
+        self.n = self.raw.numel()
+        self.seed = seed & _U64
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.raw.device)
+        L = _lib.lib()
+        self.need = int(L.rdkv_fnv1a64_device_scratch(self.n))
+        with torch.cuda.stream(self.stream):
+            self.ws = torch.empty(self.need, dtype=torch.uint8, device=self.raw.device)
+            self.out = torch.empty(1, dtype=torch.int64, device=self.raw.device)
+        self.next = 0
+
+    def advance(self, ready: int) -> None:
+        c = int(_lib.lib().rdkv_fnv1a64_device_partial(self.raw.data_ptr(), self.n, min(ready, self.n), self.next,
+                                                       self.ws.data_ptr(), self.need, self.stream.cuda_stream))
+        _lib.check(c)
+        self.next = c
+
+    def result(self) -> int:
+        self.advance(self.n)
+        L = _lib.lib()
+        _lib.check(L.rdkv_fnv1a64_device_finish(self.raw.data_ptr(), self.n, self.seed, self.ws.data_ptr(), self.need,
+                                                self.out.data_ptr(), self.stream.cuda_stream))
+        self.stream.synchronize()
+        return int(self.out.item()) & _U64
+
+
 def fnv1a64_many(buffers: Sequence, threads: int = 8) -> list[int]:
     """FNV-1a of several independent buffers in parallel (one chain per buffer)."""
     n = len(buffers)

@@ -50,12 +50,12 @@ __device__ __forceinline__ uint64_t pow_p(uint64_t e) {
 // ((p ^ bb) & 0x00FF00FF) and one IMAD (* 0xB3, < 2^16 so the halves never mix).
 constexpr int kWarpsPerBlock = 4;
 __global__ void __launch_bounds__(32 * kWarpsPerBlock) fnv_fsm_kernel(const uint8_t* __restrict__ data, size_t n,
-                                                                      int chunks, uint8_t* __restrict__ end_state) {
+                                                                      int c0, int chunks, uint8_t* __restrict__ end_state) {
   pdl_trigger();
   pdl_wait();
   __shared__ __align__(16) uint32_t buf[kWarpsPerBlock][kStage / 4];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x * kWarpsPerBlock + warp;
+  const int c = c0 + blockIdx.x * kWarpsPerBlock + warp;  // chunks [c0, chunks)
   if (c >= chunks) return;
   const size_t base = (size_t)c * kChunk;
   const int len = (int)min((size_t)kChunk, n - base);
@@ -189,15 +189,42 @@ extern "C" size_t rdkv_fnv1a64_device_scratch(size_t len) {
   return chunks * 256 + chunks + chunks * 8 + 64;
 }
 
-// Device FNV-1a of `len` bytes at `data` (device memory), written to
-// *out_dev (device uint64) asynchronously on `stream`.
-extern "C" int rdkv_fnv1a64_device(const void* data, size_t len, uint64_t seed, void* scratch, size_t scratch_bytes,
-                                   uint64_t* out_dev, void* stream) {
-  if (!out_dev || (len && !data)) return set_error(RDKV_ERR_ARG, "fnv_device: null argument");
+namespace {
+int check_args(const void* data, size_t len, const void* scratch, size_t scratch_bytes) {
+  if (len && !data) return set_error(RDKV_ERR_ARG, "fnv_device: null argument");
   const size_t chunks = (len + kChunk - 1) / kChunk;
   if (chunks > (size_t)1 << 30) return set_error(RDKV_ERR_ARG, "fnv_device: input too large");
   if (scratch_bytes < rdkv_fnv1a64_device_scratch(len) || (chunks && !scratch))
     return set_error(RDKV_ERR_ARG, "fnv_device: scratch too small");
+  return 0;
+}
+}  // namespace
+
+// Pass 1 alone for the whole 16-KiB chunks of bytes [0, ready) of a `len`-byte
+// input, from chunk `chunk_begin` on (a payload still arriving: run it per landed
+// segment, then rdkv_fnv1a64_device_finish).  Returns the next chunk to run.
+extern "C" int64_t rdkv_fnv1a64_device_partial(const void* data, size_t len, size_t ready, int64_t chunk_begin,
+                                               void* scratch, size_t scratch_bytes, void* stream) {
+  RDKV_TRY(check_args(data, len, scratch, scratch_bytes));
+  const size_t chunks = (len + kChunk - 1) / kChunk;
+  const int64_t c1 = ready >= len ? (int64_t)chunks : (int64_t)(ready / kChunk);
+  if (chunk_begin < 0 || chunk_begin > c1) return set_error(RDKV_ERR_ARG, "fnv_device: bad chunk range");
+  if (c1 > chunk_begin) {
+    const int n = (int)(c1 - chunk_begin);
+    CUDA_TRY(launch_k(fnv_fsm_kernel, dim3((n + kWarpsPerBlock - 1) / kWarpsPerBlock), dim3(32 * kWarpsPerBlock), 0,
+                      static_cast<cudaStream_t>(stream), static_cast<const uint8_t*>(data), len, (int)chunk_begin,
+                      (int)c1, static_cast<uint8_t*>(scratch)));
+    CUDA_TRY(cudaGetLastError());
+  }
+  return c1;
+}
+
+// Passes 2-4 (after pass 1 covered every chunk): *out_dev on `stream`.
+extern "C" int rdkv_fnv1a64_device_finish(const void* data, size_t len, uint64_t seed, void* scratch,
+                                          size_t scratch_bytes, uint64_t* out_dev, void* stream) {
+  if (!out_dev) return set_error(RDKV_ERR_ARG, "fnv_device: null argument");
+  RDKV_TRY(check_args(data, len, scratch, scratch_bytes));
+  const size_t chunks = (len + kChunk - 1) / kChunk;
   auto st = static_cast<cudaStream_t>(stream);
   auto* ws = static_cast<uint8_t*>(scratch);
   uint8_t* end_state = ws;                                   // [chunks][256]
@@ -206,8 +233,6 @@ extern "C" int rdkv_fnv1a64_device(const void* data, size_t len, uint64_t seed, 
   const auto* d = static_cast<const uint8_t*>(data);
   const int nc = (int)chunks;
   if (nc > 0) {
-    CUDA_TRY(launch_k(fnv_fsm_kernel, dim3((nc + kWarpsPerBlock - 1) / kWarpsPerBlock), dim3(32 * kWarpsPerBlock), 0, st,
-                      d, len, nc, end_state));
     CUDA_TRY(launch_k(fnv_stitch_kernel, dim3(1), dim3(256), 0, st, (const uint8_t*)end_state, nc, seed, start_state));
     CUDA_TRY(launch_k(fnv_affine_kernel, dim3((nc + 127) / 128), dim3(128), 0, st, d, len, nc,
                       (const uint8_t*)start_state, cterm));
@@ -215,4 +240,14 @@ extern "C" int rdkv_fnv1a64_device(const void* data, size_t len, uint64_t seed, 
   CUDA_TRY(launch_k(fnv_combine_kernel, dim3(1), dim3(32), 0, st, (const uint64_t*)cterm, nc, len, seed, out_dev));
   CUDA_TRY(cudaGetLastError());
   return 0;
+}
+
+// Device FNV-1a of `len` bytes at `data` (device memory), written to
+// *out_dev (device uint64) asynchronously on `stream`.
+extern "C" int rdkv_fnv1a64_device(const void* data, size_t len, uint64_t seed, void* scratch, size_t scratch_bytes,
+                                   uint64_t* out_dev, void* stream) {
+  if (!out_dev) return set_error(RDKV_ERR_ARG, "fnv_device: null argument");
+  const int64_t c = rdkv_fnv1a64_device_partial(data, len, len, 0, scratch, scratch_bytes, stream);
+  if (c < 0) return (int)c;
+  return rdkv_fnv1a64_device_finish(data, len, seed, scratch, scratch_bytes, out_dev, stream);
 }

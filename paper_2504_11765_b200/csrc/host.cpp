@@ -153,18 +153,18 @@ int pread_all(int fd, uint8_t* b, size_t n, off_t off) {
 // Whole-file read.  Cold multi-MiB blobs are read by several threads at once
 // (contiguous 2-MiB-aligned ranges): a single buffered reader keeps one request
 // in flight, several keep the NVMe queue busy.
-int read_all(int fd, void* p, size_t n) {
+int read_all(int fd, void* p, size_t n, size_t base = 0) {  // file bytes [base, base + n)
   constexpr size_t kPiece = 2u << 20;
   const size_t pieces = n / kPiece;
   const int threads = (int)std::min<size_t>(8, pieces);
-  if (threads < 2) return pread_all(fd, static_cast<uint8_t*>(p), n, 0);
+  if (threads < 2) return pread_all(fd, static_cast<uint8_t*>(p), n, (off_t)base);
   const size_t per = (pieces + threads - 1) / threads * kPiece;
   std::vector<std::thread> pool;
   std::vector<int> rc(threads, 0);
   for (int t = 0; t < threads; ++t) {
     const size_t a = (size_t)t * per, b = t + 1 == threads ? n : std::min(n, a + per);  // last range takes the tail
     if (a >= b) break;
-    pool.emplace_back([&, t, a, b] { rc[t] = pread_all(fd, static_cast<uint8_t*>(p) + a, b - a, (off_t)a); });
+    pool.emplace_back([&, t, a, b] { rc[t] = pread_all(fd, static_cast<uint8_t*>(p) + a, b - a, (off_t)(base + a)); });
   }
   for (auto& th : pool) th.join();
   for (int r : rc)
@@ -185,7 +185,7 @@ int io_threads() {
   return t;
 }
 
-int read_all_direct(int fd, void* p, size_t n) {
+int read_all_direct(int fd, void* p, size_t n, size_t base = 0) {  // file bytes [base, base + n)
   constexpr size_t kPiece = 2u << 20, kBlk = 4096;
   const size_t pieces = (n + kPiece - 1) / kPiece;
   const int threads = (int)std::min<size_t>((size_t)io_threads(), std::max<size_t>(1, pieces));
@@ -200,7 +200,7 @@ int read_all_direct(int fd, void* p, size_t n) {
       size_t off = a;
       const size_t end = (b + kBlk - 1) / kBlk * kBlk;  // block-rounded request end
       while (off < b) {
-        ssize_t r = ::pread(fd, dst, end - off, (off_t)off);
+        ssize_t r = ::pread(fd, dst, end - off, (off_t)(base + off));
         if (r < 0) {
           if (errno == EINTR) continue;
           rc[t] = errno == EINVAL ? -3 : -1;
@@ -366,6 +366,39 @@ int rdkv_blob_read(const char* path, void* buf, size_t cap, size_t align, int ve
   if (file_off) *file_off = pad;
   if (payload_off) *payload_off = pad + poff;
   return 0;
+}
+
+int64_t rdkv_file_read_range(const char* path, void* dst, size_t cap, uint64_t off, size_t len, int direct) {
+  constexpr size_t kBlk = 4096;
+  if (!dst || len == 0) return set_error(RDKV_ERR_ARG, "read_range: empty request");
+  const size_t need = direct ? (len + kBlk - 1) / kBlk * kBlk : len;
+  if (cap < need) return set_error(RDKV_ERR_ARG, "read_range: buffer too small (%zu < %zu)", cap, need);
+  if (direct && ((reinterpret_cast<uintptr_t>(dst) | off) % kBlk))
+    return set_error(RDKV_ERR_ARG, "read_range: O_DIRECT needs a 4096-aligned buffer and offset");
+  int fd = ::open(path, O_RDONLY | O_CLOEXEC);
+  if (fd < 0) return set_error(RDKV_ERR_IO, "open %s: %s", path, strerror(errno));
+  struct stat st;
+  if (::fstat(fd, &st) != 0) {
+    ::close(fd);
+    return set_error(RDKV_ERR_IO, "stat %s: %s", path, strerror(errno));
+  }
+  if (off >= (uint64_t)st.st_size) {
+    ::close(fd);
+    return 0;
+  }
+  const size_t n = std::min<uint64_t>(len, (uint64_t)st.st_size - off);
+  int r = -3;
+  if (direct) {
+    const int dfd = ::open(path, O_RDONLY | O_CLOEXEC | O_DIRECT);
+    if (dfd >= 0) {
+      r = read_all_direct(dfd, dst, n, (size_t)off);
+      ::close(dfd);
+    }
+  }
+  if (r == -3) r = read_all(fd, dst, n, (size_t)off);
+  ::close(fd);
+  if (r != 0) return set_error(RDKV_ERR_IO, "read %s [%llu, +%zu) failed", path, (unsigned long long)off, n);
+  return (int64_t)n;
 }
 
 int rdkv_drop_page_cache(const char* path) {

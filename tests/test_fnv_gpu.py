@@ -45,6 +45,21 @@ def test_random_buffers_match_serial(n):
     assert fnv1a64_device(dev[1:]) == oracle_fnv(host[1:].tobytes(), FNV_OFFSET)
 
 
+@pytest.mark.parametrize("n", [1, 16384, 16385, 5 * 16384 + 77, 1 << 20])
+def test_streaming_fnv_matches_one_shot(n):
+    """codec.StreamingFnv (the automaton pass per landed segment, then the rest) gives the
+    one-shot checksum whatever the segment boundaries (mid-chunk, repeated, past the end)."""
+    rng = np.random.default_rng(n + 1)
+    host = rng.integers(0, 256, n, dtype=np.uint8)
+    dev = torch.from_numpy(host).cuda()
+    want = oracle_fnv(host.tobytes(), FNV_OFFSET)
+    for steps in ([], [n // 3, n // 3, 2 * n // 3 + 1], [16383, 16384, 40000, n + 5]):
+        s = codec.StreamingFnv(dev)
+        for r in steps:
+            s.advance(r)
+        assert s.result() == want, (n, steps)
+
+
 def test_large_payload_matches_native():
     x = torch.randint(0, 256, (80 << 20,), dtype=torch.uint8, device="cuda")   # one C2 composite
     assert fnv1a64_device(x) == codec.fnv1a64(x.cpu())
