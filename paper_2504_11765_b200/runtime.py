@@ -76,7 +76,7 @@ class RuntimeConfig:
     # 8B composite of 5120 tokens reads in ~190 ms from a ~3.4 GB/s disk but prefills in
     # ~55 ms (bench ttft_ms.cold_disk vs full_prefill), so the reference rule loses there.
     cost_aware: bool = False
-    disk_gbps: float = 3.4              # sustained cold read of the shared store (bench / disk probe)
+    disk_gbps: float = 5.0              # cold O_DIRECT read of the shared store (scripts/micro/cold_path.py)
     prefill_s_per_token: float = 1.1e-5 # measured full-prefill cost per prefix token on this GPU
     # Decode after the first token (decode.py; the reference's decode_tokens, sim.py:572-573):
     # every query generates this many more tokens greedily; the instance batches them
