@@ -142,7 +142,7 @@ RDKV_API int rdkv_blob_read(const char* path, void* buf, size_t cap, size_t alig
 /* Read file bytes [off, off + len) into `dst` (the part of a blob file a
  * streamed disk hit has not read yet; store.read_blob_file overlaps each
  * segment's H2D copy with the next segment's read).  direct != 0: O_DIRECT,
- * `dst` and `off` 4096-aligned, `cap` >= len rounded up to 4096 (buffered
+ * `dst` and `off` 4096-aligned, `cap` >= the bytes read rounded up to 4096 (buffered
  * fallback where the file system refuses O_DIRECT).  Returns the bytes read
  * (short only at end of file), or < 0. */
 RDKV_API int64_t rdkv_file_read_range(const char* path, void* dst, size_t cap, uint64_t off, size_t len, int direct);

@@ -371,8 +371,6 @@ int rdkv_blob_read(const char* path, void* buf, size_t cap, size_t align, int ve
 int64_t rdkv_file_read_range(const char* path, void* dst, size_t cap, uint64_t off, size_t len, int direct) {
   constexpr size_t kBlk = 4096;
   if (!dst || len == 0) return set_error(RDKV_ERR_ARG, "read_range: empty request");
-  const size_t need = direct ? (len + kBlk - 1) / kBlk * kBlk : len;
-  if (cap < need) return set_error(RDKV_ERR_ARG, "read_range: buffer too small (%zu < %zu)", cap, need);
   if (direct && ((reinterpret_cast<uintptr_t>(dst) | off) % kBlk))
     return set_error(RDKV_ERR_ARG, "read_range: O_DIRECT needs a 4096-aligned buffer and offset");
   int fd = ::open(path, O_RDONLY | O_CLOEXEC);
@@ -387,6 +385,11 @@ int64_t rdkv_file_read_range(const char* path, void* dst, size_t cap, uint64_t o
     return 0;
   }
   const size_t n = std::min<uint64_t>(len, (uint64_t)st.st_size - off);
+  const size_t need = direct ? (n + kBlk - 1) / kBlk * kBlk : n;  // bytes written into dst
+  if (cap < need) {
+    ::close(fd);
+    return set_error(RDKV_ERR_ARG, "read_range: buffer too small (%zu < %zu)", cap, need);
+  }
   int r = -3;
   if (direct) {
     const int dfd = ::open(path, O_RDONLY | O_CLOEXEC | O_DIRECT);

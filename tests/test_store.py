@@ -183,3 +183,34 @@ def test_large_blob_file_roundtrip_parallel_read(tmp_path, monkeypatch, direct):
         look = store.get(key)
         assert look.outcome is Outcome.DISK_HIT
         assert look.blob == blob
+
+
+@pytest.mark.parametrize("direct", [0, 1])
+def test_file_read_range(tmp_path, direct):
+    """rdkv_file_read_range (the streamed disk hit's segment reader): exact bytes for
+    block-aligned ranges, short only at end of file, O_DIRECT alignment enforced."""
+    import ctypes as C
+
+    import numpy as np
+
+    from paper_2504_11765_b200 import _lib
+
+    data = np.random.default_rng(7).integers(0, 256, (5 << 20) + 1234, dtype=np.uint8)
+    path = tmp_path / "f.bin"
+    path.write_bytes(data.tobytes())
+    L = _lib.lib()
+    raw = np.zeros(len(data) + 3 * 4096, np.uint8)
+    base = (-raw.ctypes.data) % 4096
+    dst = raw.ctypes.data + base
+    cap = len(raw) - base
+    p = str(path).encode()
+    for off, n in ((0, 4096), (4096, 3 << 20), (2 << 20, len(data) - (2 << 20)), (4 << 20, 8 << 20)):
+        got = int(L.rdkv_file_read_range(p, C.c_void_p(dst), cap, off, n, direct))
+        want = min(n, len(data) - off)
+        assert got == want
+        assert np.array_equal(raw[base: base + got], data[off: off + got])
+    past = (len(data) + 4095) // 4096 * 4096 + 4096                                          # past the end
+    assert int(L.rdkv_file_read_range(p, C.c_void_p(dst), cap, past, 4096, direct)) == 0
+    if direct:
+        assert int(L.rdkv_file_read_range(p, C.c_void_p(dst + 1), cap - 1, 0, 4096, 1)) < 0    # unaligned buffer
+        assert int(L.rdkv_file_read_range(p, C.c_void_p(dst), cap, 100, 4096, 1)) < 0          # unaligned offset
