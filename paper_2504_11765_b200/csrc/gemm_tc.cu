@@ -444,7 +444,16 @@ struct PairCfg {
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE + 256;
 };
 
-template <int BN, int EPI, int DH>
+__device__ __forceinline__ int ld_acquire_flag(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_flag(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int BN, int EPI, int DH, bool SK = false>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
                          int N, int K, GemmEpi ep) {
@@ -468,6 +477,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int pair = (int)cluster_id_x(), npairs = (int)nclusters_x();
   const int m_tiles = (M + 255) / 256, n_tiles = (N + BN - 1) / BN;
   const int units = m_tiles * n_tiles, kblocks = K / BK;
+  // Work items: whole tiles round-robin over the pairs, or (SK, stream-K) equal shares of
+  // the unit-major k-block order, cut at tile boundaries into segments [kb0, kb1)
+  const long long W = (long long)units * kblocks;
+  auto share = [&](int p) { return W * p / npairs; };
+  auto for_segments = [&](auto&& fn) {  // fn(unit, kb0, kb1)
+    if constexpr (SK) {
+      const long long hi = share(pair + 1);
+      for (long long w = share(pair); w < hi;) {
+        const int u = (int)(w / kblocks), kb0 = (int)(w % kblocks);
+        const int kb1 = (int)min((long long)kblocks, kb0 + (hi - w));
+        fn(u, kb0, kb1);
+        w += kb1 - kb0;
+      }
+    } else {
+      for (int u = pair; u < units; u += npairs) fn(u, 0, kblocks);
+    }
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -500,12 +526,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       const int pf = ep.b_pf;
-      for (int u = pair; u < units; u += npairs) {
+      for_segments([&](int u, int kb0, int kb1) {
         const int mb = u % m_tiles, nb = u / m_tiles;
         // this CTA's half of B, k-blocks kb with kb % m_tiles == mb (the M tiles sharing the
         // B tile split the prefetch stream)
         auto prefetch_b = [&](int kb) {
-          if (kb >= kblocks || kb % m_tiles != mb) return;
+          if (kb >= kb1 || kb % m_tiles != mb) return;
           if constexpr (BN == 384) {
             tma_prefetch_2d(&tmB, kb * BK, nb * BN + (int)rank * 128);
             tma_prefetch_2d(&tmB, kb * BK, nb * BN + (int)rank * 128 + 64);
@@ -515,8 +541,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         };
         if (pf > 0)
-          for (int kb = 0; kb < pf; ++kb) prefetch_b(kb);
-        for (int kb = 0; kb < kblocks; ++kb) {
+          for (int kb = kb0; kb < kb0 + pf; ++kb) prefetch_b(kb);
+        for (int kb = kb0; kb < kb1; ++kb) {
           if (pf > 0) prefetch_b(kb + pf);
           mbar_wait(&empty[stage], phase ^ 1);
           if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * STAGE);
@@ -537,7 +563,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             phase ^= 1;
           }
         }
-      }
+      });
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
@@ -546,22 +572,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       constexpr uint32_t idesc2 = idesc_bf16_f32(256, 128);
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
-      for (int u = pair; u < units; u += npairs) {
+      for_segments([&](int, int kb0, int kb1) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t ad = sdesc_k_sw128(smem_u32(sA + stage * A_BYTES));
           const uint64_t bd = sdesc_k_sw128(smem_u32(sB + stage * B_BYTES));
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) umma_bf16_2sm(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16_2sm(d, ad + 2 * k, bd + 2 * k, idesc, ((kb - kb0) | k) != 0 ? 1u : 0u);
           if constexpr (BN == 384) {
             const uint64_t bd2 = sdesc_k_sw128(smem_u32(sB + stage * B_BYTES + 128 * 128));
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
-              umma_bf16_2sm(d + 256, ad + 2 * k, bd2 + 2 * k, idesc2, (kb | k) != 0 ? 1u : 0u);
+              umma_bf16_2sm(d + 256, ad + 2 * k, bd2 + 2 * k, idesc2, ((kb - kb0) | k) != 0 ? 1u : 0u);
           }
           umma_commit_2sm(&empty[stage], 0x3);
           if (++stage == STAGES) {
@@ -572,7 +599,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         umma_commit_2sm(&tfull[acc], 0x3);
         if (NACC == 2) acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
-      }
+      });
     }
   } else if (warp == 3) {
     // idle warp: pull the next kernel's weights into L2 while this GEMM computes
@@ -582,21 +609,78 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 0), tempty1 = mapa_shared(smem_u32(&tempty[1]), 0);
-    for (int u = pair; u < units; u += npairs) {
+    const int half = (warp - 4) >> 2;
+    auto epi_bar = [&]() { asm volatile("bar.sync 2, 256;" ::: "memory"); };  // the 8 epilogue warps
+    for_segments([&](int u, int kb0, int kb1) {
       const int mb = u % m_tiles, nb = u / m_tiles;
       const int row = mb * 256 + (int)rank * 128 + wq * 32 + lane;
-      const float rs = epi_rscale<EPI>(ep, row, M);  // overlaps this tile's MMAs
+      const float rs = kb0 == 0 ? epi_rscale<EPI>(ep, row, M) : 1.f;  // overlaps this tile's MMAs
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(wq * 32) << 16);
-      epilogue_rows<BN, EPI, DH>(taddr, row, nb, 0, M, N, ep, (warp - 4) >> 2, rs);
+      if constexpr (SK) {
+        // partial tiles: [BN/4][128 rows][4] fp32 per (pair, CTA) slot, so a warp's float4
+        // accesses of one column group cover 512 contiguous bytes
+        auto slot = [&](int p) {
+          return reinterpret_cast<float4*>(ep.sk_part + (size_t)(p * 2 + (int)rank) * 128 * BN) + wq * 32 + lane;
+        };
+        if (kb0 > 0) {  // a later part of a tile whose first k-blocks another pair holds
+          float4* dst = slot(pair);
+#pragma unroll 1
+          for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
+            uint32_t r[32];
+            tmem_ld32(taddr + c * 32, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              dst[(c * 8 + e) * 128] = make_float4(__uint_as_float(r[4 * e]), __uint_as_float(r[4 * e + 1]),
+                                                   __uint_as_float(r[4 * e + 2]), __uint_as_float(r[4 * e + 3]));
+          }
+          __threadfence();
+          epi_bar();
+          if (warp == 4 && lane == 0) st_release_flag(ep.sk_flag + pair * 2 + (int)rank, 1);
+        } else if (kb1 < kblocks) {  // the tile's first k-blocks: add the later pairs' parts
+          const long long uend = (long long)(u + 1) * kblocks;
+          for (int q = pair + 1; q < npairs && share(q) < uend; ++q) {
+            if (lane == 0) {
+              long long spins = 0;
+              while (ld_acquire_flag(ep.sk_flag + q * 2 + (int)rank) == 0)
+                if (++spins > (1ll << 31)) __trap();
+            }
+            __syncwarp();
+            const float4* src = slot(q);
+#pragma unroll 1
+            for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
+              uint32_t r[32];
+              tmem_ld32(taddr + c * 32, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const float4 t = __ldcg(src + (c * 8 + e) * 128);
+                r[4 * e] = __float_as_uint(__uint_as_float(r[4 * e]) + t.x);
+                r[4 * e + 1] = __float_as_uint(__uint_as_float(r[4 * e + 1]) + t.y);
+                r[4 * e + 2] = __float_as_uint(__uint_as_float(r[4 * e + 2]) + t.z);
+                r[4 * e + 3] = __float_as_uint(__uint_as_float(r[4 * e + 3]) + t.w);
+              }
+              tmem_st32(taddr + c * 32, r);
+            }
+          }
+          tmem_st_wait();
+          tc_fence_before();
+          epi_bar();  // every column of the summed tile is in TMEM before any epilogue reads it
+          tc_fence_after();
+          if (warp == 4 && lane == 0)  // consumed: re-arm the parts' flags for the next launch
+            for (int q = pair + 1; q < npairs && share(q) < uend; ++q) ep.sk_flag[q * 2 + (int)rank] = 0;
+        }
+      }
+      if (kb0 == 0) epilogue_rows<BN, EPI, DH>(taddr, row, nb, 0, M, N, ep, half, rs);
       if constexpr (EPI == EPI_PUSH) __threadfence_system();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(acc ? tempty1 : tempty0);
       if (NACC == 2) acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
-    }
+    });
   }
   __syncthreads();
   cluster_sync();  // the leader's MMAs into this CTA's TMEM / smem are complete
@@ -606,11 +690,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
-template <int BN, int EPI, int DH>
+template <int BN, int EPI, int DH, bool SK = false>
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const GemmEpi& ep,
-                cudaStream_t stream) {
+                cudaStream_t stream, int sk_pairs = 0) {
   constexpr size_t SMEM = PairCfg<BN>::SMEM;
-  auto kern = gemm_bf16_tc2_kernel<BN, EPI, DH>;
+  auto kern = gemm_bf16_tc2_kernel<BN, EPI, DH, SK>;
   static bool attr_set = false;
   if (!attr_set) {
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
@@ -618,7 +702,8 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int 
   }
   const int units = ((M + 255) / 256) * ((N + BN - 1) / BN);
   const int max_pairs = num_sms() / 2;
-  const int pairs = units < max_pairs ? units : max_pairs;
+  // stream-K: every pair co-resident (a split tile's first pair waits for the later ones)
+  const int pairs = SK ? sk_pairs : units < max_pairs ? units : max_pairs;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(GEMM_THREADS);
@@ -1292,6 +1377,22 @@ size_t splitk_scratch_bytes(int M, int N, int K) {
   return sp.nt > 0 ? (size_t)sp.splits * M * N * sizeof(float) : 0;
 }
 
+// RDKV_GEMM_SK: stream-K for the CTA-pair GEMM — 1: only grids that leave pairs idle
+// (single-wave projections at M = 1024: 64 tiles on 74 pairs), 2: any grid whose last
+// round is partial.  0 (default): whole tiles.
+int gemm_sk_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("RDKV_GEMM_SK");
+    return e ? std::atoi(e) : 0;
+  }();
+  return m;
+}
+
+size_t gemm_sk_scratch_bytes() {
+  const size_t slots = (size_t)num_sms();  // two per pair
+  return slots * 128 * 384 * sizeof(float) + slots * sizeof(int);
+}
+
 namespace {
 
 // Sum `splits` fp32 partial slabs and apply the requested epilogue.
@@ -1386,6 +1487,50 @@ int dispatch(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long
   }
 }
 
+// Co-resident 2-CTA clusters of the pair kernel (all of them must be, for stream-K).
+template <int BN, int EPI, int DH>
+int sk_resident_pairs() {
+  static int n = -1;
+  if (n < 0) {
+    auto kern = gemm_bf16_tc2_kernel<BN, EPI, DH, true>;
+    constexpr size_t SMEM = PairCfg<BN>::SMEM;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0) != cudaSuccess) {
+      n = 0;
+      return n;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(num_sms());
+    cfg.blockDim = dim3(GEMM_THREADS);
+    cfg.dynamicSmemBytes = SMEM;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int c = 0;
+    n = cudaOccupancyMaxActiveClusters(&c, kern, &cfg) == cudaSuccess ? std::min(c, num_sms() / 2) : 0;
+    cudaGetLastError();
+  }
+  return n;
+}
+
+template <int BN, int EPI, int DH>
+int launch_pair_auto(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const GemmEpi& ep,
+                     cudaStream_t stream) {
+  const int mode = gemm_sk_mode();
+  if (mode > 0 && EPI != EPI_PUSH && ep.sk_part && ep.sk_flag) {
+    const int units = ((M + 255) / 256) * ((N + BN - 1) / BN), kblocks = K / BK;
+    const int P = sk_resident_pairs<BN, EPI, DH>();
+    const bool partial = P > 0 && units % P != 0 && (mode >= 2 || units < P);
+    if (partial && (long long)units * kblocks >= 8ll * P && 2 * P <= ep.sk_slots)
+      return launch_pair<BN, EPI, DH, true>(ta, tb, M, N, K, ep, stream, P);
+  }
+  return launch_pair<BN, EPI, DH>(ta, tb, M, N, K, ep, stream);
+}
+
 template <int BN>
 int dispatch_pair(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long long ldb, int M, int N, int K,
                   int kind, int dh, const GemmEpi& ep, cudaStream_t stream) {
@@ -1393,17 +1538,17 @@ int dispatch_pair(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B,
   RDKV_TRY(make_tmap(&ta, A, M, K, lda, 128));
   RDKV_TRY(make_tmap(&tb, B, N, K, ldb, BN == 384 ? 64 : BN / 2));
   switch (kind) {
-    case EPI_STORE: return launch_pair<BN, EPI_STORE, 0>(ta, tb, M, N, K, ep, stream);
-    case EPI_STORE_F32: return launch_pair<BN, EPI_STORE_F32, 0>(ta, tb, M, N, K, ep, stream);
-    case EPI_RESID: return launch_pair<BN, EPI_RESID, 0>(ta, tb, M, N, K, ep, stream);
+    case EPI_STORE: return launch_pair_auto<BN, EPI_STORE, 0>(ta, tb, M, N, K, ep, stream);
+    case EPI_STORE_F32: return launch_pair_auto<BN, EPI_STORE_F32, 0>(ta, tb, M, N, K, ep, stream);
+    case EPI_RESID: return launch_pair_auto<BN, EPI_RESID, 0>(ta, tb, M, N, K, ep, stream);
     case EPI_SWIGLU:
-      if constexpr (BN % 128 == 0) return launch_pair<BN, EPI_SWIGLU, 0>(ta, tb, M, N, K, ep, stream);
+      if constexpr (BN % 128 == 0) return launch_pair_auto<BN, EPI_SWIGLU, 0>(ta, tb, M, N, K, ep, stream);
       return set_error(RDKV_ERR_ARG, "swiglu: tile N %d must hold whole gate/up block pairs", BN);
     case EPI_PUSH: return launch_pair<BN, EPI_PUSH, 0>(ta, tb, M, N, K, ep, stream);
     case EPI_QKV:
-      if (dh == 64) return launch_pair<BN, EPI_QKV, 64>(ta, tb, M, N, K, ep, stream);
+      if (dh == 64) return launch_pair_auto<BN, EPI_QKV, 64>(ta, tb, M, N, K, ep, stream);
       if constexpr (BN % 128 == 0)
-        if (dh == 128) return launch_pair<BN, EPI_QKV, 128>(ta, tb, M, N, K, ep, stream);
+        if (dh == 128) return launch_pair_auto<BN, EPI_QKV, 128>(ta, tb, M, N, K, ep, stream);
       return set_error(RDKV_ERR_ARG, "qkv: head_dim %d unsupported with tile N %d", dh, BN);
     default: return set_error(RDKV_ERR_ARG, "gemm: unknown epilogue %d", kind);
   }

@@ -82,7 +82,18 @@ struct GemmEpi {
   // Null = the split-K partials go through a separate finalize kernel.
   int* counters;
   int n_counters;
+  // Large-M stream-K (CTA-pair GEMM): fp32 partial tiles [2 per pair][128 rows][tile N]
+  // and one release flag per slot, zero before the launch and left zero by it (the pair
+  // holding a split tile's first k-block adds the later pairs' partials).  Null = off.
+  float* sk_part;
+  int* sk_flag;
+  int sk_slots;
 };
+
+// Bytes of stream-K scratch (partials + flags) for the CTA-pair GEMM on this GPU, and the
+// RDKV_GEMM_SK mode (0 off, 1 grids leaving pairs idle, 2 any partial last round).
+size_t gemm_sk_scratch_bytes();
+int gemm_sk_mode();
 
 // True when launch_gemm will take the split-K path for this shape (small M).
 bool gemm_splits(int M, int N, int K, size_t splitk_bytes);

@@ -94,6 +94,7 @@ struct Ws {
   void* attn_split;
   size_t attn_split_bytes;
   void* attn_sk;  // stream-K attention partials + flags (num_sms() CTAs)
+  void* gemm_sk;  // stream-K CTA-pair GEMM partials + flags (RDKV_GEMM_SK; large M only)
   void* argmax;
   int* counters;  // fused small-M split-K tickets (zeroed at the start of every forward)
 };
@@ -121,6 +122,8 @@ size_t ws_layout(const rdkv_model_desc& d, int T, int S, Ws* ws, void* base) {
   const size_t ask = attention_split_scratch_bytes(T, d.n_heads, d.head_dim);
   const size_t oask = take(ask);
   const size_t osk_attn = take(attention_sk_scratch_bytes(num_sms(), d.head_dim));
+  const size_t gsk = T >= 256 && gemm_sk_mode() > 0 ? gemm_sk_scratch_bytes() : 0;
+  const size_t ogsk = take(gsk);
   const size_t oam = take(argmax_scratch_bytes(S));
   const size_t ossq = take((size_t)(d.hidden / 32) * T * sizeof(float));
   const size_t octr = take((size_t)N_SPLITK_COUNTERS * sizeof(int));
@@ -131,6 +134,7 @@ size_t ws_layout(const rdkv_model_desc& d, int T, int S, Ws* ws, void* base) {
     ws->attn_split = ask ? static_cast<uint8_t*>(base) + oask : nullptr;
     ws->attn_split_bytes = ask;
     ws->attn_sk = static_cast<uint8_t*>(base) + osk_attn;
+    ws->gemm_sk = gsk ? static_cast<uint8_t*>(base) + ogsk : nullptr;
     ws->splitk = sk ? static_cast<uint8_t*>(base) + osk : nullptr;
     ws->splitk_bytes = sk;
     auto* b = static_cast<uint8_t*>(base);
@@ -258,7 +262,20 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     ws.attn_split = nullptr;
     ws.attn_split_bytes = 0;
     ws.attn_sk = nullptr;
+    ws.gemm_sk = nullptr;
   }
+  float* gsk_part = nullptr;
+  int* gsk_flag = nullptr;
+  if (ws.gemm_sk) {  // GEMM stream-K flags start at zero (every launch leaves them zero)
+    gsk_part = static_cast<float*>(ws.gemm_sk);
+    gsk_flag = reinterpret_cast<int*>(gsk_part + (size_t)num_sms() * 128 * 384);
+    CUDA_TRY(cudaMemsetAsync(gsk_flag, 0, (size_t)num_sms() * sizeof(int), st));
+  }
+  auto set_sk = [&](GemmEpi& e) {
+    e.sk_part = gsk_part;
+    e.sk_flag = gsk_flag;
+    e.sk_slots = num_sms();
+  };
   if (ws.attn_sk) {  // stream-K flags start at zero (every launch leaves them zero)
     AttnParams z{};
     attention_sk_carve(z, ws.attn_sk, num_sms(), dh);
@@ -315,6 +332,7 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     eq.n_counters = N_SPLITK_COUNTERS;
     eq.splitk_ws = ws.splitk;  // small M: split-K (the finalize handles the norm statistics)
     eq.splitk_bytes = ws.splitk_bytes;
+    set_sk(eq);
     if (ssq_path) {
       eq.ssq_in = ws.ssq;
       eq.ssq_parts = d.hidden / 32;
@@ -398,6 +416,7 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     er.n_counters = N_SPLITK_COUNTERS;
     er.splitk_ws = ws.splitk;  // small M: split-K (the finalize handles the norm statistics)
     er.splitk_bytes = ws.splitk_bytes;
+    set_sk(er);
     er.out = ws.x;
     er.ldo = d.hidden;
     er.resid = ws.x;
@@ -424,6 +443,7 @@ int rdkv_forward(rdkv_model* m, const rdkv_batch* b, void* ws_base, size_t ws_by
     eg.n_counters = N_SPLITK_COUNTERS;
     eg.splitk_ws = ws.splitk;  // small M: split-K (the finalize handles the norm statistics)
     eg.splitk_bytes = ws.splitk_bytes;
+    set_sk(eg);
     eg.out = ws.a;
     eg.ldo = d.ffn;
     if (ssq_path) {
