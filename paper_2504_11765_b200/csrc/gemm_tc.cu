@@ -479,10 +479,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int units = m_tiles * n_tiles, kblocks = K / BK;
   // Work items: whole tiles round-robin over the pairs, or (SK, stream-K) equal shares of
   // the unit-major k-block order, cut at tile boundaries into segments [kb0, kb1)
-  const long long W = (long long)units * kblocks;
-  auto share = [&](int p) { return W * p / npairs; };
+  // (hybrid: the first sk_dp units whole and round-robin, then the k-blocks of the rest
+  // shared by the first sk_tp pairs)
+  const int sk_dp = SK ? ep.sk_dp : 0, sk_tp = SK ? ep.sk_tp : npairs;
+  const long long W0 = (long long)sk_dp * kblocks, W = (long long)units * kblocks - W0;
+  auto share = [&](int p) { return W0 + W * min(p, sk_tp) / sk_tp; };
   auto for_segments = [&](auto&& fn) {  // fn(unit, kb0, kb1)
     if constexpr (SK) {
+      for (int u = pair; u < sk_dp; u += npairs) fn(u, 0, kblocks);
       const long long hi = share(pair + 1);
       for (long long w = share(pair); w < hi;) {
         const int u = (int)(w / kblocks), kb0 = (int)(w % kblocks);
@@ -1379,7 +1383,8 @@ size_t splitk_scratch_bytes(int M, int N, int K) {
 
 // RDKV_GEMM_SK: stream-K for the CTA-pair GEMM — 1: only grids that leave pairs idle
 // (single-wave projections at M = 1024: 64 tiles on 74 pairs), 2: any grid whose last
-// round is partial.  0 (default): whole tiles.
+// round is partial, 3: whole tiles for the full rounds and only the partial last round's
+// tiles split in k (gate/up at M = 1024: 448 tiles = 6 x 74 + 4).  0 (default): whole tiles.
 int gemm_sk_mode() {
   static const int m = [] {
     const char* e = std::getenv("RDKV_GEMM_SK");
@@ -1525,8 +1530,27 @@ int launch_pair_auto(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N,
     const int units = ((M + 255) / 256) * ((N + BN - 1) / BN), kblocks = K / BK;
     const int P = sk_resident_pairs<BN, EPI, DH>();
     const bool partial = P > 0 && units % P != 0 && (mode >= 2 || units < P);
-    if (partial && (long long)units * kblocks >= 8ll * P && 2 * P <= ep.sk_slots)
-      return launch_pair<BN, EPI, DH, true>(ta, tb, M, N, K, ep, stream, P);
+    if (mode == 3) {
+      // whole tiles for the full rounds; the last round's `tail` tiles each split in k over
+      // s pairs (s - 1 fp32 partial tiles added by the first), so the round costs ~1/s
+      const int tail = P > 0 ? units % P : 0;
+      static const int smax = [] {
+        const char* e = std::getenv("RDKV_GEMM_SK_SPLIT");
+        return e ? std::max(1, std::atoi(e)) : 4;
+      }();
+      const int s = tail ? std::min(smax, P / tail) : 0;
+      if (units > P && s >= 2 && kblocks >= 4 * s && 2 * P <= ep.sk_slots) {
+        GemmEpi e = ep;
+        e.sk_dp = units - tail;
+        e.sk_tp = tail * s;
+        return launch_pair<BN, EPI, DH, true>(ta, tb, M, N, K, e, stream, P);
+      }
+    } else if (partial && (long long)units * kblocks >= 8ll * P && 2 * P <= ep.sk_slots) {
+      GemmEpi e = ep;
+      e.sk_dp = 0;
+      e.sk_tp = P;
+      return launch_pair<BN, EPI, DH, true>(ta, tb, M, N, K, e, stream, P);
+    }
   }
   return launch_pair<BN, EPI, DH>(ta, tb, M, N, K, ep, stream);
 }

@@ -88,10 +88,17 @@ struct GemmEpi {
   float* sk_part;
   int* sk_flag;
   int sk_slots;
+  // Which units the stream-K launch splits: the first sk_dp tiles run whole, round-robin
+  // over the pairs; the k-blocks of the rest are shared equally by the first sk_tp pairs
+  // (pure stream-K: sk_dp = 0, sk_tp = every pair; the DP + split-tail hybrid: sk_dp =
+  // the full rounds, sk_tp = tail tiles x split).  Set by the launcher.
+  int sk_dp;
+  int sk_tp;
 };
 
 // Bytes of stream-K scratch (partials + flags) for the CTA-pair GEMM on this GPU, and the
-// RDKV_GEMM_SK mode (0 off, 1 grids leaving pairs idle, 2 any partial last round).
+// RDKV_GEMM_SK mode (0 off, 1 grids leaving pairs idle, 2 any partial last round,
+// 3 whole tiles for the full rounds + the partial last round's tiles split in k).
 size_t gemm_sk_scratch_bytes();
 int gemm_sk_mode();
 

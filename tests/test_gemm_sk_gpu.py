@@ -1,0 +1,33 @@
+"""Stream-K modes of the CTA-pair GEMM (RDKV_GEMM_SK, csrc/gemm_tc.cu launch_pair_auto)
+against whole tiles on a 16-query C2 batch (M = 1024: gate/up = 256 tiles on 74 pairs, a
+partial last round).  Split tiles only reorder the fp32 k-sum, so the logits agree to
+fp32/bf16 rounding (rel err <= 2e-3) and the first tokens are identical."""
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _logits(tmp_path, mode):
+    out = tmp_path / f"sk{mode}.npy"
+    env = dict(os.environ, RDKV_GEMM_SK=str(mode))
+    res = subprocess.run([sys.executable, str(ROOT / "scripts" / "sk_logits.py"), str(out)], cwd=ROOT, env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-3000:]
+    return np.load(out)
+
+
+@pytest.mark.parametrize("mode", [2, 3])
+def test_stream_k_modes_match_whole_tiles(tmp_path, mode):
+    base, got = _logits(tmp_path, 0), _logits(tmp_path, mode)
+    assert base.shape == got.shape == (16, base.shape[1])
+    err = np.abs(got - base).max() / np.abs(base).max()
+    assert err <= 2e-3, f"rel err {err:.3e}"
+    assert (got.argmax(1) == base.argmax(1)).all()
