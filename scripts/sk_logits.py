@@ -3,9 +3,12 @@ the HBM tier) -> argv[1] (.npy).  tests/test_gemm_sk_gpu.py runs it under each
 RDKV_GEMM_SK mode (read once per process) and compares the modes."""
 
 import sys
+from pathlib import Path
 
 import numpy as np
 import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 from paper_2504_11765_b200.engine import Engine
 from paper_2504_11765_b200.generator import KvGenerator

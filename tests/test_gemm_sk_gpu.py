@@ -24,9 +24,14 @@ def _logits(tmp_path, mode):
     return np.load(out)
 
 
+@pytest.fixture(scope="module")
+def whole_tiles(tmp_path_factory):
+    return _logits(tmp_path_factory.mktemp("sk"), 0)
+
+
 @pytest.mark.parametrize("mode", [2, 3])
-def test_stream_k_modes_match_whole_tiles(tmp_path, mode):
-    base, got = _logits(tmp_path, 0), _logits(tmp_path, mode)
+def test_stream_k_modes_match_whole_tiles(tmp_path, whole_tiles, mode):
+    base, got = whole_tiles, _logits(tmp_path, mode)
     assert base.shape == got.shape == (16, base.shape[1])
     err = np.abs(got - base).max() / np.abs(base).max()
     assert err <= 2e-3, f"rel err {err:.3e}"
