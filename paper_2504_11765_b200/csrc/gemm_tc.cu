@@ -453,7 +453,7 @@ __device__ __forceinline__ void st_release_flag(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <int BN, int EPI, int DH, bool SK = false>
+template <int BN, int EPI, int DH, bool SK = false, bool MC = false>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
                          int N, int K, GemmEpi ep) {
@@ -473,8 +473,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
-  const int pair = (int)cluster_id_x(), npairs = (int)nclusters_x();
+  // MC: clusters of two CTA pairs that own M tiles 2j, 2j + 1 of the same B tile; each CTA
+  // loads half of its B rows and multicasts them to its counterpart in the other pair
+  const uint32_t crank = cluster_ctarank();
+  const uint32_t rank = crank & 1u, grp = MC ? crank >> 1 : 0u, lead = crank & ~1u;
+  const int pair = MC ? (int)cluster_id_x() * 2 + (int)grp : (int)cluster_id_x();
+  const int npairs = MC ? 2 * (int)nclusters_x() : (int)nclusters_x();
   const int m_tiles = (M + 255) / 256, n_tiles = (N + BN - 1) / BN;
   const int units = m_tiles * n_tiles, kblocks = K / BK;
   // Work items: whole tiles round-robin over the pairs, or (SK, stream-K) equal shares of
@@ -494,6 +498,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         fn(u, kb0, kb1);
         w += kb1 - kb0;
       }
+    } else if constexpr (MC) {
+      for (int j = (int)cluster_id_x(); j < units / 2; j += (int)nclusters_x()) fn(2 * j + (int)grp, 0, kblocks);
     } else {
       for (int u = pair; u < units; u += npairs) fn(u, 0, kblocks);
     }
@@ -506,7 +512,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC ? 2 : 1);  // MC: both pairs' MMAs read the multicast B
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -550,7 +556,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (pf > 0) prefetch_b(kb + pf);
           mbar_wait(&empty[stage], phase ^ 1);
           if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * STAGE);
-          const uint32_t bar = mapa_shared(smem_u32(&full[stage]), 0);
+          const uint32_t bar = mapa_shared(smem_u32(&full[stage]), lead);
           tma_load_2d_2sm(&tmA, bar, sA + stage * A_BYTES, kb * BK, mb * 256 + (int)rank * 128, pol_act);
           if constexpr (BN == 384) {
             // each CTA holds its N-half of both MMAs: rows [128 r, +128) of the N = 256 one and
@@ -559,6 +565,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             tma_load_2d_2sm(&tmB, bar, b, kb * BK, nb * BN + (int)rank * 128, pol_w);
             tma_load_2d_2sm(&tmB, bar, b + 64 * 128, kb * BK, nb * BN + (int)rank * 128 + 64, pol_w);
             tma_load_2d_2sm(&tmB, bar, b + 128 * 128, kb * BK, nb * BN + 256 + (int)rank * 64, pol_w);
+          } else if constexpr (MC) {
+            tma_load_2d_2sm_mc(&tmB, bar, sB + stage * B_BYTES + grp * (BN / 4) * 128, kb * BK,
+                               nb * BN + (int)rank * (BN / 2) + (int)grp * (BN / 4), (uint16_t)(0x5u << rank), pol_w);
           } else {
             tma_load_2d_2sm(&tmB, bar, sB + stage * B_BYTES, kb * BK, nb * BN + (int)rank * (BN / 2), pol_w);
           }
@@ -594,13 +603,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             for (int k = 0; k < BK / 16; ++k)
               umma_bf16_2sm(d + 256, ad + 2 * k, bd2 + 2 * k, idesc2, ((kb - kb0) | k) != 0 ? 1u : 0u);
           }
-          umma_commit_2sm(&empty[stage], 0x3);
+          umma_commit_2sm(&empty[stage], MC ? 0xF : 0x3);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit_2sm(&tfull[acc], 0x3);
+        umma_commit_2sm(&tfull[acc], (uint16_t)(0x3u << (2 * grp)));
         if (NACC == 2) acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       });
@@ -612,7 +621,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int wq = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
-    const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 0), tempty1 = mapa_shared(smem_u32(&tempty[1]), 0);
+    const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), lead), tempty1 = mapa_shared(smem_u32(&tempty[1]), lead);
     const int half = (warp - 4) >> 2;
     auto epi_bar = [&]() { asm volatile("bar.sync 2, 256;" ::: "memory"); };  // the 8 epilogue warps
     for_segments([&](int u, int kb0, int kb1) {
@@ -694,11 +703,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
-template <int BN, int EPI, int DH, bool SK = false>
+template <int BN, int EPI, int DH, bool SK = false, bool MC = false>
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const GemmEpi& ep,
                 cudaStream_t stream, int sk_pairs = 0) {
   constexpr size_t SMEM = PairCfg<BN>::SMEM;
-  auto kern = gemm_bf16_tc2_kernel<BN, EPI, DH, SK>;
+  auto kern = gemm_bf16_tc2_kernel<BN, EPI, DH, SK, MC>;
   static bool attr_set = false;
   if (!attr_set) {
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
@@ -707,7 +716,30 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int 
   const int units = ((M + 255) / 256) * ((N + BN - 1) / BN);
   const int max_pairs = num_sms() / 2;
   // stream-K: every pair co-resident (a split tile's first pair waits for the later ones)
-  const int pairs = SK ? sk_pairs : units < max_pairs ? units : max_pairs;
+  int pairs = SK ? sk_pairs : units < max_pairs ? units : max_pairs;
+  if constexpr (MC) {
+    // clusters of two pairs, one M-tile couple each; a persistent grid only as large as the
+    // 4-CTA clusters that fit at once (GPCs whose SM count is not a multiple of 4 hold fewer)
+    static int fit = -1;
+    if (fit < 0) {
+      cudaLaunchConfig_t q{};
+      q.gridDim = dim3(num_sms());
+      q.blockDim = dim3(GEMM_THREADS);
+      q.dynamicSmemBytes = SMEM;
+      cudaLaunchAttribute a{};
+      a.id = cudaLaunchAttributeClusterDimension;
+      a.val.clusterDim.x = 4;
+      a.val.clusterDim.y = 1;
+      a.val.clusterDim.z = 1;
+      q.attrs = &a;
+      q.numAttrs = 1;
+      int c = 0;
+      fit = cudaOccupancyMaxActiveClusters(&c, kern, &q) == cudaSuccess && c > 0 ? std::min(c, num_sms() / 4) : 1;
+      cudaGetLastError();
+      if (std::getenv("RDKV_GEMM_MC_VERBOSE")) std::fprintf(stderr, "rdkv: %d 4-CTA clusters fit\n", fit);
+    }
+    pairs = std::min(units, 2 * fit) & ~1;
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(GEMM_THREADS);
@@ -715,7 +747,7 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int 
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = MC ? 4 : 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1522,9 +1554,28 @@ int sk_resident_pairs() {
   return n;
 }
 
+// RDKV_GEMM_MC: B-tile TMA multicast across two CTA pairs (clusters of 4) for 256 x 256 pair
+// tiles with an even number of M tiles — 1: every such grid, 2: only multi-wave grids, 3: only
+// single-wave grids (units <= the pairs).  0: off.
+int gemm_mc_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("RDKV_GEMM_MC");
+    return e ? std::atoi(e) : 0;
+  }();
+  return m;
+}
+template <int BN>
+bool use_mc(int M, int N, int kind) {
+  const int mode = gemm_mc_mode(), m_tiles = (M + 255) / 256, units = m_tiles * ((N + BN - 1) / BN);
+  const bool multi = units > num_sms() / 2;
+  return BN == 256 && mode > 0 && kind != EPI_PUSH && m_tiles % 2 == 0 && (mode == 1 || (mode == 2) == multi);
+}
+
 template <int BN, int EPI, int DH>
 int launch_pair_auto(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const GemmEpi& ep,
                      cudaStream_t stream) {
+  if constexpr (BN == 256)
+    if (use_mc<BN>(M, N, EPI)) return launch_pair<BN, EPI, DH, false, true>(ta, tb, M, N, K, ep, stream);
   const int mode = gemm_sk_mode();
   if (mode > 0 && EPI != EPI_PUSH && ep.sk_part && ep.sk_flag) {
     const int units = ((M + 255) / 256) * ((N + BN - 1) / BN), kblocks = K / BK;
@@ -1560,7 +1611,7 @@ int dispatch_pair(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B,
                   int kind, int dh, const GemmEpi& ep, cudaStream_t stream) {
   CUtensorMap ta, tb;
   RDKV_TRY(make_tmap(&ta, A, M, K, lda, 128));
-  RDKV_TRY(make_tmap(&tb, B, N, K, ldb, BN == 384 ? 64 : BN / 2));
+  RDKV_TRY(make_tmap(&tb, B, N, K, ldb, BN == 384 ? 64 : use_mc<BN>(M, N, kind) ? BN / 4 : BN / 2));
   switch (kind) {
     case EPI_STORE: return launch_pair_auto<BN, EPI_STORE, 0>(ta, tb, M, N, K, ep, stream);
     case EPI_STORE_F32: return launch_pair_auto<BN, EPI_STORE_F32, 0>(ta, tb, M, N, K, ep, stream);

@@ -368,6 +368,16 @@ __device__ __forceinline__ void tma_load_2d_2sm(const CUtensorMap* m, uint32_t b
       "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
 }
+// 2-SM TMA multicast: the box lands at the same smem offset in every CTA of `mask`;
+// each destination's bytes are counted on its own pair leader's mbarrier.
+__device__ __forceinline__ void tma_load_2d_2sm_mc(const CUtensorMap* m, uint32_t bar_cluster, void* dst, int c0,
+                                                   int c1, uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1), "h"(mask), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_alloc_2sm(uint32_t* dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
                "r"(ncols)
