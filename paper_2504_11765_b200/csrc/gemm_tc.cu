@@ -1556,11 +1556,12 @@ int sk_resident_pairs() {
 
 // RDKV_GEMM_MC: B-tile TMA multicast across two CTA pairs (clusters of 4) for 256 x 256 pair
 // tiles with an even number of M tiles — 1: every such grid, 2: only multi-wave grids, 3: only
-// single-wave grids (units <= the pairs).  0: off.
+// single-wave grids (units <= the pairs).  0: off.  Default 2 (C3 step, 5 interleaved pairs:
+// gate/up -3%, 1034 vs 1023 q/s, profiles/r2s4_gemm_mc_ab.txt).
 int gemm_mc_mode() {
   static const int m = [] {
     const char* e = std::getenv("RDKV_GEMM_MC");
-    return e ? std::atoi(e) : 0;
+    return e ? std::atoi(e) : 2;
   }();
   return m;
 }
